@@ -1,0 +1,328 @@
+"""Benchmark: C_W assembly covariance pairs/s and FP64 TFLOP/s (BASELINE.json metric).
+
+A step is one pass of the whole hot path on one synthetic input of the workload (SURVEY.md
+section 8(a) rows a1-a7): mlk_build_tree -> mlk_build_basis -> mlk_assemble_cw (admission,
+fused tiles, W_a contraction, NCCL all-gather of the BSR shards when N > 1) -> mlk_cw_matvec
+EXACT (allreduce when N > 1).  value = covariance pairs (sum over admitted blocks |a||b|)
+processed per second of step time (max over ranks), device-resident inputs.  e2e = the same
+metric through the same public API with host (pinned) inputs and the BSR values + C_W v read
+back to host inside the timed region.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl reference]
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as wl  # noqa: E402
+
+PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "k5a_traffic_r01.json")
+
+
+def fp64_peak():
+    d = json.load(open(PEAK_FILE))
+    return float(max(d["fp64_peak_tflops_dmma"], d["fp64_peak_tflops_dfma"]))
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + q,
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.1)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i]
+                          and "Not" not in s[2 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return ws, rank, local
+
+
+# --------------------------------------------------------------------------- reference arm
+def oracle_sample(cfg_name, budget_s, seed_tag=0):
+    """The oracle (as it stands) on a bounded, seeded sample of the workload's admitted blocks.
+    Returns (pairs/s, description, cores)."""
+    from oracle import admission as OA
+    from oracle import assemble as OAs
+    from oracle import basis as OB
+    from oracle import tree as OT
+
+    inp = wl.make(cfg_name)
+    c = inp["cfg"]
+    X = inp["X"]
+    tr = OT.build_tree(X, c["leaf"], c["tree"], inp["dirs"])
+    B = OB.build_basis(X, tr, c["w"])
+    pairs = OA.admitted_pairs(X, tr, B, c["pairs"], c["tau"])
+    kern = wl.kernel_dict(c)
+    rng = np.random.default_rng([0, 3, seed_tag])
+    order = rng.permutation(len(pairs))
+    ent = 0.0
+    nb = 0
+    t0 = time.perf_counter()
+    for k in order:
+        a, b = pairs[k]
+        OAs.block(X, tr, B, kern, a, b)
+        ent += float(tr.end[a] - tr.begin[a]) * float(tr.end[b] - tr.begin[b])
+        nb += 1
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    dt = time.perf_counter() - t0
+    cores = len(os.sched_getaffinity(0))
+    try:
+        from threadpoolctl import threadpool_info
+        blas = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        blas = None
+    desc = ("oracle blocks W_a C W_b^T (direct differences + NumPy matmul) for %d of %d admitted %s "
+            "blocks in seeded random order, %.1f s budget; tree/basis/admission untimed; BLAS threads %s"
+            % (nb, len(pairs), cfg_name, budget_s, blas))
+    return ent / dt, desc, cores, blas
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    vals = []
+    for _ in range(args.warmup):
+        oracle_sample(args.config, min(5.0, args.ref_budget))
+    desc = cores = None
+    for s in range(args.steps):
+        v, desc, cores, blas = oracle_sample(args.config, args.ref_budget, seed_tag=s + 1)
+        vals.append(v)
+    value = float(np.mean(vals))
+    c = wl.CONFIGS[args.config]
+    line = {
+        "impl": "reference", "metric": "C_W assembly covariance pairs/s", "value": value,
+        "unit": "covariance pairs/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "higher_is_better": True, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "n": c["n"], "d": c["d"], "w": c["w"], "leaf": c["leaf"],
+                   "tau": c["tau"]},
+        "cpu_baseline": {"value": value, "unit": "covariance pairs/s", "cores": cores, "kind": "oracle",
+                         "sample": desc},
+        "e2e": {"value": value, "unit": "covariance pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "vs_baseline": None,
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# --------------------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--impl", default="ours")
+    ap.add_argument("--ref-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1701_00285_b200 import mlk
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.Stream(dev)
+    ctx = mlk.Ctx(local, ws, rank, stream.cuda_stream)
+    inp = wl.make(args.config)
+    c = inp["cfg"]
+    kern = wl.kernel_dict(c)
+    spars = dict(mode=c["pairs"], tau=c["tau"])
+    X_d = torch.from_numpy(inp["X"]).to(dev)
+    dirs = inp["dirs"]
+    dirs_d = torch.from_numpy(dirs).to(dev) if dirs is not None else None
+    nvec = 1
+    torch.cuda.synchronize()
+
+    def step(X, D, v_host=None, out_vals=None, out_y=None):
+        tr = mlk.build_tree(ctx, X, c["leaf"], c["tree"], D)
+        B = mlk.build_basis(ctx, tr, c["w"])
+        cw = mlk.assemble_cw(ctx, tr, B, kern, spars)
+        if ws > 1:
+            mlk.gather_cw(ctx, cw)
+        if v_host is None:
+            v = torch.ones((nvec, B.dim), dtype=torch.float64, device=dev)
+            y = torch.empty_like(v)
+        else:
+            v, y = v_host, out_y
+        mlk.cw_matvec(ctx, tr, B, kern, None, mlk.MATVEC_EXACT, v, out=y)
+        if out_vals is not None:
+            cw.export(out=out_vals)
+        return tr, B, cw
+
+    # L2 flush buffer (> 126 MB L2) written between timed steps, outside the timed events
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device=dev)
+
+    for _ in range(args.warmup):
+        step(X_d, dirs_d)
+    torch.cuda.synchronize()
+    # one untimed pass for the structure numbers
+    tr, B, cw = step(X_d, dirs_d)
+    entries, flops = cw.entries, cw.flops
+    sf = cw.stage_flops()
+    nnz, dim = cw.nnz, B.dim
+    del tr, B, cw
+
+    sampler = ClockSampler(local) if rank == 0 else None
+    ctx.reset_stats()
+    ctx.set_timing(True)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.start()
+    launches0 = mlk.launch_count()
+    step_ms = []
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step(X_d, dirs_d)
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    launches = mlk.launch_count() - launches0
+    clocks = sampler.stop() if sampler else None
+    stats = ctx.kernel_stats()
+    ctx.set_timing(False)
+    total_ms = float(np.sum(step_ms))
+    if ws > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = entries * args.steps / (total_ms * 1e-3)
+
+    # ---- e2e: host (pinned) inputs, BSR values + C_W v read back, through the same API
+    Xh = torch.from_numpy(inp["X"]).pin_memory()
+    Dh = torch.from_numpy(dirs).pin_memory() if dirs is not None else None
+    vh = torch.ones((nvec, dim), dtype=torch.float64).pin_memory()
+    yh = torch.empty((nvec, dim), dtype=torch.float64).pin_memory()
+    valsh = torch.empty(max(nnz, 1), dtype=torch.float64).pin_memory()
+    e2e_ms = []
+    for _ in range(args.e2e_steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        step(Xh.numpy(), Dh.numpy() if Dh is not None else None, vh.numpy(), valsh.numpy()[:nnz], yh.numpy())
+        torch.cuda.synchronize()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_total = float(np.sum(e2e_ms))
+    if ws > 1:
+        t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    e2e_val = entries * args.e2e_steps / (e2e_total * 1e-3)
+    h2d = inp["X"].nbytes + (dirs.nbytes if dirs is not None else 0) + vh.numel() * 8
+    d2h = nnz * 8 + yh.numel() * 8
+
+    if rank == 0:
+        peak = fp64_peak()
+        k5 = stats.get("assemble_tile_contract", {"ms": float("nan"), "launches": 1})
+        k5_ms_per_step = k5["ms"] / args.steps
+        k5_flops = (sf["gram"] + sf["contract1"]) / ws
+        achieved = k5_flops / (k5_ms_per_step * 1e-3) / 1e12
+        traffic = None
+        if os.path.exists(TRAFFIC_FILE):
+            traffic = json.load(open(TRAFFIC_FILE)).get("bytes_per_launch")
+        asm_ms = sum(stats.get(k, {"ms": 0.0})["ms"] for k in
+                     ("search", "assemble_tile_contract", "assemble_wa_gemm")) / args.steps
+        cpu = None
+        if not args.no_cpu_baseline and ws == 1:
+            v, desc, cores, blas = oracle_sample(args.config, args.ref_budget)
+            cpu = {"value": v, "unit": "covariance pairs/s", "cores": cores, "kind": "oracle", "sample": desc}
+        line = {
+            "metric": "C_W assembly covariance pairs/s (FP64 TFLOP/s and % of FP64 peak in 'fp64')",
+            "value": value, "unit": "covariance pairs/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "n": c["n"], "d": c["d"], "w": c["w"], "leaf": c["leaf"],
+                       "family": c["family"], "rho": c["rho"], "tau": c["tau"], "pairs_mode": c["pairs"],
+                       "parallelism": "pairs%d" % ws, "l2": "flushed (512 MB write) between timed steps",
+                       "step": "build_tree + build_basis + assemble_cw(+all-gather) + cw_matvec EXACT nvec=1"},
+            "fp64": {"assembly_flops_per_step": flops, "tflops_step": flops / (ms_per_step * 1e-3) / 1e12,
+                     "tflops_assembly": flops / (asm_ms * 1e-3) / 1e12 if asm_ms > 0 else None,
+                     "pct_of_peak_step": 100.0 * flops / (ms_per_step * 1e-3) / 1e12 / peak,
+                     "peak_tflops": peak, "peak_source": "measured, profiles/fp64_peak_r01.json (DMMA loop)"},
+            "roofline": {"kernel": "assemble_tile_contract (K5a)", "bound": "fp64", "achieved": achieved,
+                         "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                         "algorithmic_flops_per_step": k5_flops, "ms_per_step": k5_ms_per_step},
+            "kernels_ms_per_step": {k: v["ms"] / args.steps for k, v in sorted(stats.items())},
+            "entries_per_step": entries, "blocks_nnz": nnz,
+            "clocks": clocks, "gpu_launches": launches,
+            "e2e": {"value": e2e_val, "unit": "covariance pairs/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_total / args.e2e_steps},
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

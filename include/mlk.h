@@ -1,0 +1,232 @@
+/*
+ * mlk.h -- C ABI of the B200-native multi-level covariance library (libmlk.so).
+ *
+ * The library computes the hot path of multi-level kriging (J. E. Castrillon-Candas,
+ * "High Dimensional Multi-Level Covariance Estimation and Kriging", arXiv:1701.00285):
+ * the multi-level covariance matrix C_W = W C(theta) W^T and
+ * the products C_W v.  "P:n" cites line n of the paper's LaTeX source
+ * (PAPER.md); readings of ambiguous passages are numbered R1.. in DESIGN.md.
+ *
+ * Conventions common to every call
+ *  - Every call returns mlk_status; no C++ exception crosses the ABI.  On a non-OK status
+ *    mlk_last_error() returns a thread-local description.  Handles passed to a failing call
+ *    stay valid; output handles are left NULL.
+ *  - Arguments are validated before any launch (MLK_ERR_INVALID_ARG).
+ *  - Pointer arguments documented "host or device" are classified with
+ *    cudaPointerGetAttributes: device (or managed) memory of the context's device is read
+ *    in place, anything else is treated as host memory and staged through the context's
+ *    stream.  Output pointers follow the same rule.
+ *  - Handles own all device memory they allocate (stream-ordered on the context stream).
+ *    Export calls copy into caller memory; passing NULL for an output skips it.
+ *  - A context is single-threaded; calls are stream-ordered on the context's stream and
+ *    return after the work they enqueue has completed unless stated otherwise.
+ *  - Multi-GPU (nranks > 1): one process per GPU.  Points and basis are replicated; the
+ *    assembly and the matvec split their work across ranks and return this rank's part.
+ *    The collectives (an all-gather of BSR values, an allreduce of C_W v) are issued by the
+ *    caller's NCCL process group between mlk_cw_pack / mlk_cw_unpack, and after
+ *    mlk_cw_matvec (see those calls).  Every rank must make the same calls with the same
+ *    arguments.
+ *  - Point-space vectors are in TREE ORDER: entry k belongs to original observation perm[k]
+ *    (mlk_tree_export).  C_W-space vectors are in C_W row order (levels t..0, heap order
+ *    within a level, reading R11).
+ *  - All floating point is IEEE binary64.
+ */
+#ifndef MLK_H_
+#define MLK_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MLK_OK = 0,
+  MLK_ERR_INVALID_ARG = 1,      /* a size, enum or pointer argument is out of range          */
+  MLK_ERR_DUPLICATE_POINTS = 2, /* two observation sites coincide (P:167-169 needs x_i != x_j) */
+  MLK_ERR_RANK_DEFICIENT = 3,   /* a moment matrix has rank < M (reading R9)                  */
+  MLK_ERR_OUT_OF_MEMORY = 4,    /* a device allocation failed                                 */
+  MLK_ERR_CUDA = 5,             /* any other CUDA runtime error                               */
+  MLK_ERR_UNSUPPORTED = 6       /* valid request this build does not implement                */
+} mlk_status;
+
+/* Text for the last non-OK status returned on this thread ("" if none). */
+const char* mlk_last_error(void);
+/* Library version string. */
+const char* mlk_version(void);
+/* Number of CUDA kernels this process has launched through the library so far. */
+int64_t mlk_launch_count(void);
+
+typedef struct mlk_ctx_s* mlk_ctx;
+typedef struct mlk_tree_s* mlk_tree;
+typedef struct mlk_basis_s* mlk_basis;
+typedef struct mlk_cw_s* mlk_cw;
+
+/* ------------------------------------------------------------------------------------------
+ * Context.  device: CUDA ordinal.  nranks >= 1, 0 <= rank < nranks.  cuda_stream: a
+ * cudaStream_t the library launches on (NULL: the library creates and owns one).
+ */
+mlk_status mlk_ctx_create(int device, int nranks, int rank, void* cuda_stream, mlk_ctx* out);
+void mlk_ctx_destroy(mlk_ctx ctx); /* NULL-safe */
+/* The cudaStream_t the context launches on. */
+void* mlk_ctx_stream(mlk_ctx ctx);
+/* Per-kernel timing with CUDA events recorded on the context stream around every launch
+ * (enable != 0).  Stats accumulate until mlk_ctx_reset_stats. */
+mlk_status mlk_ctx_set_timing(mlk_ctx ctx, int enable);
+mlk_status mlk_ctx_reset_stats(mlk_ctx ctx);
+/* Kernel stats: idx in [0, *count).  Call with name == NULL to get *count only.
+ * name receives the kernel name (NUL-terminated, truncated to name_len), launches the
+ * number of launches, ms the summed event-measured duration. */
+mlk_status mlk_ctx_kernel_stats(mlk_ctx ctx, int idx, int* count, char* name, int name_len,
+                                int64_t* launches, double* ms);
+
+/* ------------------------------------------------------------------------------------------
+ * mlk_build_tree -- binary median-split tree, Algorithm 1 with ChooseRule RP (Alg 2) or kD
+ * (Alg 2-kd).
+ *  X           n x d row-major observation sites, host or device.  Sites must be distinct
+ *              (MLK_ERR_DUPLICATE_POINTS otherwise).
+ *  leaf_size   a cell is a leaf iff it holds <= leaf_size points (R1).
+ *  kind        MLK_TREE_KD: direction e_(depth mod d) (R4); MLK_TREE_RP: `directions`.
+ *  directions  RP only: n_dir_rows x d row-major unit vectors, host or device, row q used
+ *              as given for heap node q (R3); needs n_dir_rows >= 2^t - 1 where t is the
+ *              tree depth (smallest delta with ceil(n / 2^delta) <= leaf_size).
+ * Split rule (R2): sort the cell by (x.v, original index); the first ceil(s/2) go left;
+ * threshold = median (midpoint of the two middle projections for even s).  Projections are
+ * summed left to right with separately rounded products and sums (R6).
+ * Nodes are numbered in heap order (children of q are 2q+1, 2q+2; R5).
+ * Cost: O(n d t) projections + one segmented sort per level, all on the device.
+ */
+typedef enum { MLK_TREE_KD = 0, MLK_TREE_RP = 1 } mlk_tree_kind;
+mlk_status mlk_build_tree(mlk_ctx ctx, const double* X, int64_t n, int32_t d, int32_t leaf_size,
+                          int32_t kind, const double* directions, int64_t n_dir_rows,
+                          mlk_tree* out);
+void mlk_tree_free(mlk_tree tree); /* NULL-safe */
+/* t: depth; n_nodes = 2^(t+1) - 1 heap slots. */
+mlk_status mlk_tree_info(mlk_tree tree, int32_t* t, int32_t* n_nodes, int64_t* n, int32_t* d);
+/* Host copies (any may be NULL).  perm[n]: tree position -> original index.  Per heap slot
+ * (n_nodes): begin/end range in perm (0,0 if the slot is empty), depth, state (-1 empty,
+ * 0 internal, 1 leaf), thr (NaN unless internal), dir (n_nodes x d, zero unless internal). */
+mlk_status mlk_tree_export(mlk_tree tree, int64_t* perm, int64_t* begin, int64_t* end,
+                           int32_t* depth, int32_t* state, double* thr, double* dir);
+
+/* ------------------------------------------------------------------------------------------
+ * mlk_build_basis -- multi-level basis, steps (a)-(f) P:1427-1515, with the orthonormal
+ * split of step (b) taken from a complete Householder QR in the LAPACK convention (R7):
+ * leaf: P(X_leaf) = Q R (s x M, total-degree-w monomials of the raw coordinates, R8),
+ *       Phi = Q_1^T, W = Q_2^T;
+ * internal: [R_L; R_R] = Q R (2M x M), Phi = Q_1^T (Phi_L (+) Phi_R), W = Q_2^T (...).
+ * M = C(d + w, w).  L = Phi_root (R10).  MLK_ERR_RANK_DEFICIENT if a leaf has fewer than M
+ * points or |R_kk| <= 1e-13 max_i |R_ii| in any cell (R9).
+ */
+mlk_status mlk_build_basis(mlk_ctx ctx, mlk_tree tree, int32_t w, mlk_basis* out);
+void mlk_basis_free(mlk_basis basis); /* NULL-safe */
+/* M; dim = N - M rows of W; n_cells = cells with at least one wavelet. */
+mlk_status mlk_basis_info(mlk_basis basis, int32_t* M, int64_t* dim, int32_t* n_cells);
+/* Host copies.  cells[n_cells]: heap node of each cell in C_W order; cell_row_off[n_cells+1]
+ * prefix sums of the wavelet counts.  If node >= 0: W_block (p_node x |node| row-major,
+ * columns = the node's points in tree order) and Phi_block (M x |node|).  L: M x n. */
+mlk_status mlk_basis_export(mlk_basis basis, int32_t* cells, int64_t* cell_row_off, int32_t node,
+                            double* W_block, double* Phi_block, double* L);
+/* a = W^T v (step (1) of P:2146-2170).  v: nvec x dim, a: nvec x n (host or device). */
+mlk_status mlk_apply_wt(mlk_ctx ctx, mlk_basis basis, const double* v, double* a, int32_t nvec);
+/* y = W b (step (3)).  b: nvec x n, y: nvec x dim. */
+mlk_status mlk_apply_w(mlk_ctx ctx, mlk_basis basis, const double* b, double* y, int32_t nvec);
+
+/* ------------------------------------------------------------------------------------------
+ * Covariance C(x, y) = sigma2 phi(|x - y|) + nugget [same observation] (R18), phi one of
+ * the Matern closed forms nu = 1/2, 3/2, 5/2 with z = sqrt(2 nu) r / rho (R16)
+ * or the Gaussian exp(-r^2 / rho^2) (R17).  rho > 0, sigma2 > 0, nugget >= 0.
+ */
+typedef enum { MLK_MATERN_12 = 0, MLK_MATERN_32 = 1, MLK_MATERN_52 = 2, MLK_GAUSSIAN = 3 } mlk_family;
+typedef struct {
+  int32_t family;
+  double rho, sigma2, nugget;
+} mlk_kernel;
+
+/* Sparsity: MLK_PAIRS_ALL admits every cell pair (dense C_W); MLK_PAIRS_PAPER_TAU admits the
+ * pairs of Algorithm 6 with tau_{i,j} = tau 2^(t-(i+j)/2) (R15),
+ * the symmetric projection rule (R12), the root row dense (R21) and self pairs. tau >= 0. */
+typedef enum { MLK_PAIRS_ALL = 0, MLK_PAIRS_PAPER_TAU = 1 } mlk_pairs;
+typedef struct {
+  int32_t mode;
+  double tau;
+} mlk_sparsity;
+
+/* Precision of the block computation.  FP64: FP64 DMMA tiles (Gram identity + fused kernel
+ * evaluation + two contractions).  DD: double-double tile generation and contractions for
+ * workloads at the FP64 floor (e.g. BASELINE cfg1). */
+typedef enum { MLK_PREC_FP64 = 0, MLK_PREC_DD = 1 } mlk_precision;
+
+/* ------------------------------------------------------------------------------------------
+ * mlk_assemble_cw -- the sparse multi-level covariance matrix C~_W (Algorithm 6; blocks
+ * W_i C W_j^T of P:1636-1653) in variable-block BSR form:
+ *  block rows/cols = cells in C_W order; each admitted unordered pair is stored once as
+ *  (row, col) with row <= col in C_W order, row-major p_row x p_col, blocks sorted by
+ *  (row, col).  Every block is computed exactly (no approximation inside a block).
+ * With nranks > 1 this rank computes only the blocks the LPT partition gives it (written to
+ * its shard buffer); see mlk_cw_pack/unpack for the gather.
+ */
+mlk_status mlk_assemble_cw(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const mlk_kernel* kernel,
+                           const mlk_sparsity* sparsity, int32_t precision, mlk_cw* out);
+void mlk_cw_free(mlk_cw cw); /* NULL-safe */
+/* n_cells; n_blocks; nnz values; entries = sum over blocks |row cell| |col cell| (covariance
+ * pairs evaluated); flops = algorithmic FP64 flops (Gram 2d per entry + the contractions of
+ * the chosen order); own_* = the same for this rank's blocks. */
+mlk_status mlk_cw_info(mlk_cw cw, int32_t* n_cells, int64_t* n_blocks, int64_t* nnz,
+                       double* entries, double* flops, double* own_entries, double* own_flops);
+/* Host copies of the structure (brow_ptr[n_cells+1], bcol[n_blocks], val_off[n_blocks+1])
+ * and, if values != NULL, of all nnz values (host or device pointer).  With nranks > 1 the
+ * values are complete only after mlk_cw_unpack. */
+mlk_status mlk_cw_export(mlk_cw cw, int32_t* brow_ptr, int32_t* bcol, int64_t* val_off,
+                         double* values);
+/* Algorithmic FP64 flops by stage (all blocks): gram = 2 d |a||b|, contract1 = the fused
+ * tile products C W_b^T (2 |a||b| p_b), contract2 = W_a U (2 p_a |a| p_b), for the order the
+ * planner chose per block (b = the side contracted first). */
+mlk_status mlk_cw_flops(mlk_cw cw, double* gram, double* contract1, double* contract2);
+/* Owner rank of every block (n_blocks), host copy. */
+mlk_status mlk_cw_owner(mlk_cw cw, int32_t* owner);
+/* Gather support (nranks > 1).  shard_len: doubles this rank produced; max_shard_len: the
+ * maximum over ranks.  mlk_cw_pack writes this rank's values, in block order, to `dst`
+ * (device, >= max_shard_len doubles, tail zero-filled).  After the caller's all-gather of
+ * the packed shards into `gathered` (device, nranks x max_shard_len, rank-major),
+ * mlk_cw_unpack scatters every rank's values to their BSR positions. */
+mlk_status mlk_cw_shard_len(mlk_cw cw, int64_t* shard_len, int64_t* max_shard_len);
+mlk_status mlk_cw_pack(mlk_ctx ctx, mlk_cw cw, double* dst);
+mlk_status mlk_cw_unpack(mlk_ctx ctx, mlk_cw cw, const double* gathered);
+/* Device pointer to the BSR values (valid while cw lives). */
+mlk_status mlk_cw_values_device(mlk_cw cw, double** values);
+
+/* ------------------------------------------------------------------------------------------
+ * mlk_cov_matvec -- b = C a, exact direct summation with on-the-fly covariance tiles (step
+ * (2) of P:2146-2170).  a, b: nvec x n in tree order (host or device), 1 <= nvec <= 64.
+ * With nranks > 1 only this rank's rows of b are computed; the others are zero.
+ */
+mlk_status mlk_cov_matvec(mlk_ctx ctx, mlk_tree tree, const mlk_kernel* kernel, const double* a,
+                          double* b, int32_t nvec);
+
+/* mlk_cw_matvec -- y = C_W v.  EXACT: y = W (C (W^T v)) by the three steps of
+ * P:2146-2170 (cw may be NULL).  BSR: y = C~_W v on the assembled blocks (mirrored lower
+ * triangle).  v, y: nvec x dim (host or device).  With nranks > 1 y is this rank's partial
+ * sum (its row panel of C, or its blocks); the caller sum-allreduces y over the ranks. */
+typedef enum { MLK_MATVEC_EXACT = 0, MLK_MATVEC_BSR = 1 } mlk_matvec_mode;
+mlk_status mlk_cw_matvec(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const mlk_kernel* kernel,
+                         mlk_cw cw, int32_t mode, const double* v, double* y, int32_t nvec);
+
+/* ------------------------------------------------------------------------------------------
+ * Host-only helpers (no device needed).
+ * mlk_partition_lpt: longest-processing-time assignment of n units with the given costs to
+ * nranks ranks (largest first to the least-loaded rank; ties to the lower rank), the
+ * partition mlk_assemble_cw uses.  owner[n] receives ranks.
+ */
+mlk_status mlk_partition_lpt(const double* cost, int64_t n, int32_t nranks, int32_t* owner);
+/* mlk_shard_plan: the gather layout mlk_assemble_cw uses.  Given block value offsets
+ * val_off[n+1] and owner[n], shard_off[k] = offset of block k inside its owner's packed shard
+ * (blocks in order), shard_len[nranks] = doubles per rank.  The gathered buffer holds rank r's
+ * shard at r * max(shard_len). */
+mlk_status mlk_shard_plan(const int64_t* val_off, const int32_t* owner, int64_t n, int32_t nranks,
+                          int64_t* shard_off, int64_t* shard_len);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MLK_H_ */

@@ -1,0 +1,103 @@
+// Handle types shared by the translation units of libmlk, and the ABI try/catch wrapper.
+#pragma once
+#include <new>
+
+#include "common.cuh"
+
+#define MLK_API_BEGIN try {
+#define MLK_API_END                                                        \
+  }                                                                        \
+  catch (const ::mlk::Error& e) {                                          \
+    ::mlk::set_last_error(e.what());                                       \
+    return e.status;                                                       \
+  }                                                                        \
+  catch (const std::bad_alloc&) {                                          \
+    ::mlk::set_last_error("host allocation failed");                       \
+    return MLK_ERR_OUT_OF_MEMORY;                                          \
+  }                                                                        \
+  catch (const std::exception& e) {                                        \
+    ::mlk::set_last_error(e.what());                                       \
+    return MLK_ERR_CUDA;                                                   \
+  }                                                                        \
+  return MLK_OK;
+
+namespace mlk {
+void partition_lpt(const double* cost, int64_t n, int nranks, int32_t* owner);
+void shard_plan(const int64_t* val_off, const int32_t* owner, int64_t n, int nranks, int64_t* shard_off,
+                int64_t* shard_len);
+
+// padded coordinate count for the DMMA k = 4 Gram steps
+inline int pad4(int d) { return (d + 3) / 4 * 4; }
+}  // namespace mlk
+
+// Tree (heap-numbered nodes).  Shape arrays are host-side (they depend only on n and the
+// leaf size); the permutation, thresholds and tree-ordered points live on the device.
+struct mlk_tree_s {
+  int device = 0;
+  int64_t n = 0;
+  int d = 0, d_pad = 0, leaf = 0, kind = 0, t = 0, n_nodes = 0;
+  std::vector<int8_t> state;      // -1 empty, 0 internal, 1 leaf
+  std::vector<int64_t> begin, end;
+  std::vector<int32_t> depth;
+  std::vector<double> thr;        // NaN unless internal
+  std::vector<double> dir;        // n_nodes x d
+  std::vector<int64_t> perm;      // host copy
+  mlk::DevBuf<int32_t> perm_d;    // tree position -> original index
+  mlk::DevBuf<double> X;          // n x d, original order
+  mlk::DevBuf<double> Xt;         // n x d_pad, tree order, zero padded
+  mlk::DevBuf<double> norm2;      // |x|^2 in tree order
+  mlk::DevBuf<double> thr_d;      // n_nodes
+  mlk::DevBuf<double> dir_d;      // n_nodes x d
+};
+
+// Basis blocks per heap node; cells (nodes with >= 1 wavelet) listed in C_W order.
+struct mlk_basis_s {
+  int device = 0;
+  int M = 0, w = 0;
+  int64_t dim = 0;
+  const mlk_tree_s* tree = nullptr;
+  std::vector<int32_t> cells;      // C_W order
+  std::vector<int64_t> row_off;    // n_cells + 1
+  std::vector<int32_t> p;          // wavelets per node (n_nodes)
+  std::vector<int32_t> cell_pos;   // node -> position in cells, or -1
+  std::vector<int64_t> w_off;      // node -> offset of W block (doubles) in W
+  std::vector<int64_t> phi_off;    // node -> offset of Phi block in Phi
+  mlk::DevBuf<double> W;           // all W blocks, C_W order, each p x |node| row-major
+  mlk::DevBuf<double> Phi;         // all Phi blocks, M x |node| row-major
+};
+
+struct mlk_cw_s {
+  int device = 0, nranks = 1, rank = 0;
+  int32_t n_cells = 0;
+  int64_t n_blocks = 0, nnz = 0;
+  std::vector<int32_t> brow_ptr, bcol, brow, owner;
+  std::vector<int64_t> val_off, shard_off;
+  int64_t shard_len = 0, max_shard_len = 0;
+  bool complete = false;           // values hold every block (nranks == 1 or unpacked)
+  double entries = 0, flops = 0, own_entries = 0, own_flops = 0;
+  double f_gram = 0, f_c1 = 0, f_c2 = 0;
+  mlk::DevBuf<double> values;      // nnz (complete for nranks == 1 or after unpack)
+  mlk::DevBuf<double> shard;       // this rank's packed values (nranks > 1)
+  // device structure for the BSR matvec
+  mlk::DevBuf<int32_t> brow_d, bcol_d, owner_d;
+  mlk::DevBuf<int64_t> val_off_d, shard_off_d;
+  mlk::DevBuf<int32_t> csc_ptr_d, csc_blk_d;   // blocks (r, c), r != c, grouped by column c
+};
+
+namespace mlk {
+// Row-major NN product C = A B (m x k times k x n); if trans_c, C^T is stored (C[j][i]).
+// If accumulate, the product is added to C (fixed order: exactly one job per C tile).
+struct GemmDesc {
+  const double* A;
+  int64_t lda;
+  const double* B;
+  int64_t ldb;
+  double* C;
+  int64_t ldc;
+  int32_t m, n, k;
+  int32_t trans_c;
+};
+// Launch all products on the context stream with FP64 DMMA tiles (64 x 64 x 16); large k
+// is split into fixed chunks whose partial tiles are reduced in chunk order (deterministic).
+void gemm_batched(Ctx& c, const std::vector<GemmDesc>& descs, const char* name);
+}  // namespace mlk

@@ -1,0 +1,189 @@
+// Internal runtime of libmlk: error handling, context, device buffers, timed launches.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <atomic>
+
+#include <cstdint>
+#include <cstdio>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/mlk.h"
+
+namespace mlk {
+
+// An error carrying an mlk_status; thrown inside the library, converted at the ABI edge.
+struct Error : std::runtime_error {
+  mlk_status status;
+  Error(mlk_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+void set_last_error(const std::string& msg);
+
+#define MLK_REQUIRE(cond, msg)                                                  \
+  do {                                                                          \
+    if (!(cond)) throw ::mlk::Error(MLK_ERR_INVALID_ARG, std::string(msg));     \
+  } while (0)
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    throw Error(MLK_ERR_OUT_OF_MEMORY, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+  throw Error(MLK_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CUDA_CHECK(x) ::mlk::cuda_check((x), #x)
+
+struct KStat {
+  int64_t launches = 0;
+  double ms = 0.0;
+};
+
+struct Ctx {
+  int device = 0, nranks = 1, rank = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  bool timing = false;
+  std::map<std::string, KStat> stats;
+  struct Pending {
+    std::string name;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> event_pool;
+
+  cudaEvent_t get_event();
+  void flush_timing();  // synchronize and fold pending events into stats
+};
+
+// Times a launch region with CUDA events on the context stream when timing is enabled.
+struct TimedLaunch {
+  Ctx& c;
+  const char* name;
+  cudaEvent_t a = nullptr;
+  TimedLaunch(Ctx& ctx, const char* n) : c(ctx), name(n) {
+    if (c.timing) {
+      a = c.get_event();
+      CUDA_CHECK(cudaEventRecord(a, c.stream));
+    }
+  }
+  ~TimedLaunch() noexcept(false) {
+    if (c.timing) {
+      cudaEvent_t b = c.get_event();
+      CUDA_CHECK(cudaEventRecord(b, c.stream));
+      c.pending.push_back({name, a, b});
+    }
+  }
+};
+
+extern std::atomic<int64_t> g_launches;
+
+inline void check_launch(const char* name) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw Error(MLK_ERR_CUDA, std::string("launch ") + name + ": " + cudaGetErrorString(e));
+}
+
+// Stream-ordered device buffer.
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(size_t count, cudaStream_t stream) { alloc(count, stream); }
+  void alloc(size_t count, cudaStream_t stream) {
+    release();
+    s = stream;
+    n = count;
+    if (count) CUDA_CHECK(cudaMallocAsync((void**)&p, count * sizeof(T), stream));
+  }
+  void zero() {
+    if (n) CUDA_CHECK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+  void upload(const T* host, size_t count) {
+    if (count) CUDA_CHECK(cudaMemcpyAsync(p, host, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void upload(const std::vector<T>& v) {
+    if (v.size() > n) alloc(v.size(), s);
+    upload(v.data(), v.size());
+  }
+  std::vector<T> download(size_t count) const {
+    std::vector<T> h(count);
+    if (count) {
+      CUDA_CHECK(cudaMemcpyAsync(h.data(), p, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+      CUDA_CHECK(cudaStreamSynchronize(s));
+    }
+    return h;
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { release(); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    release();
+    p = o.p; n = o.n; s = o.s;
+    o.p = nullptr; o.n = 0;
+    return *this;
+  }
+};
+
+// True if ptr is device or managed memory usable by the current device.
+bool is_device_ptr(const void* ptr);
+
+// Read-only view of a host-or-device input as a device pointer (copied if on the host).
+template <typename T>
+struct DevIn {
+  DevBuf<T> staged;
+  const T* p = nullptr;
+  DevIn(const T* src, size_t count, cudaStream_t s) {
+    if (src == nullptr || count == 0) { p = src; return; }
+    if (is_device_ptr(src)) { p = src; return; }
+    staged.alloc(count, s);
+    staged.upload(src, count);
+    p = staged.p;
+  }
+};
+
+// Write target: device pointer directly, or a staging buffer copied back by finish().
+template <typename T>
+struct DevOut {
+  DevBuf<T> staged;
+  T* dst;
+  T* p;
+  size_t count;
+  cudaStream_t s;
+  bool host;
+  DevOut(T* out, size_t cnt, cudaStream_t stream) : dst(out), count(cnt), s(stream) {
+    host = out != nullptr && cnt > 0 && !is_device_ptr(out);
+    if (host) {
+      staged.alloc(cnt, stream);
+      p = staged.p;
+    } else {
+      p = out;
+    }
+  }
+  void finish() {
+    if (host) CUDA_CHECK(cudaMemcpyAsync(dst, p, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+  }
+};
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+int num_sms(int device);
+
+}  // namespace mlk
+
+struct mlk_ctx_s {
+  mlk::Ctx c;
+};

@@ -1,0 +1,197 @@
+// Context, error reporting, per-kernel timing and host-only helpers of the C ABI.
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <queue>
+
+#include "api.cuh"
+#include "common.cuh"
+
+namespace mlk {
+
+static thread_local std::string g_last_error;
+std::atomic<int64_t> g_launches{0};
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+bool is_device_ptr(const void* ptr) {
+  cudaPointerAttributes attr;
+  cudaError_t e = cudaPointerGetAttributes(&attr, ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+int num_sms(int device) {
+  static int cached[64] = {0};
+  if (device >= 0 && device < 64 && cached[device]) return cached[device];
+  int v = 0;
+  CUDA_CHECK(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device));
+  if (device >= 0 && device < 64) cached[device] = v;
+  return v;
+}
+
+cudaEvent_t Ctx::get_event() {
+  if (!event_pool.empty()) {
+    cudaEvent_t e = event_pool.back();
+    event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  CUDA_CHECK(cudaEventCreate(&e));
+  return e;
+}
+
+void Ctx::flush_timing() {
+  if (pending.empty()) return;
+  CUDA_CHECK(cudaStreamSynchronize(stream));
+  for (auto& p : pending) {
+    float ms = 0.f;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, p.a, p.b));
+    KStat& s = stats[p.name];
+    s.launches += 1;
+    s.ms += ms;
+    event_pool.push_back(p.a);
+    event_pool.push_back(p.b);
+  }
+  pending.clear();
+}
+
+void partition_lpt(const double* cost, int64_t n, int nranks, int32_t* owner) {
+  std::vector<int64_t> idx(n);
+  std::iota(idx.begin(), idx.end(), 0);
+  std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) { return cost[a] > cost[b]; });
+  // min-heap of (load, rank); ties resolved to the lower rank
+  using E = std::pair<double, int>;
+  std::priority_queue<E, std::vector<E>, std::greater<E>> heap;
+  for (int r = 0; r < nranks; r++) heap.push({0.0, r});
+  for (int64_t k : idx) {
+    E e = heap.top();
+    heap.pop();
+    owner[k] = e.second;
+    e.first += cost[k];
+    heap.push(e);
+  }
+}
+
+void shard_plan(const int64_t* val_off, const int32_t* owner, int64_t n, int nranks, int64_t* shard_off,
+                int64_t* shard_len) {
+  for (int r = 0; r < nranks; r++) shard_len[r] = 0;
+  for (int64_t k = 0; k < n; k++) {
+    shard_off[k] = shard_len[owner[k]];
+    shard_len[owner[k]] += val_off[k + 1] - val_off[k];
+  }
+}
+
+}  // namespace mlk
+
+using namespace mlk;
+
+extern "C" {
+
+const char* mlk_last_error(void) { return g_last_error.c_str(); }
+
+const char* mlk_version(void) { return "mlk 0.1 (sm_100a, FP64 DMMA)"; }
+
+int64_t mlk_launch_count(void) { return g_launches.load(); }
+
+mlk_status mlk_ctx_create(int device, int nranks, int rank, void* cuda_stream, mlk_ctx* out) {
+  MLK_API_BEGIN
+  MLK_REQUIRE(out != nullptr, "out is NULL");
+  *out = nullptr;
+  MLK_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, "need 0 <= rank < nranks");
+  int ndev = 0;
+  CUDA_CHECK(cudaGetDeviceCount(&ndev));
+  MLK_REQUIRE(device >= 0 && device < ndev, "invalid device ordinal");
+  CUDA_CHECK(cudaSetDevice(device));
+  auto* h = new mlk_ctx_s();
+  h->c.device = device;
+  h->c.nranks = nranks;
+  h->c.rank = rank;
+  if (cuda_stream) {
+    h->c.stream = (cudaStream_t)cuda_stream;
+  } else {
+    cudaError_t e = cudaStreamCreateWithFlags(&h->c.stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      delete h;
+      cuda_check(e, "cudaStreamCreate");
+    }
+    h->c.own_stream = true;
+  }
+  *out = h;
+  MLK_API_END
+}
+
+void mlk_ctx_destroy(mlk_ctx ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->c.device);
+  cudaStreamSynchronize(ctx->c.stream);
+  for (auto& p : ctx->c.pending) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  for (auto e : ctx->c.event_pool) cudaEventDestroy(e);
+  if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
+  delete ctx;
+}
+
+void* mlk_ctx_stream(mlk_ctx ctx) { return ctx ? (void*)ctx->c.stream : nullptr; }
+
+mlk_status mlk_ctx_set_timing(mlk_ctx ctx, int enable) {
+  MLK_API_BEGIN
+  MLK_REQUIRE(ctx, "ctx is NULL");
+  ctx->c.flush_timing();
+  ctx->c.timing = enable != 0;
+  MLK_API_END
+}
+
+mlk_status mlk_ctx_reset_stats(mlk_ctx ctx) {
+  MLK_API_BEGIN
+  MLK_REQUIRE(ctx, "ctx is NULL");
+  ctx->c.flush_timing();
+  ctx->c.stats.clear();
+  MLK_API_END
+}
+
+mlk_status mlk_ctx_kernel_stats(mlk_ctx ctx, int idx, int* count, char* name, int name_len,
+                                int64_t* launches, double* ms) {
+  MLK_API_BEGIN
+  MLK_REQUIRE(ctx, "ctx is NULL");
+  CUDA_CHECK(cudaSetDevice(ctx->c.device));
+  ctx->c.flush_timing();
+  if (count) *count = (int)ctx->c.stats.size();
+  if (name == nullptr && launches == nullptr && ms == nullptr) return MLK_OK;
+  MLK_REQUIRE(idx >= 0 && idx < (int)ctx->c.stats.size(), "stat index out of range");
+  auto it = ctx->c.stats.begin();
+  std::advance(it, idx);
+  if (name && name_len > 0) {
+    std::strncpy(name, it->first.c_str(), name_len - 1);
+    name[name_len - 1] = 0;
+  }
+  if (launches) *launches = it->second.launches;
+  if (ms) *ms = it->second.ms;
+  MLK_API_END
+}
+
+mlk_status mlk_partition_lpt(const double* cost, int64_t n, int32_t nranks, int32_t* owner) {
+  MLK_API_BEGIN
+  MLK_REQUIRE(n >= 0 && nranks >= 1, "invalid sizes");
+  MLK_REQUIRE(n == 0 || (cost && owner), "NULL pointer");
+  for (int64_t k = 0; k < n; k++) MLK_REQUIRE(cost[k] >= 0.0, "negative cost");
+  partition_lpt(cost, n, nranks, owner);
+  MLK_API_END
+}
+
+mlk_status mlk_shard_plan(const int64_t* val_off, const int32_t* owner, int64_t n, int32_t nranks,
+                          int64_t* shard_off, int64_t* shard_len) {
+  MLK_API_BEGIN
+  MLK_REQUIRE(n >= 0 && nranks >= 1, "invalid sizes");
+  MLK_REQUIRE(val_off && shard_len && (n == 0 || (owner && shard_off)), "NULL pointer");
+  for (int64_t k = 0; k < n; k++) MLK_REQUIRE(owner[k] >= 0 && owner[k] < nranks, "owner out of range");
+  shard_plan(val_off, owner, n, nranks, shard_off, shard_len);
+  MLK_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,265 @@
+// C_W v by the three steps of P:2146-2170 -- (1) a = W^T v, (2) b = C a, (3) y = W b -- and
+// the BSR product y = C~_W v.  Step (2) is the fused tile kernel of tile.cu with the vectors
+// in place of a wavelet block; steps (1), (3) and the BSR product are HBM-bound passes over
+// the stored W blocks / BSR values with a fixed summation order (deterministic).
+#include <algorithm>
+
+#include "api.cuh"
+#include "tile.cuh"
+
+namespace mlk {
+namespace {
+
+struct CellJob {
+  int64_t pt_begin;   // first tree position of the cell
+  int32_t s, p;       // points, wavelets
+  int64_t row_off;    // C_W row offset
+  const double* W;    // p x s
+};
+
+// a[v][begin + x] += sum_r W[r][x] v[v][row_off + r] for the cells of one level
+__global__ void k_apply_wt(const CellJob* __restrict__ jobs, const double* __restrict__ v, int64_t dim,
+                           double* __restrict__ a, int64_t n, int nvec) {
+  const CellJob jb = jobs[blockIdx.x];
+  for (int x = blockIdx.y * blockDim.x + threadIdx.x; x < jb.s; x += gridDim.y * blockDim.x) {
+    for (int iv = 0; iv < nvec; iv++) {
+      const double* vv = v + (int64_t)iv * dim + jb.row_off;
+      double s = 0.0;
+      for (int r = 0; r < jb.p; r++) s = fma(jb.W[(int64_t)r * jb.s + x], vv[r], s);
+      a[(int64_t)iv * n + jb.pt_begin + x] += s;
+    }
+  }
+}
+
+// y[v][row_off + r] = sum_x W[r][x] b[v][begin + x]; one warp per row
+__global__ void k_apply_w(const CellJob* __restrict__ jobs, const double* __restrict__ b, int64_t n,
+                          double* __restrict__ y, int64_t dim, int nvec) {
+  const CellJob jb = jobs[blockIdx.x];
+  const int lane = threadIdx.x & 31;
+  const int wid = blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int nw = gridDim.y * (blockDim.x >> 5);
+  for (int r = wid; r < jb.p; r += nw) {
+    const double* w = jb.W + (int64_t)r * jb.s;
+    for (int iv = 0; iv < nvec; iv++) {
+      const double* bb = b + (int64_t)iv * n + jb.pt_begin;
+      double s = 0.0;
+      for (int x = lane; x < jb.s; x += 32) s = fma(w[x], bb[x], s);
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) y[(int64_t)iv * dim + jb.row_off + r] = s;
+    }
+  }
+}
+
+// BSR: y_r = sum_{own blocks (r,c)} B v_c + sum_{own blocks (c,r), c != r} B^T v_c
+__global__ void k_bsr_matvec(const int32_t* __restrict__ brow_ptr, const int32_t* __restrict__ bcol,
+                             const int64_t* __restrict__ val_off, const int32_t* __restrict__ owner, int rank,
+                             const int32_t* __restrict__ csc_ptr, const int32_t* __restrict__ csc_blk,
+                             const int32_t* __restrict__ brow, const int64_t* __restrict__ row_off,
+                             const double* __restrict__ vals, const double* __restrict__ v, double* __restrict__ y,
+                             int64_t dim, int nvec) {
+  extern __shared__ double part[];  // p_r x nvec
+  const int r = blockIdx.x;
+  const int64_t r0 = row_off[r];
+  const int pr = (int)(row_off[r + 1] - r0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int e = threadIdx.x; e < pr * nvec; e += blockDim.x) part[e] = 0.0;
+  __syncthreads();
+  // row blocks: warp per output row, lanes over the block's columns
+  for (int k = brow_ptr[r]; k < brow_ptr[r + 1]; k++) {
+    if (owner[k] != rank) continue;
+    const int c = bcol[k];
+    const int64_t c0 = row_off[c];
+    const int pc = (int)(row_off[c + 1] - c0);
+    const double* B = vals + val_off[k];
+    for (int i = warp; i < pr; i += nw) {
+      for (int iv = 0; iv < nvec; iv++) {
+        const double* vv = v + (int64_t)iv * dim + c0;
+        double s = 0.0;
+        for (int j = lane; j < pc; j += 32) s = fma(B[(int64_t)i * pc + j], vv[j], s);
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) part[i * nvec + iv] += s;
+      }
+    }
+  }
+  __syncthreads();
+  // mirrored blocks: thread per output row (column of the stored block)
+  for (int i = threadIdx.x; i < pr; i += blockDim.x) {
+    for (int iv = 0; iv < nvec; iv++) {
+      double s = part[i * nvec + iv];
+      for (int q = csc_ptr[r]; q < csc_ptr[r + 1]; q++) {
+        const int k = csc_blk[q];
+        if (owner[k] != rank) continue;
+        const int c = brow[k];
+        const int64_t c0 = row_off[c];
+        const int pc = (int)(row_off[c + 1] - c0);
+        const double* B = vals + val_off[k];  // pc x pr
+        const double* vv = v + (int64_t)iv * dim + c0;
+        for (int j = 0; j < pc; j++) s = fma(B[(int64_t)j * pr + i], vv[j], s);
+      }
+      y[(int64_t)iv * dim + r0 + i] = s;
+    }
+  }
+}
+
+std::vector<std::vector<CellJob>> level_jobs(const mlk_tree_s* tree, const mlk_basis_s* B) {
+  std::vector<std::vector<CellJob>> lv(tree->t + 1);
+  for (size_t i = 0; i < B->cells.size(); i++) {
+    int q = B->cells[i];
+    lv[tree->depth[q]].push_back({tree->begin[q], (int32_t)(tree->end[q] - tree->begin[q]), B->p[q],
+                                  B->row_off[i], B->W.p + B->w_off[q]});
+  }
+  return lv;
+}
+
+void apply_wt_dev(Ctx& c, const mlk_tree_s* tree, const mlk_basis_s* B, const double* v, double* a, int nvec) {
+  CUDA_CHECK(cudaMemsetAsync(a, 0, sizeof(double) * nvec * tree->n, c.stream));
+  auto lv = level_jobs(tree, B);
+  TimedLaunch tl(c, "apply_wt");
+  for (int dep = tree->t; dep >= 0; dep--) {  // fixed level order: t .. 0
+    if (lv[dep].empty()) continue;
+    DevBuf<CellJob> dj(lv[dep].size(), c.stream);
+    dj.upload(lv[dep]);
+    int smax = 0;
+    for (auto& j : lv[dep]) smax = std::max(smax, j.s);
+    dim3 grid((unsigned)lv[dep].size(), (unsigned)std::max<int64_t>(1, std::min<int64_t>(64, ceil_div(smax, 256))));
+    k_apply_wt<<<grid, 256, 0, c.stream>>>(dj.p, v, B->dim, a, tree->n, nvec);
+    check_launch("k_apply_wt");
+  }
+}
+
+void apply_w_dev(Ctx& c, const mlk_tree_s* tree, const mlk_basis_s* B, const double* b, double* y, int nvec) {
+  std::vector<CellJob> all;
+  int pmax = 0;
+  for (auto& l : level_jobs(tree, B))
+    for (auto& j : l) {
+      all.push_back(j);
+      pmax = std::max(pmax, j.p);
+    }
+  if (all.empty()) return;
+  DevBuf<CellJob> dj(all.size(), c.stream);
+  dj.upload(all);
+  TimedLaunch tl(c, "apply_w");
+  dim3 grid((unsigned)all.size(), (unsigned)std::max<int64_t>(1, std::min<int64_t>(32, ceil_div(pmax, 8))));
+  k_apply_w<<<grid, 256, 0, c.stream>>>(dj.p, b, tree->n, y, B->dim, nvec);
+  check_launch("k_apply_w");
+}
+
+// b = C a for this rank's rows (others zero); a, b device, nvec x n
+void cov_matvec_dev(Ctx& c, const mlk_tree_s* tree, const mlk_kernel& k, const double* a, double* b, int nvec) {
+  const int64_t n = tree->n;
+  CUDA_CHECK(cudaMemsetAsync(b, 0, sizeof(double) * nvec * n, c.stream));
+  // rows of this rank: contiguous 32-row tiles
+  int64_t tiles = ceil_div(n, 32);
+  int64_t t0 = tiles * c.rank / c.nranks, t1 = tiles * (c.rank + 1) / c.nranks;
+  if (t1 <= t0) return;
+  int64_t r0 = t0 * 32, r1 = std::min<int64_t>(n, t1 * 32);
+  std::vector<TileUnit> units;
+  // rows r0..r1 as an a range; b range = all points; W_b = the vectors a (nvec x n)
+  make_tile_units(units, r0, (int32_t)(r1 - r0), 0, (int32_t)n, a, n, nvec, b + r0, n, 1, tree->d_pad);
+  run_tile_contract(c, tree, make_kernel_params(k), units, "cov_matvec_tile");
+}
+
+void check_kernel(const mlk_kernel* k) {
+  MLK_REQUIRE(k != nullptr, "kernel is NULL");
+  MLK_REQUIRE(k->family >= MLK_MATERN_12 && k->family <= MLK_GAUSSIAN, "unknown covariance family");
+  MLK_REQUIRE(k->rho > 0 && k->sigma2 > 0 && k->nugget >= 0, "need rho > 0, sigma2 > 0, nugget >= 0");
+}
+
+}  // namespace
+}  // namespace mlk
+
+using namespace mlk;
+
+extern "C" {
+
+mlk_status mlk_apply_wt(mlk_ctx ctx, mlk_basis basis, const double* v, double* a, int32_t nvec) {
+  MLK_API_BEGIN
+  MLK_REQUIRE(ctx && basis && v && a, "NULL argument");
+  MLK_REQUIRE(nvec >= 1, "need nvec >= 1");
+  Ctx& c = ctx->c;
+  CUDA_CHECK(cudaSetDevice(c.device));
+  const mlk_tree_s* tree = basis->tree;
+  DevIn<double> vin(v, (size_t)nvec * basis->dim, c.stream);
+  DevOut<double> aout(a, (size_t)nvec * tree->n, c.stream);
+  apply_wt_dev(c, tree, basis, vin.p, aout.p, nvec);
+  aout.finish();
+  MLK_API_END
+}
+
+mlk_status mlk_apply_w(mlk_ctx ctx, mlk_basis basis, const double* b, double* y, int32_t nvec) {
+  MLK_API_BEGIN
+  MLK_REQUIRE(ctx && basis && b && y, "NULL argument");
+  MLK_REQUIRE(nvec >= 1, "need nvec >= 1");
+  Ctx& c = ctx->c;
+  CUDA_CHECK(cudaSetDevice(c.device));
+  const mlk_tree_s* tree = basis->tree;
+  DevIn<double> bin(b, (size_t)nvec * tree->n, c.stream);
+  DevOut<double> yout(y, (size_t)nvec * basis->dim, c.stream);
+  apply_w_dev(c, tree, basis, bin.p, yout.p, nvec);
+  yout.finish();
+  MLK_API_END
+}
+
+mlk_status mlk_cov_matvec(mlk_ctx ctx, mlk_tree tree, const mlk_kernel* kernel, const double* a, double* b,
+                          int32_t nvec) {
+  MLK_API_BEGIN
+  MLK_REQUIRE(ctx && tree && a && b, "NULL argument");
+  check_kernel(kernel);
+  MLK_REQUIRE(nvec >= 1 && nvec <= 64, "need 1 <= nvec <= 64");
+  Ctx& c = ctx->c;
+  CUDA_CHECK(cudaSetDevice(c.device));
+  DevIn<double> ain(a, (size_t)nvec * tree->n, c.stream);
+  DevOut<double> bout(b, (size_t)nvec * tree->n, c.stream);
+  cov_matvec_dev(c, tree, *kernel, ain.p, bout.p, nvec);
+  bout.finish();
+  MLK_API_END
+}
+
+mlk_status mlk_cw_matvec(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const mlk_kernel* kernel, mlk_cw cw,
+                         int32_t mode, const double* v, double* y, int32_t nvec) {
+  MLK_API_BEGIN
+  MLK_REQUIRE(ctx && tree && basis && v && y, "NULL argument");
+  MLK_REQUIRE(basis->tree == tree, "basis was built for another tree");
+  MLK_REQUIRE(mode == MLK_MATVEC_EXACT || mode == MLK_MATVEC_BSR, "unknown matvec mode");
+  MLK_REQUIRE(nvec >= 1 && nvec <= 64, "need 1 <= nvec <= 64");
+  Ctx& c = ctx->c;
+  CUDA_CHECK(cudaSetDevice(c.device));
+  const int64_t dim = basis->dim;
+  DevIn<double> vin(v, (size_t)nvec * dim, c.stream);
+  DevOut<double> yout(y, (size_t)nvec * dim, c.stream);
+  if (mode == MLK_MATVEC_EXACT) {
+    check_kernel(kernel);
+    DevBuf<double> a((size_t)nvec * tree->n, c.stream), b((size_t)nvec * tree->n, c.stream);
+    apply_wt_dev(c, tree, basis, vin.p, a.p, nvec);
+    cov_matvec_dev(c, tree, *kernel, a.p, b.p, nvec);
+    apply_w_dev(c, tree, basis, b.p, yout.p, nvec);
+    yout.finish();
+  } else {
+    MLK_REQUIRE(cw != nullptr, "BSR mode needs the assembled matrix");
+    MLK_REQUIRE(cw->n_cells == (int32_t)basis->cells.size(), "cw does not match the basis");
+    MLK_REQUIRE(cw->complete, "BSR mode with nranks > 1 needs mlk_cw_unpack first");
+    DevBuf<int64_t> ro(basis->row_off.size(), c.stream);
+    ro.upload(basis->row_off);
+    DevBuf<int32_t> brp(cw->brow_ptr.size(), c.stream);
+    brp.upload(cw->brow_ptr);
+    // values: the gathered matrix when nranks == 1 or after unpack; a rank applies only its
+    // own blocks (the caller allreduces y)
+    int pmax = 0;
+    for (size_t i = 0; i + 1 < basis->row_off.size(); i++)
+      pmax = std::max<int>(pmax, (int)(basis->row_off[i + 1] - basis->row_off[i]));
+    size_t smem = sizeof(double) * (size_t)std::max(1, pmax) * nvec;
+    MLK_REQUIRE(smem <= 200 * 1024, "BSR matvec: p_max x nvec too large");
+    CUDA_CHECK(cudaFuncSetAttribute(k_bsr_matvec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (cw->n_cells > 0) {
+      TimedLaunch tl(c, "bsr_matvec");
+      k_bsr_matvec<<<cw->n_cells, 256, smem, c.stream>>>(brp.p, cw->bcol_d.p, cw->val_off_d.p, cw->owner_d.p, c.rank,
+                                                          cw->csc_ptr_d.p, cw->csc_blk_d.p, cw->brow_d.p, ro.p,
+                                                          cw->values.p, vin.p, yout.p, dim, nvec);
+      check_launch("k_bsr_matvec");
+    }
+    yout.finish();
+  }
+  MLK_API_END
+}
+
+}  // extern "C"

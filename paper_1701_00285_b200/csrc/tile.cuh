@@ -1,0 +1,46 @@
+// The fused tile-and-contract kernel (K5a): for a cell pair (a, b) it computes
+//     U[r, l] = sum_y C(x_{a,r}, x_{b,y}) W_b[l, y]
+// with the covariance tile generated in registers -- Gram product x.y on FP64 DMMA, the
+// Gram identity r^2 = |x|^2 + |y|^2 - 2 x.y, the Matern/Gaussian closed form -- and
+// contracted immediately on FP64 DMMA; C never reaches memory.  It serves the assembly
+// (W_b = wavelet block of the contracted-first cell) and the exact product b = C a
+// (W_b = the vectors a).
+#pragma once
+#include "api.cuh"
+
+namespace mlk {
+
+struct TileUnit {
+  int64_t a_begin, b_begin;  // first tree position of the a / b point ranges
+  int32_t s_a, s_b;          // points in the ranges
+  int32_t row0;              // first a row handled by this unit (multiple of 32)
+  int32_t c0, qc;            // first column of W_b rows handled, and how many (<= 8 RQ)
+  int32_t p_b;               // rows of W_b
+  int32_t trans;             // 0: U[r * ldu + c0 + l]; 1: U[(c0 + l) * ldu + r]
+  int32_t rq;                // instantiation class (columns padded to 8 rq)
+  const double* Wb;          // W_b[l][y] at Wb + l * ldw + y
+  int64_t ldw;
+  double* U;                 // base of this pair's U
+  int64_t ldu;
+  double cost;               // for scheduling
+};
+
+struct KernelParams {
+  int32_t family;
+  double c1;      // sqrt(2 nu) / rho (Matern) or 1 / rho^2 (Gaussian)
+  double sigma2;
+  double nugget;
+};
+
+KernelParams make_kernel_params(const mlk_kernel& k);
+// column-class instantiations available to the planner
+int tile_rq_class(int qc);  // smallest available rq with 8 rq >= qc
+constexpr int kTileMaxRQ = 24;
+// Run all units (any mix of rq classes) on the context stream.
+void run_tile_contract(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, std::vector<TileUnit>& units,
+                       const char* name);
+// Split a (pair, output) into units: rows in blocks of 32, W_b rows in balanced chunks.
+void make_tile_units(std::vector<TileUnit>& out, int64_t a_begin, int32_t s_a, int64_t b_begin, int32_t s_b,
+                     const double* Wb, int64_t ldw, int32_t p_b, double* U, int64_t ldu, int32_t trans, int dp);
+
+}  // namespace mlk

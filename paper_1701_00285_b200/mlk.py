@@ -1,0 +1,419 @@
+"""Thin ctypes binding of libmlk.so (include/mlk.h).  Argument marshalling only: every step of
+the path runs in the library's CUDA kernels.  There is no CPU fallback -- importing this module
+fails loudly when the in-tree libmlk.so is missing.
+
+Arrays: host inputs may be NumPy arrays (float64, C-contiguous); device inputs/outputs may be
+torch CUDA tensors (float64, contiguous).  Results are returned as NumPy arrays unless a torch
+`out=` tensor is supplied.
+"""
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmlk.so")
+if not os.path.exists(LIB_PATH):
+    raise ImportError("libmlk.so is not built (run `python -m paper_1701_00285_b200.build` or "
+                      "__graft_entry__.build()); there is no CPU fallback")
+_lib = C.CDLL(LIB_PATH)
+
+# enums (include/mlk.h)
+OK, ERR_INVALID_ARG, ERR_DUPLICATE_POINTS, ERR_RANK_DEFICIENT, ERR_OUT_OF_MEMORY, ERR_CUDA, \
+    ERR_UNSUPPORTED = range(7)
+TREE_KD, TREE_RP = 0, 1
+MATERN_12, MATERN_32, MATERN_52, GAUSSIAN = 0, 1, 2, 3
+PAIRS_ALL, PAIRS_PAPER_TAU = 0, 1
+PREC_FP64, PREC_DD = 0, 1
+MATVEC_EXACT, MATVEC_BSR = 0, 1
+
+SYMBOLS = [
+    "mlk_last_error", "mlk_version", "mlk_ctx_create", "mlk_ctx_destroy", "mlk_ctx_stream",
+    "mlk_ctx_set_timing", "mlk_ctx_reset_stats", "mlk_ctx_kernel_stats", "mlk_build_tree",
+    "mlk_tree_free", "mlk_tree_info", "mlk_tree_export", "mlk_build_basis", "mlk_basis_free",
+    "mlk_basis_info", "mlk_basis_export", "mlk_apply_wt", "mlk_apply_w", "mlk_assemble_cw",
+    "mlk_cw_free", "mlk_cw_info", "mlk_cw_export", "mlk_cw_owner", "mlk_cw_shard_len", "mlk_cw_pack",
+    "mlk_cw_unpack", "mlk_cw_values_device", "mlk_cov_matvec", "mlk_cw_matvec", "mlk_partition_lpt",
+    "mlk_shard_plan", "mlk_launch_count", "mlk_cw_flops",
+]
+
+
+class MlkError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__("mlk status %d: %s" % (status, msg))
+        self.status = status
+
+
+class DuplicatePoints(MlkError):
+    pass
+
+
+class RankDeficient(MlkError):
+    pass
+
+
+class KernelSpec(C.Structure):
+    _fields_ = [("family", C.c_int32), ("rho", C.c_double), ("sigma2", C.c_double), ("nugget", C.c_double)]
+
+
+class SparsitySpec(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("tau", C.c_double)]
+
+
+P = C.c_void_p
+_sig = {
+    "mlk_last_error": (C.c_char_p, []),
+    "mlk_version": (C.c_char_p, []),
+    "mlk_ctx_create": (C.c_int, [C.c_int, C.c_int, C.c_int, P, C.POINTER(P)]),
+    "mlk_ctx_destroy": (None, [P]),
+    "mlk_ctx_stream": (P, [P]),
+    "mlk_ctx_set_timing": (C.c_int, [P, C.c_int]),
+    "mlk_ctx_reset_stats": (C.c_int, [P]),
+    "mlk_ctx_kernel_stats": (C.c_int, [P, C.c_int, C.POINTER(C.c_int), C.c_char_p, C.c_int,
+                                       C.POINTER(C.c_int64), C.POINTER(C.c_double)]),
+    "mlk_build_tree": (C.c_int, [P, P, C.c_int64, C.c_int32, C.c_int32, C.c_int32, P, C.c_int64,
+                                 C.POINTER(P)]),
+    "mlk_tree_free": (None, [P]),
+    "mlk_tree_info": (C.c_int, [P, P, P, P, P]),
+    "mlk_tree_export": (C.c_int, [P, P, P, P, P, P, P, P]),
+    "mlk_build_basis": (C.c_int, [P, P, C.c_int32, C.POINTER(P)]),
+    "mlk_basis_free": (None, [P]),
+    "mlk_basis_info": (C.c_int, [P, P, P, P]),
+    "mlk_basis_export": (C.c_int, [P, P, P, C.c_int32, P, P, P]),
+    "mlk_apply_wt": (C.c_int, [P, P, P, P, C.c_int32]),
+    "mlk_apply_w": (C.c_int, [P, P, P, P, C.c_int32]),
+    "mlk_assemble_cw": (C.c_int, [P, P, P, C.POINTER(KernelSpec), C.POINTER(SparsitySpec), C.c_int32,
+                                  C.POINTER(P)]),
+    "mlk_cw_free": (None, [P]),
+    "mlk_cw_info": (C.c_int, [P, P, P, P, P, P, P, P]),
+    "mlk_cw_export": (C.c_int, [P, P, P, P, P]),
+    "mlk_cw_owner": (C.c_int, [P, P]),
+    "mlk_cw_shard_len": (C.c_int, [P, P, P]),
+    "mlk_cw_pack": (C.c_int, [P, P, P]),
+    "mlk_cw_unpack": (C.c_int, [P, P, P]),
+    "mlk_cw_values_device": (C.c_int, [P, C.POINTER(P)]),
+    "mlk_cov_matvec": (C.c_int, [P, P, C.POINTER(KernelSpec), P, P, C.c_int32]),
+    "mlk_cw_matvec": (C.c_int, [P, P, P, C.POINTER(KernelSpec), P, C.c_int32, P, P, C.c_int32]),
+    "mlk_partition_lpt": (C.c_int, [P, C.c_int64, C.c_int32, P]),
+    "mlk_shard_plan": (C.c_int, [P, P, C.c_int64, C.c_int32, P, P]),
+    "mlk_launch_count": (C.c_int64, []),
+    "mlk_cw_flops": (C.c_int, [P, P, P, P]),
+}
+for _n, (_r, _a) in _sig.items():
+    _f = getattr(_lib, _n)
+    _f.restype = _r
+    _f.argtypes = _a
+
+
+def _check(st):
+    if st != OK:
+        msg = _lib.mlk_last_error().decode()
+        if st == ERR_DUPLICATE_POINTS:
+            raise DuplicatePoints(st, msg)
+        if st == ERR_RANK_DEFICIENT:
+            raise RankDeficient(st, msg)
+        raise MlkError(st, msg)
+
+
+def version():
+    return _lib.mlk_version().decode()
+
+
+def launch_count():
+    """Kernels launched through libmlk in this process so far."""
+    return int(_lib.mlk_launch_count())
+
+
+def _ptr(x, dtype=np.float64):
+    """(pointer, keepalive) for a NumPy array or torch tensor (no copy for contiguous inputs)."""
+    if x is None:
+        return None, None
+    if hasattr(x, "data_ptr") and hasattr(x, "is_cuda"):
+        assert x.is_contiguous(), "tensor must be contiguous"
+        return C.c_void_p(x.data_ptr()), x
+    a = np.ascontiguousarray(x, dtype=dtype)
+    return a.ctypes.data_as(C.c_void_p), a
+
+
+def _np(ptr_holder):
+    return ptr_holder.ctypes.data_as(C.c_void_p)
+
+
+def kernel_spec(family, rho, sigma2=1.0, nugget=0.0):
+    return KernelSpec(int(family), float(rho), float(sigma2), float(nugget))
+
+
+def _kspec(k):
+    if isinstance(k, KernelSpec):
+        return k
+    return kernel_spec(k["family"], k["rho"], k.get("sigma2", 1.0), k.get("nugget", 0.0))
+
+
+class Ctx:
+    def __init__(self, device=0, nranks=1, rank=0, stream=None):
+        h = C.c_void_p()
+        _check(_lib.mlk_ctx_create(int(device), int(nranks), int(rank),
+                                   C.c_void_p(stream) if stream else None, C.byref(h)))
+        self.h = h
+        self.device, self.nranks, self.rank = device, nranks, rank
+
+    @property
+    def stream(self):
+        return _lib.mlk_ctx_stream(self.h)
+
+    def set_timing(self, on=True):
+        _check(_lib.mlk_ctx_set_timing(self.h, 1 if on else 0))
+
+    def reset_stats(self):
+        _check(_lib.mlk_ctx_reset_stats(self.h))
+
+    def kernel_stats(self):
+        cnt = C.c_int()
+        _check(_lib.mlk_ctx_kernel_stats(self.h, 0, C.byref(cnt), None, 0, None, None))
+        out = {}
+        buf = C.create_string_buffer(128)
+        for i in range(cnt.value):
+            l = C.c_int64()
+            ms = C.c_double()
+            _check(_lib.mlk_ctx_kernel_stats(self.h, i, None, buf, 128, C.byref(l), C.byref(ms)))
+            out[buf.value.decode()] = dict(launches=l.value, ms=ms.value)
+        return out
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.mlk_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Tree:
+    def __init__(self, h):
+        self.h = h
+        t, nn, n, d = C.c_int32(), C.c_int32(), C.c_int64(), C.c_int32()
+        _check(_lib.mlk_tree_info(h, C.byref(t), C.byref(nn), C.byref(n), C.byref(d)))
+        self.t, self.n_nodes, self.n, self.d = t.value, nn.value, n.value, d.value
+
+    def export(self):
+        nn, n, d = self.n_nodes, self.n, self.d
+        perm = np.empty(n, np.int64)
+        begin = np.empty(nn, np.int64)
+        end = np.empty(nn, np.int64)
+        depth = np.empty(nn, np.int32)
+        state = np.empty(nn, np.int32)
+        thr = np.empty(nn, np.float64)
+        dirs = np.empty((nn, d), np.float64)
+        _check(_lib.mlk_tree_export(self.h, _np(perm), _np(begin), _np(end), _np(depth), _np(state),
+                                    _np(thr), _np(dirs)))
+        return dict(perm=perm, begin=begin, end=end, depth=depth, state=state, thr=thr, dirs=dirs)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            _lib.mlk_tree_free(self.h)
+            self.h = None
+
+
+def build_tree(ctx, X, leaf_size, kind, directions=None):
+    Xp, keep = _ptr(X)
+    n, d = X.shape
+    Dp, keep2 = _ptr(directions)
+    nrows = 0 if directions is None else directions.shape[0]
+    h = C.c_void_p()
+    _check(_lib.mlk_build_tree(ctx.h, Xp, n, d, int(leaf_size), int(kind), Dp, nrows, C.byref(h)))
+    return Tree(h)
+
+
+class Basis:
+    def __init__(self, h, tree):
+        self.h = h
+        self.tree = tree
+        M, dim, nc = C.c_int32(), C.c_int64(), C.c_int32()
+        _check(_lib.mlk_basis_info(h, C.byref(M), C.byref(dim), C.byref(nc)))
+        self.M, self.dim, self.n_cells = M.value, dim.value, nc.value
+        self.cells = np.empty(self.n_cells, np.int32)
+        self.row_off = np.empty(self.n_cells + 1, np.int64)
+        _check(_lib.mlk_basis_export(h, _np(self.cells), _np(self.row_off), -1, None, None, None))
+
+    def block(self, node, size):
+        """(W_node, Phi_node) host copies; size = number of points of the node."""
+        pos = np.nonzero(self.cells == node)[0]
+        p = int(self.row_off[pos[0] + 1] - self.row_off[pos[0]]) if pos.size else 0
+        W = np.empty((p, size), np.float64)
+        Phi = np.empty((self.M, size), np.float64)
+        _check(_lib.mlk_basis_export(self.h, None, None, int(node), _np(W), _np(Phi), None))
+        return W, Phi
+
+    def L(self):
+        L = np.empty((self.M, self.tree.n), np.float64)
+        _check(_lib.mlk_basis_export(self.h, None, None, -1, None, None, _np(L)))
+        return L
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            _lib.mlk_basis_free(self.h)
+            self.h = None
+
+
+def build_basis(ctx, tree, w):
+    h = C.c_void_p()
+    _check(_lib.mlk_build_basis(ctx.h, tree.h, int(w), C.byref(h)))
+    return Basis(h, tree)
+
+
+def _vec_io(x, nvec_dim, out, out_cols):
+    xp, keep = _ptr(x)
+    nvec = 1 if x.ndim == 1 else x.shape[0]
+    if out is None:
+        res = np.empty((nvec, out_cols), np.float64)
+        op = _np(res)
+    else:
+        res = out
+        op, _ = _ptr(out)
+    return xp, keep, nvec, res, op
+
+
+def apply_wt(ctx, basis, v, out=None):
+    vp, keep, nvec, res, op = _vec_io(v, basis.dim, out, basis.tree.n)
+    _check(_lib.mlk_apply_wt(ctx.h, basis.h, vp, op, nvec))
+    return res
+
+
+def apply_w(ctx, basis, b, out=None):
+    bp, keep, nvec, res, op = _vec_io(b, basis.tree.n, out, basis.dim)
+    _check(_lib.mlk_apply_w(ctx.h, basis.h, bp, op, nvec))
+    return res
+
+
+class CW:
+    def __init__(self, h):
+        self.h = h
+        nc, nb, nnz = C.c_int32(), C.c_int64(), C.c_int64()
+        ent, fl, oent, ofl = C.c_double(), C.c_double(), C.c_double(), C.c_double()
+        _check(_lib.mlk_cw_info(h, C.byref(nc), C.byref(nb), C.byref(nnz), C.byref(ent), C.byref(fl),
+                                C.byref(oent), C.byref(ofl)))
+        self.n_cells, self.n_blocks, self.nnz = nc.value, nb.value, nnz.value
+        self.entries, self.flops = ent.value, fl.value
+        self.own_entries, self.own_flops = oent.value, ofl.value
+
+    def structure(self):
+        brow_ptr = np.empty(self.n_cells + 1, np.int32)
+        bcol = np.empty(self.n_blocks, np.int32)
+        val_off = np.empty(self.n_blocks + 1, np.int64)
+        _check(_lib.mlk_cw_export(self.h, _np(brow_ptr), _np(bcol), _np(val_off), None))
+        return brow_ptr, bcol, val_off
+
+    def export(self, out=None):
+        brow_ptr, bcol, val_off = self.structure()
+        vals = np.empty(self.nnz, np.float64) if out is None else out
+        vp, _ = _ptr(vals)
+        _check(_lib.mlk_cw_export(self.h, None, None, None, vp))
+        return dict(brow_ptr=brow_ptr, bcol=bcol, val_off=val_off, values=vals)
+
+    def stage_flops(self):
+        g, a, b = C.c_double(), C.c_double(), C.c_double()
+        _check(_lib.mlk_cw_flops(self.h, C.byref(g), C.byref(a), C.byref(b)))
+        return dict(gram=g.value, contract1=a.value, contract2=b.value)
+
+    def owner(self):
+        o = np.empty(self.n_blocks, np.int32)
+        _check(_lib.mlk_cw_owner(self.h, _np(o)))
+        return o
+
+    def shard_len(self):
+        a, b = C.c_int64(), C.c_int64()
+        _check(_lib.mlk_cw_shard_len(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def values_ptr(self):
+        p = C.c_void_p()
+        _check(_lib.mlk_cw_values_device(self.h, C.byref(p)))
+        return p.value
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            _lib.mlk_cw_free(self.h)
+            self.h = None
+
+
+def assemble_cw(ctx, tree, basis, kernel, sparsity, precision=PREC_FP64):
+    h = C.c_void_p()
+    ks = _kspec(kernel)
+    sp = sparsity if isinstance(sparsity, SparsitySpec) else SparsitySpec(int(sparsity["mode"]),
+                                                                           float(sparsity.get("tau", 0.0)))
+    _check(_lib.mlk_assemble_cw(ctx.h, tree.h, basis.h, C.byref(ks), C.byref(sp), int(precision), C.byref(h)))
+    return CW(h)
+
+
+def gather_cw(ctx, cw, group=None):
+    """All-gather of the BSR shards over the caller's process group (NCCL on GPUs):
+    pack this rank's blocks, all_gather_into_tensor, unpack into BSR order."""
+    import torch
+    import torch.distributed as dist
+
+    if ctx.nranks == 1:
+        return
+    _, mx = cw.shard_len()
+    dev = torch.device("cuda", ctx.device)
+    send = torch.empty(max(mx, 1), dtype=torch.float64, device=dev)
+    _check(_lib.mlk_cw_pack(ctx.h, cw.h, C.c_void_p(send.data_ptr())))
+    recv = torch.empty(ctx.nranks * max(mx, 1), dtype=torch.float64, device=dev)
+    dist.all_gather_into_tensor(recv, send, group=group)
+    torch.cuda.current_stream(dev).synchronize()
+    _check(_lib.mlk_cw_unpack(ctx.h, cw.h, C.c_void_p(recv.data_ptr())))
+
+
+def pack_cw(ctx, cw, dst):
+    _check(_lib.mlk_cw_pack(ctx.h, cw.h, C.c_void_p(dst.data_ptr())))
+
+
+def unpack_cw(ctx, cw, gathered):
+    _check(_lib.mlk_cw_unpack(ctx.h, cw.h, C.c_void_p(gathered.data_ptr())))
+
+
+def cov_matvec(ctx, tree, kernel, a, out=None):
+    ap, keep, nvec, res, op = _vec_io(a, tree.n, out, tree.n)
+    ks = _kspec(kernel)
+    _check(_lib.mlk_cov_matvec(ctx.h, tree.h, C.byref(ks), ap, op, nvec))
+    return res
+
+
+def cw_matvec(ctx, tree, basis, kernel, cw, mode, v, out=None, allreduce=True, group=None):
+    """y = C_W v.  With nranks > 1 the partial results are sum-allreduced over `group`
+    (torch.distributed, NCCL) unless allreduce=False."""
+    vp, keep, nvec, res, op = _vec_io(v, basis.dim, out, basis.dim)
+    ks = _kspec(kernel) if kernel is not None else kernel_spec(0, 1.0)
+    _check(_lib.mlk_cw_matvec(ctx.h, tree.h, basis.h, C.byref(ks), cw.h if cw is not None else None,
+                              int(mode), vp, op, nvec))
+    if ctx.nranks > 1 and allreduce:
+        import torch
+        import torch.distributed as dist
+
+        if isinstance(res, np.ndarray):
+            t = torch.from_numpy(res).to(torch.device("cuda", ctx.device))
+            dist.all_reduce(t, group=group)
+            res[...] = t.cpu().numpy()
+        else:
+            dist.all_reduce(res, group=group)
+    return res
+
+
+def partition_lpt(cost, nranks):
+    cost = np.ascontiguousarray(cost, dtype=np.float64)
+    owner = np.empty(cost.size, np.int32)
+    _check(_lib.mlk_partition_lpt(_np(cost), cost.size, int(nranks), _np(owner)))
+    return owner
+
+
+def shard_plan(val_off, owner, nranks):
+    """(shard_off[n], shard_len[nranks]) -- the gather layout of mlk_assemble_cw (host only)."""
+    val_off = np.ascontiguousarray(val_off, dtype=np.int64)
+    owner = np.ascontiguousarray(owner, dtype=np.int32)
+    n = owner.size
+    so = np.empty(n, np.int64)
+    sl = np.empty(int(nranks), np.int64)
+    _check(_lib.mlk_shard_plan(_np(val_off), _np(owner), n, int(nranks), _np(so), _np(sl)))
+    return so, sl

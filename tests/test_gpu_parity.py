@@ -1,0 +1,334 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle on the same seeded inputs.
+
+Bars: tree permutation, thresholds, cell lists, row offsets and the
+admitted pair list bit-exact; W blocks <= 1e-11 relative Frobenius per cell; C_W blocks
+<= 1e-11 relative Frobenius per block (north_star), except where plain FP64 is at its floor
+(cfg1, reading H1), where the DD mode carries the 1e-11 bar against a long-double oracle and
+the FP64 mode is held to 1e-13 of |W_a| |C_ab| |W_b|; C_W v <= 1e-11 relative.
+"""
+import numpy as np
+import pytest
+
+import workloads as wl
+from oracle import admission as OA
+from oracle import assemble as OAs
+from oracle import basis as OB
+from oracle import covariance as OC
+from oracle import matvec as OM
+from oracle import tree as OT
+
+pytestmark = pytest.mark.gpu
+
+TOL_BLOCK = 1e-11
+
+
+@pytest.fixture(scope="module")
+def mlk():
+    from paper_1701_00285_b200 import mlk as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def ctx(mlk):
+    return mlk.Ctx(0)
+
+
+def _setup(n, d, leaf, kind, points="uniform", seed=0):
+    X = wl.points(points, n, d, seed)
+    t = wl.tree_levels(n, leaf)
+    dirs = wl.directions(2 ** t - 1, d, seed) if kind == 1 else None
+    return X, dirs
+
+
+def _tree_both(mlk, ctx, X, leaf, kind, dirs):
+    g = mlk.build_tree(ctx, X, leaf, kind, dirs)
+    o = OT.build_tree(X, leaf, kind, dirs)
+    return g, o
+
+
+def _check_tree(g, o):
+    e = g.export()
+    assert g.t == o.t and g.n_nodes == o.n_nodes
+    assert np.array_equal(e["perm"], o.perm)
+    st = np.where(o.exists, np.where(o.is_leaf, 1, 0), -1)
+    assert np.array_equal(e["state"], st)
+    ex = o.exists
+    assert np.array_equal(e["begin"][ex], o.begin[ex]) and np.array_equal(e["end"][ex], o.end[ex])
+    assert np.array_equal(e["depth"][ex], o.depth[ex])
+    internal = o.exists & ~o.is_leaf
+    assert np.array_equal(e["thr"][internal], o.thr[internal])          # bit-exact thresholds
+    assert np.array_equal(e["dirs"][internal], o.dirs[internal])
+
+
+def _block_errs(got, ref):
+    errs = []
+    for k in range(len(ref.val_off) - 1):
+        a, b = ref.val_off[k], ref.val_off[k + 1]
+        r = np.asarray(ref.values[a:b], dtype=np.float64)
+        nr = np.linalg.norm(r)
+        errs.append(np.linalg.norm(got[a:b] - r) / nr if nr > 0 else np.linalg.norm(got[a:b]))
+    return np.array(errs)
+
+
+# --------------------------------------------------------------------------------- tree
+@pytest.mark.parametrize("n,d,leaf,kind,points", [
+    (1024, 2, 32, 0, "uniform"),       # cfg1 shape (kD)
+    (1000, 3, 32, 0, "uniform"),       # ragged kD
+    (4099, 10, 100, 1, "uniform"),     # ragged RP
+    (32768, 10, 256, 1, "uniform"),    # cfg2 full size
+    (131072, 20, 256, 1, "normal"),    # cfg3 full size
+    (40, 2, 64, 0, "uniform"),         # root is a leaf
+])
+def test_tree_bit_exact(mlk, ctx, n, d, leaf, kind, points):
+    X, dirs = _setup(n, d, leaf, kind, points)
+    g, o = _tree_both(mlk, ctx, X, leaf, kind, dirs)
+    _check_tree(g, o)
+
+
+def test_tree_cfg4_mixture_bit_exact(mlk, ctx):
+    inp = wl.make("cfg4")
+    c = inp["cfg"]
+    g, o = _tree_both(mlk, ctx, inp["X"], c["leaf"], c["tree"], inp["dirs"])
+    _check_tree(g, o)
+
+
+def test_duplicate_points_rejected(mlk, ctx):
+    X = wl.points("uniform", 300, 3)
+    X[17] = X[200]
+    with pytest.raises(mlk.DuplicatePoints):
+        mlk.build_tree(ctx, X, 16, 0)
+    with pytest.raises(mlk.DuplicatePoints):
+        mlk.build_tree(ctx, np.vstack([X[:30], X[5:6]]), 64, 0)      # root is a leaf
+
+
+def test_invalid_arguments(mlk, ctx):
+    X = wl.points("uniform", 100, 3)
+    with pytest.raises(mlk.MlkError):
+        mlk.build_tree(ctx, X, 0, 0)
+    with pytest.raises(mlk.MlkError):
+        mlk.build_tree(ctx, X, 8, 1, None)        # RP needs directions
+    tr = mlk.build_tree(ctx, X, 8, 0)
+    with pytest.raises(mlk.RankDeficient):
+        mlk.build_basis(ctx, tr, 3)               # M = 20 > leaf points
+
+
+# --------------------------------------------------------------------------------- basis
+@pytest.mark.parametrize("n,d,w,leaf,kind,points", [
+    (1024, 2, 2, 32, 0, "uniform"),    # cfg1
+    (1000, 3, 2, 32, 0, "uniform"),    # ragged
+    (4096, 10, 2, 256, 1, "uniform"),  # cfg2 shape, fewer levels
+    (8192, 20, 1, 256, 1, "normal"),   # cfg3 shape
+    (4096, 50, 1, 512, 1, "mixture"),  # cfg4 shape
+])
+def test_basis_parity_and_invariants(mlk, ctx, n, d, w, leaf, kind, points):
+    X, dirs = _setup(n, d, leaf, kind, points)
+    g, o = _tree_both(mlk, ctx, X, leaf, kind, dirs)
+    gb = mlk.build_basis(ctx, g, w)
+    ob = OB.build_basis(X, o, w)
+    assert gb.M == ob.M and gb.dim == ob.dim == n - ob.M
+    assert np.array_equal(gb.cells, np.array(ob.cells))
+    assert np.array_equal(gb.row_off[:-1], np.array([ob.row_off[q] for q in ob.cells]))
+    worst = 0.0
+    for q in ob.cells:
+        Wg, Pg = gb.block(q, int(o.end[q] - o.begin[q]))
+        worst = max(worst, np.linalg.norm(Wg - ob.W[q]) / np.linalg.norm(ob.W[q]))
+    assert worst <= TOL_BLOCK, worst
+    # invariants on the GPU basis itself: P P^T = I, W P(X) = 0
+    if n <= 4096:
+        Wd = np.zeros((gb.dim, n))
+        for i, q in enumerate(gb.cells):
+            Wg, _ = gb.block(q, int(o.end[q] - o.begin[q]))
+            Wd[gb.row_off[i]:gb.row_off[i + 1], o.begin[q]:o.end[q]] = Wg
+        Pm = np.vstack([Wd, gb.L()])
+        assert np.max(np.abs(Pm @ Pm.T - np.eye(n))) < 1e-12
+        from oracle.index_set import monomials
+        Mx = monomials(X[o.perm], ob.exps)
+        assert np.max(np.abs(Wd @ Mx)) <= 1e-12 * np.max(np.abs(Mx))
+
+
+# --------------------------------------------------------------------------------- admission
+@pytest.mark.parametrize("n,d,leaf,kind,tau,points", [
+    (4096, 10, 64, 1, 0.0, "uniform"),
+    (4096, 10, 64, 1, 0.05, "uniform"),
+    (2000, 3, 16, 1, 0.02, "normal"),
+    (1024, 2, 32, 0, 0.1, "uniform"),
+    (32768, 10, 256, 1, 1e-6, "uniform"),   # cfg2 at the paper's tau
+])
+def test_admission_bit_exact(mlk, ctx, n, d, leaf, kind, tau, points):
+    X, dirs = _setup(n, d, leaf, kind, points)
+    g, o = _tree_both(mlk, ctx, X, leaf, kind, dirs)
+    w = 1
+    gb = mlk.build_basis(ctx, g, w)
+    ob = OB.build_basis(X, o, w)
+    pairs = OA.admitted_pairs(X, o, ob, OA.PAIRS_PAPER_TAU, tau)
+    cw = mlk.assemble_cw(ctx, g, gb, dict(family=0, rho=1.0), dict(mode=1, tau=tau))
+    brow_ptr, bcol, val_off = cw.structure()
+    _, _, rp, bc, vo = OAs.bsr_structure(ob, pairs)
+    assert np.array_equal(brow_ptr, rp) and np.array_equal(bcol, bc) and np.array_equal(val_off, vo)
+    if tau == 0.0:
+        assert cw.n_blocks == OA.ancestor_pattern_count(o, ob)
+
+
+# --------------------------------------------------------------------------------- assembly
+FAMS = [(OC.MATERN_12, 0.5), (OC.MATERN_32, 1.0), (OC.MATERN_52, 2.0), (OC.GAUSSIAN, 1.5)]
+
+
+@pytest.mark.parametrize("fam,rho", FAMS)
+@pytest.mark.parametrize("n,d,w,leaf,kind,mode,tau,points", [
+    (2048, 10, 2, 128, 1, 0, 0.0, "uniform"),     # cfg2 shape, ALL pairs
+    (1000, 3, 1, 40, 0, 1, 0.05, "normal"),       # ragged, tau
+    (4096, 20, 1, 256, 1, 1, 1e-7, "normal"),     # cfg3 shape
+])
+def test_assembly_fp64_parity(mlk, ctx, fam, rho, n, d, w, leaf, kind, mode, tau, points):
+    X, dirs = _setup(n, d, leaf, kind, points)
+    g, o = _tree_both(mlk, ctx, X, leaf, kind, dirs)
+    gb = mlk.build_basis(ctx, g, w)
+    ob = OB.build_basis(X, o, w)
+    kern = dict(family=fam, rho=rho, sigma2=1.3, nugget=1e-3 if fam == OC.GAUSSIAN else 0.0)
+    pairs = OA.admitted_pairs(X, o, ob, mode, tau)
+    ref = OAs.assemble(X, o, ob, kern, pairs)
+    cw = mlk.assemble_cw(ctx, g, gb, kern, dict(mode=mode, tau=tau))
+    got = cw.export()
+    assert np.array_equal(got["val_off"], ref.val_off)
+    errs = _block_errs(got["values"], ref)
+    assert errs.max() <= TOL_BLOCK, (errs.max(), int(errs.argmax()))
+
+
+def test_assembly_cfg4_shape_parity(mlk, ctx):
+    X, dirs = _setup(8192, 50, 512, 1, "mixture")
+    g, o = _tree_both(mlk, ctx, X, 512, 1, dirs)
+    gb = mlk.build_basis(ctx, g, 1)
+    ob = OB.build_basis(X, o, 1)
+    kern = dict(family=OC.MATERN_12, rho=3.0)
+    pairs = OA.admitted_pairs(X, o, ob, 1, 1e-7)
+    ref = OAs.assemble(X, o, ob, kern, pairs)
+    got = mlk.assemble_cw(ctx, g, gb, kern, dict(mode=1, tau=1e-7)).export()
+    assert np.array_equal(got["val_off"], ref.val_off)
+    assert _block_errs(got["values"], ref).max() <= TOL_BLOCK
+
+
+def test_cfg1_dd_mode_against_longdouble_oracle(mlk, ctx):
+    inp = wl.make("cfg1")
+    c = inp["cfg"]
+    X = inp["X"]
+    g, o = _tree_both(mlk, ctx, X, c["leaf"], c["tree"], None)
+    gb = mlk.build_basis(ctx, g, c["w"])
+    ob = OB.build_basis(X, o, c["w"])
+    kern = wl.kernel_dict(c)
+    pairs = OA.admitted_pairs(X, o, ob, OA.PAIRS_ALL)
+    ref = OAs.assemble(X, o, ob, kern, pairs, dtype=np.longdouble)
+    dd = mlk.assemble_cw(ctx, g, gb, kern, dict(mode=0, tau=0.0), precision=mlk.PREC_DD).export()
+    errs = _block_errs(dd["values"], ref)
+    assert errs.max() <= TOL_BLOCK, errs.max()
+    # FP64 mode: held to the conditioning-normalised bound |dB| <= 1e-13 |W_a| |C_ab| |W_b|
+    f64 = mlk.assemble_cw(ctx, g, gb, kern, dict(mode=0, tau=0.0)).export()
+    for k, (a, b) in enumerate(pairs):
+        lo, hi = ref.val_off[k], ref.val_off[k + 1]
+        ia = o.perm[o.begin[a]:o.end[a]]
+        ib = o.perm[o.begin[b]:o.end[b]]
+        Cab = OC.cov(X[ia], X[ib], ia, ib, kern["family"], kern["rho"])
+        scale = np.linalg.norm(ob.W[a]) * np.linalg.norm(Cab) * np.linalg.norm(ob.W[b])
+        assert np.linalg.norm(f64["values"][lo:hi] - np.asarray(ref.values[lo:hi], float)) <= 1e-13 * scale
+
+
+def test_identity_pin_on_gpu(mlk, ctx):
+    inp = wl.make("cfg1")
+    X = inp["X"]
+    g = mlk.build_tree(ctx, X, 32, 0)
+    gb = mlk.build_basis(ctx, g, 2)
+    for prec in (mlk.PREC_FP64, mlk.PREC_DD):
+        cw = mlk.assemble_cw(ctx, g, gb, dict(family=OC.GAUSSIAN, rho=1e-5), dict(mode=0), precision=prec)
+        D = OAs.bsr_to_dense(OAs.BSR([0] * gb.n_cells, gb.row_off, *[cw.export()[k] for k in
+                                                                   ("brow_ptr", "bcol", "val_off", "values")]))
+        assert np.max(np.abs(D - np.eye(gb.dim))) < 1e-13
+
+
+def test_cfg2_full_size_sampled_blocks(mlk, ctx):
+    """cfg2 at BASELINE size in the bench's launch configuration; blocks sampled and recomputed
+    one by one by the oracle (root-root, leaf self blocks, random admitted pairs)."""
+    inp = wl.make("cfg2")
+    c = inp["cfg"]
+    X = inp["X"]
+    g, o = _tree_both(mlk, ctx, X, c["leaf"], c["tree"], inp["dirs"])
+    gb = mlk.build_basis(ctx, g, c["w"])
+    ob = OB.build_basis(X, o, c["w"])
+    kern = wl.kernel_dict(c)
+    pairs = OA.admitted_pairs(X, o, ob, c["pairs"], c["tau"])
+    cw = mlk.assemble_cw(ctx, g, gb, kern, dict(mode=c["pairs"], tau=c["tau"]))
+    got = cw.export()
+    _, _, brow_ptr, bcol, val_off = OAs.bsr_structure(ob, pairs)
+    assert np.array_equal(got["val_off"], val_off) and len(pairs) == 2074
+    rng = np.random.default_rng([0, 3])
+    idx = set(rng.choice(len(pairs), 24, replace=False).tolist())
+    idx |= {k for k, (a, b) in enumerate(pairs) if a == 0 or b == 0}
+    idx |= {k for k, (a, b) in enumerate(pairs) if a == b}
+    idx = sorted(idx)[:60]
+    for k in idx:
+        a, b = pairs[k]
+        ref = OAs.block(X, o, ob, kern, a, b).ravel()
+        e = np.linalg.norm(got["values"][val_off[k]:val_off[k + 1]] - ref) / np.linalg.norm(ref)
+        assert e <= TOL_BLOCK, (k, a, b, e)
+
+
+def test_assembly_deterministic(mlk, ctx):
+    X, dirs = _setup(4096, 10, 128, 1)
+    g = mlk.build_tree(ctx, X, 128, 1, dirs)
+    gb = mlk.build_basis(ctx, g, 2)
+    k = dict(family=1, rho=1.0)
+    a = mlk.assemble_cw(ctx, g, gb, k, dict(mode=1, tau=1e-3)).export()["values"]
+    b = mlk.assemble_cw(ctx, g, gb, k, dict(mode=1, tau=1e-3)).export()["values"]
+    assert np.array_equal(a, b)
+
+
+# --------------------------------------------------------------------------------- matvec
+@pytest.mark.parametrize("fam,rho", FAMS)
+def test_matvec_exact_and_bsr(mlk, ctx, fam, rho):
+    X, dirs = _setup(2048, 10, 128, 1)
+    g, o = _tree_both(mlk, ctx, X, 128, 1, dirs)
+    gb = mlk.build_basis(ctx, g, 2)
+    ob = OB.build_basis(X, o, 2)
+    kern = dict(family=fam, rho=rho, nugget=1e-4 if fam == OC.GAUSSIAN else 0.0)
+    v = wl.vectors(3, gb.dim, seed=1)
+    y = mlk.cw_matvec(ctx, g, gb, kern, None, mlk.MATVEC_EXACT, v)
+    yr = OM.cw_matvec_exact(X, o, ob, kern, v)
+    assert np.linalg.norm(y - yr) <= 1e-11 * np.linalg.norm(yr)
+    a = mlk.apply_wt(ctx, gb, v)
+    assert np.max(np.abs(a - OM.apply_wt(o, ob, v))) <= 1e-12 * np.max(np.abs(a))
+    b = mlk.cov_matvec(ctx, g, kern, a)
+    br = OM.cov_matvec(X, o, kern, a)
+    assert np.linalg.norm(b - br) <= 1e-12 * np.linalg.norm(br)
+    pairs = OA.admitted_pairs(X, o, ob, OA.PAIRS_PAPER_TAU, 0.02)
+    cw = mlk.assemble_cw(ctx, g, gb, kern, dict(mode=1, tau=0.02))
+    yb = mlk.cw_matvec(ctx, g, gb, kern, cw, mlk.MATVEC_BSR, v)
+    ref = OAs.assemble(X, o, ob, kern, pairs)
+    ybr = OM.cw_matvec_bsr(ref, v)
+    assert np.linalg.norm(yb - ybr) <= 1e-11 * np.linalg.norm(ybr)
+    # ALL pairs: BSR product == exact product
+    cwa = mlk.assemble_cw(ctx, g, gb, kern, dict(mode=0))
+    ya = mlk.cw_matvec(ctx, g, gb, kern, cwa, mlk.MATVEC_BSR, v)
+    assert np.linalg.norm(ya - yr) <= 1e-11 * np.linalg.norm(yr)
+
+
+def test_matvec_cfg3_sampled_rows(mlk, ctx):
+    """cfg3 at full size with its 10 N(0,1) vectors: apply_wt / apply_w in full, C a on 512
+    seeded rows (the host cannot do the 1.7e10-entry product in test time)."""
+    inp = wl.make("cfg3")
+    c = inp["cfg"]
+    X = inp["X"]
+    g, o = _tree_both(mlk, ctx, X, c["leaf"], c["tree"], inp["dirs"])
+    gb = mlk.build_basis(ctx, g, c["w"])
+    ob = OB.build_basis(X, o, c["w"])
+    kern = wl.kernel_dict(c)
+    v = wl.vectors(10, gb.dim)
+    a = mlk.apply_wt(ctx, gb, v)
+    ar = OM.apply_wt(o, ob, v)
+    assert np.max(np.abs(a - ar)) <= 1e-11 * np.max(np.abs(ar))
+    b = mlk.cov_matvec(ctx, g, kern, a)
+    rows = np.random.default_rng([0, 3]).choice(c["n"], 512, replace=False)
+    br = OM.cov_matvec(X, o, kern, a, rows=rows)
+    assert np.linalg.norm(b[:, rows] - br) <= 1e-11 * np.linalg.norm(br)
+    y = mlk.apply_w(ctx, gb, b)
+    yr = OM.apply_w(o, ob, b)
+    assert np.linalg.norm(y - yr) <= 1e-12 * np.linalg.norm(yr)
+    y2 = mlk.cw_matvec(ctx, g, gb, kern, None, mlk.MATVEC_EXACT, v)
+    assert np.array_equal(y, y2)
