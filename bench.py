@@ -270,12 +270,12 @@ def main():
         step(Xh.numpy(), Dh.numpy() if Dh is not None else None, vh.numpy(), valsh.numpy()[:nnz], yh.numpy())
         torch.cuda.synchronize()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
-    e2e_total = float(np.sum(e2e_ms))
-    if ws > 1:
+    e2e_total = float(np.sum(e2e_ms)) if e2e_ms else float("nan")
+    if ws > 1 and e2e_ms:
         t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_total = float(t.item())
-    e2e_val = entries * args.e2e_steps / (e2e_total * 1e-3)
+    e2e_val = entries * args.e2e_steps / (e2e_total * 1e-3) if e2e_ms else None
     h2d = inp["X"].nbytes + (dirs.nbytes if dirs is not None else 0) + vh.numel() * 8
     d2h = nnz * 8 + yh.numel() * 8
 
@@ -314,7 +314,8 @@ def main():
             "entries_per_step": entries, "blocks_nnz": nnz,
             "clocks": clocks, "gpu_launches": launches,
             "e2e": {"value": e2e_val, "unit": "covariance pairs/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_total / args.e2e_steps},
+                    "d2h_bytes_per_step": int(d2h),
+                    "ms_per_step": e2e_total / args.e2e_steps if e2e_ms else None},
             "cpu_baseline": cpu,
         }
         print(json.dumps(line))

@@ -344,6 +344,17 @@ mlk_status mlk_assemble_cw(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const ml
 void mlk_cw_free(mlk_cw cw) {
   if (!cw) return;
   cudaSetDevice(cw->device);
+  // the creating context's stream may already be gone: drain the device, free on stream 0
+  cudaDeviceSynchronize();
+  cw->values.s = nullptr;
+  cw->shard.s = nullptr;
+  cw->brow_d.s = nullptr;
+  cw->bcol_d.s = nullptr;
+  cw->owner_d.s = nullptr;
+  cw->val_off_d.s = nullptr;
+  cw->shard_off_d.s = nullptr;
+  cw->csc_ptr_d.s = nullptr;
+  cw->csc_blk_d.s = nullptr;
   delete cw;
 }
 

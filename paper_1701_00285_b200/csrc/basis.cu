@@ -379,6 +379,10 @@ mlk_status mlk_build_basis(mlk_ctx ctx, mlk_tree tree, int32_t w, mlk_basis* out
 void mlk_basis_free(mlk_basis basis) {
   if (!basis) return;
   cudaSetDevice(basis->device);
+  // the creating context's stream may already be gone: drain the device, free on stream 0
+  cudaDeviceSynchronize();
+  basis->W.s = nullptr;
+  basis->Phi.s = nullptr;
   delete basis;
 }
 

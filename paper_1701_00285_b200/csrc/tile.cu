@@ -15,6 +15,7 @@
 #include <cmath>
 
 #include "dmma.cuh"
+#include "fastmath.cuh"
 #include "tile.cuh"
 
 namespace mlk {
@@ -74,13 +75,13 @@ void make_tile_units(std::vector<TileUnit>& out, int64_t a_begin, int32_t s_a, i
 namespace {
 
 template <int FAM>
-__device__ __forceinline__ double corr(double r2, double c1) {
-  if (FAM == MLK_GAUSSIAN) return exp(-r2 * c1);
-  double z = sqrt(r2) * c1;
-  double e = exp(-z);
+__device__ __forceinline__ double corr(double r2, double c1, const double* tab) {
+  if (FAM == MLK_GAUSSIAN) return exp_neg(-r2 * c1, tab);
+  double z = sqrt_pos(r2) * c1;
+  double e = exp_neg(-z, tab);
   if (FAM == MLK_MATERN_12) return e;
-  if (FAM == MLK_MATERN_32) return (1.0 + z) * e;
-  return fma(z, fma(z, 1.0 / 3.0, 1.0), 1.0) * e;  // 1 + z + z^2/3
+  if (FAM == MLK_MATERN_32) return fma(z, e, e);                  // (1 + z) e^{-z}
+  return fma(z, fma(z, 1.0 / 3.0, 1.0), 1.0) * e;                // (1 + z + z^2/3) e^{-z}
 }
 
 template <int RQ>
@@ -92,13 +93,15 @@ struct TileCfg {
 __host__ __device__ constexpr int stage_doubles(int rq, int bn, int dp) { return bn * dp + bn + 8 * rq * bn; }
 
 template <int RQ, int FAM>
-__global__ void __launch_bounds__(128) k_tile_contract(const TileUnit* __restrict__ units, int n_units,
+__global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4) k_tile_contract(const TileUnit* __restrict__ units, int n_units,
                                                        int* __restrict__ counter, const double* __restrict__ Xt,
                                                        const double* __restrict__ norm2, int dp, KernelParams kp) {
   constexpr int BN = TileCfg<RQ>::BN;
   constexpr int WROWS = TileCfg<RQ>::WROWS;
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_unit;
+  __shared__ double s_tab[16];
+  if (threadIdx.x < 16) s_tab[threadIdx.x] = kExp2Tab16[threadIdx.x];
   const int sd = stage_doubles(RQ, BN, dp);
   double* As = sm;                  // 32 x dp
   double* An = sm + 32 * dp;        // 32
@@ -178,35 +181,54 @@ __global__ void __launch_bounds__(128) k_tile_contract(const TileUnit* __restric
       const double* Ns = Xs + BN * dp;
       const double* Ws = Ns + BN;
       const int b0 = s * BN;
+      constexpr int T = BN / 8;
+      // 1. Gram S = X_a X_b^T for the T sub-tiles (independent accumulator chains)
+      double g[T][2];
 #pragma unroll
-      for (int t = 0; t < BN / 8; t++) {
-        double g0 = 0.0, g1 = 0.0;
-        for (int ks = 0; ks < ks_n; ks++) {
-          double a = As[ar * dp + 4 * ks + (lane & 3)];
-          double b = Xs[(8 * t + (lane >> 2)) * dp + 4 * ks + (lane & 3)];
-          dmma_8x8x4(g0, g1, a, b);
+      for (int t = 0; t < T; t++) g[t][0] = g[t][1] = 0.0;
+      for (int ks = 0; ks < ks_n; ks++) {
+        const double a = As[ar * dp + 4 * ks + (lane & 3)];
+#pragma unroll
+        for (int t = 0; t < T; t++) {
+          const double b = Xs[(8 * t + (lane >> 2)) * dp + 4 * ks + (lane & 3)];
+          dmma_8x8x4(g[t][0], g[t][1], a, b);
         }
+      }
+      // 2. covariances in registers (Gram identity, clamp, same-site fix, closed form)
+      double cv[T][2];
+#pragma unroll
+      for (int t = 0; t < T; t++) {
         const int col = 8 * t + 2 * (lane & 3);
-        double cv[2];
 #pragma unroll
         for (int e = 0; e < 2; e++) {
-          double g = e ? g1 : g0;
-          double r2 = fma(-2.0, g, na + Ns[col + e]);
-          r2 = fmax(r2, 0.0);
-          const int64_t gb = u.b_begin + b0 + col + e;
-          const bool same = (gb == ga);
+          double r2 = fmax(fma(-2.0, g[t][e], na + Ns[col + e]), 0.0);
+          const bool same = (u.b_begin + b0 + col + e) == ga;
           if (same) r2 = 0.0;
-          double v = kp.sigma2 * corr<FAM>(r2, kp.c1);
-          if (same) v += kp.nugget;
-          cv[e] = v;
+          double v = kp.sigma2 * corr<FAM>(r2, kp.c1, s_tab);
+          cv[t][e] = same ? v + kp.nugget : v;
         }
+      }
+      // 3./4. accumulator entries are the A fragments of k-steps s = 0, 1; W_b fragments
+      // are loaded 4 n-tiles at a time so consecutive DMMAs are independent
 #pragma unroll
-        for (int q = 0; q < RQ; q++) {
-          const int rho = 8 * q + (lane >> 2);
-          const int ch = 4 * t + (lane & 3);
-          const double2 w2 = *reinterpret_cast<const double2*>(Ws + rho * BN + 2 * (ch ^ ((rho & 1) << 2)));
-          dmma_8x8x4(acc[q][0], acc[q][1], cv[0], w2.x);
-          dmma_8x8x4(acc[q][0], acc[q][1], cv[1], w2.y);
+      for (int t = 0; t < T; t++) {
+#pragma unroll
+        for (int q0 = 0; q0 < RQ; q0 += 4) {
+          double2 w[4];
+#pragma unroll
+          for (int qq = 0; qq < 4; qq++) {
+            if (q0 + qq < RQ) {
+              const int rho = 8 * (q0 + qq) + (lane >> 2);
+              const int ch = 4 * t + (lane & 3);
+              w[qq] = *reinterpret_cast<const double2*>(Ws + rho * BN + 2 * (ch ^ ((rho & 1) << 2)));
+            }
+          }
+#pragma unroll
+          for (int qq = 0; qq < 4; qq++)
+            if (q0 + qq < RQ) dmma_8x8x4(acc[q0 + qq][0], acc[q0 + qq][1], cv[t][0], w[qq].x);
+#pragma unroll
+          for (int qq = 0; qq < 4; qq++)
+            if (q0 + qq < RQ) dmma_8x8x4(acc[q0 + qq][0], acc[q0 + qq][1], cv[t][1], w[qq].y);
         }
       }
       __syncthreads();

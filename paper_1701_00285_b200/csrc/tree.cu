@@ -387,6 +387,14 @@ mlk_status mlk_build_tree(mlk_ctx ctx, const double* X, int64_t n, int32_t d, in
 void mlk_tree_free(mlk_tree tree) {
   if (!tree) return;
   cudaSetDevice(tree->device);
+  // the creating context's stream may already be gone: drain the device, free on stream 0
+  cudaDeviceSynchronize();
+  tree->perm_d.s = nullptr;
+  tree->X.s = nullptr;
+  tree->Xt.s = nullptr;
+  tree->norm2.s = nullptr;
+  tree->thr_d.s = nullptr;
+  tree->dir_d.s = nullptr;
   delete tree;
 }
 

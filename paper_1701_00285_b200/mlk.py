@@ -192,8 +192,9 @@ class Ctx:
 
 
 class Tree:
-    def __init__(self, h):
+    def __init__(self, h, ctx=None):
         self.h = h
+        self.ctx = ctx  # keeps the context (and its stream) alive while the tree lives
         t, nn, n, d = C.c_int32(), C.c_int32(), C.c_int64(), C.c_int32()
         _check(_lib.mlk_tree_info(h, C.byref(t), C.byref(nn), C.byref(n), C.byref(d)))
         self.t, self.n_nodes, self.n, self.d = t.value, nn.value, n.value, d.value
@@ -224,13 +225,14 @@ def build_tree(ctx, X, leaf_size, kind, directions=None):
     nrows = 0 if directions is None else directions.shape[0]
     h = C.c_void_p()
     _check(_lib.mlk_build_tree(ctx.h, Xp, n, d, int(leaf_size), int(kind), Dp, nrows, C.byref(h)))
-    return Tree(h)
+    return Tree(h, ctx)
 
 
 class Basis:
-    def __init__(self, h, tree):
+    def __init__(self, h, tree, ctx=None):
         self.h = h
         self.tree = tree
+        self.ctx = ctx
         M, dim, nc = C.c_int32(), C.c_int64(), C.c_int32()
         _check(_lib.mlk_basis_info(h, C.byref(M), C.byref(dim), C.byref(nc)))
         self.M, self.dim, self.n_cells = M.value, dim.value, nc.value
@@ -261,7 +263,7 @@ class Basis:
 def build_basis(ctx, tree, w):
     h = C.c_void_p()
     _check(_lib.mlk_build_basis(ctx.h, tree.h, int(w), C.byref(h)))
-    return Basis(h, tree)
+    return Basis(h, tree, ctx)
 
 
 def _vec_io(x, nvec_dim, out, out_cols):
@@ -289,8 +291,9 @@ def apply_w(ctx, basis, b, out=None):
 
 
 class CW:
-    def __init__(self, h):
+    def __init__(self, h, owners=()):
         self.h = h
+        self._owners = owners  # ctx, tree, basis outlive the matrix
         nc, nb, nnz = C.c_int32(), C.c_int64(), C.c_int64()
         ent, fl, oent, ofl = C.c_double(), C.c_double(), C.c_double(), C.c_double()
         _check(_lib.mlk_cw_info(h, C.byref(nc), C.byref(nb), C.byref(nnz), C.byref(ent), C.byref(fl),
@@ -345,7 +348,7 @@ def assemble_cw(ctx, tree, basis, kernel, sparsity, precision=PREC_FP64):
     sp = sparsity if isinstance(sparsity, SparsitySpec) else SparsitySpec(int(sparsity["mode"]),
                                                                            float(sparsity.get("tau", 0.0)))
     _check(_lib.mlk_assemble_cw(ctx.h, tree.h, basis.h, C.byref(ks), C.byref(sp), int(precision), C.byref(h)))
-    return CW(h)
+    return CW(h, (ctx, tree, basis))
 
 
 def gather_cw(ctx, cw, group=None):
