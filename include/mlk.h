@@ -163,15 +163,21 @@ typedef enum { MLK_PREC_FP64 = 0, MLK_PREC_DD = 1 } mlk_precision;
  *  block rows/cols = cells in C_W order; each admitted unordered pair is stored once as
  *  (row, col) with row <= col in C_W order, row-major p_row x p_col, blocks sorted by
  *  (row, col).  Every block is computed exactly (no approximation inside a block).
- * With nranks > 1 this rank computes only the blocks the LPT partition gives it (written to
- * its shard buffer); see mlk_cw_pack/unpack for the gather.
+ * Work decomposition: for each block one cell b is contracted
+ * first; V_b = C(X_R, X_b) W_b^T is formed once for the union R of the row points of all
+ * blocks sharing b (for ancestor pairs R = X_b itself), in work units of <= 4096 rows; a
+ * block is W_a V_b[X_a], summed over the 4096-row chunks ("pieces") of X_a in chunk order.
+ * With nranks > 1 the units are LPT-partitioned over ranks, each rank writes the pieces of
+ * its units into its shard; mlk_cw_pack/unpack + the caller's all-gather complete it.
+ * Results are bit-identical for every nranks.
  */
 mlk_status mlk_assemble_cw(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const mlk_kernel* kernel,
                            const mlk_sparsity* sparsity, int32_t precision, mlk_cw* out);
 void mlk_cw_free(mlk_cw cw); /* NULL-safe */
-/* n_cells; n_blocks; nnz values; entries = sum over blocks |row cell| |col cell| (covariance
- * pairs evaluated); flops = algorithmic FP64 flops (Gram 2d per entry + the contractions of
- * the chosen order); own_* = the same for this rank's blocks. */
+/* n_cells; n_blocks; nnz values; entries = sum over blocks |row cell| |col cell| (the
+ * covariance pairs C~_W is made of); flops = FP64 flops the kernels execute (Gram 2d per
+ * evaluated entry + both contractions, see mlk_cw_flops); own_entries = covariance entries
+ * this rank evaluates, own_flops = its share of flops. */
 mlk_status mlk_cw_info(mlk_cw cw, int32_t* n_cells, int64_t* n_blocks, int64_t* nnz,
                        double* entries, double* flops, double* own_entries, double* own_flops);
 /* Host copies of the structure (brow_ptr[n_cells+1], bcol[n_blocks], val_off[n_blocks+1])
@@ -179,17 +185,19 @@ mlk_status mlk_cw_info(mlk_cw cw, int32_t* n_cells, int64_t* n_blocks, int64_t* 
  * values are complete only after mlk_cw_unpack. */
 mlk_status mlk_cw_export(mlk_cw cw, int32_t* brow_ptr, int32_t* bcol, int64_t* val_off,
                          double* values);
-/* Algorithmic FP64 flops by stage (all blocks): gram = 2 d |a||b|, contract1 = the fused
- * tile products C W_b^T (2 |a||b| p_b), contract2 = W_a U (2 p_a |a| p_b), for the order the
- * planner chose per block (b = the side contracted first). */
+/* Executed FP64 flops by stage (all ranks): gram = 2 d per evaluated covariance entry,
+ * contract1 = the fused tile products V_b = C W_b^T (2 p_b per entry), contract2 = the
+ * products W_a V_b[X_a] (2 p_a |X_a| p_b per block). */
 mlk_status mlk_cw_flops(mlk_cw cw, double* gram, double* contract1, double* contract2);
-/* Owner rank of every block (n_blocks), host copy. */
+/* Owner rank of every block (n_blocks): the rank of its first piece; mlk_cw_matvec BSR with
+ * nranks > 1 applies the blocks a rank owns. */
 mlk_status mlk_cw_owner(mlk_cw cw, int32_t* owner);
-/* Gather support (nranks > 1).  shard_len: doubles this rank produced; max_shard_len: the
- * maximum over ranks.  mlk_cw_pack writes this rank's values, in block order, to `dst`
- * (device, >= max_shard_len doubles, tail zero-filled).  After the caller's all-gather of
- * the packed shards into `gathered` (device, nranks x max_shard_len, rank-major),
- * mlk_cw_unpack scatters every rank's values to their BSR positions. */
+/* Gather support (nranks > 1).  shard_len: doubles of pieces this rank produced;
+ * max_shard_len: the maximum over ranks.  mlk_cw_pack writes this rank's pieces, in
+ * (block, chunk) order, to `dst` (device, >= max_shard_len doubles, tail zero-filled).  After
+ * the caller's all-gather of the packed shards into `gathered` (device, nranks x
+ * max_shard_len, rank-major), mlk_cw_unpack sums every block's pieces in chunk order into
+ * the BSR values (no-op for nranks == 1). */
 mlk_status mlk_cw_shard_len(mlk_cw cw, int64_t* shard_len, int64_t* max_shard_len);
 mlk_status mlk_cw_pack(mlk_ctx ctx, mlk_cw cw, double* dst);
 mlk_status mlk_cw_unpack(mlk_ctx ctx, mlk_cw cw, const double* gathered);
@@ -219,10 +227,10 @@ mlk_status mlk_cw_matvec(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const mlk_
  * partition mlk_assemble_cw uses.  owner[n] receives ranks.
  */
 mlk_status mlk_partition_lpt(const double* cost, int64_t n, int32_t nranks, int32_t* owner);
-/* mlk_shard_plan: the gather layout mlk_assemble_cw uses.  Given block value offsets
- * val_off[n+1] and owner[n], shard_off[k] = offset of block k inside its owner's packed shard
- * (blocks in order), shard_len[nranks] = doubles per rank.  The gathered buffer holds rank r's
- * shard at r * max(shard_len). */
+/* mlk_shard_plan: the gather layout mlk_assemble_cw uses.  Given piece offsets val_off[n+1]
+ * (prefix sums of piece lengths) and owner[n], shard_off[k] = offset of piece k inside its
+ * owner's packed shard (pieces in order), shard_len[nranks] = doubles per rank.  The gathered
+ * buffer holds rank r's shard at r * max(shard_len). */
 mlk_status mlk_shard_plan(const int64_t* val_off, const int32_t* owner, int64_t n, int32_t nranks,
                           int64_t* shard_off, int64_t* shard_len);
 

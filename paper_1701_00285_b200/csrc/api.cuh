@@ -71,7 +71,11 @@ struct mlk_cw_s {
   int32_t n_cells = 0;
   int64_t n_blocks = 0, nnz = 0;
   std::vector<int32_t> brow_ptr, bcol, brow, owner;
-  std::vector<int64_t> val_off, shard_off;
+  std::vector<int64_t> val_off;
+  // pieces: block k = sum of pieces piece_ptr[k]..piece_ptr[k+1] (one per row chunk), piece p
+  // stored in rank piece_owner[p]'s shard at piece_off[p]
+  std::vector<int64_t> piece_ptr, piece_off;
+  std::vector<int32_t> piece_owner, reduce_blocks;
   int64_t shard_len = 0, max_shard_len = 0;
   bool complete = false;           // values hold every block (nranks == 1 or unpacked)
   double entries = 0, flops = 0, own_entries = 0, own_flops = 0;
@@ -80,7 +84,8 @@ struct mlk_cw_s {
   mlk::DevBuf<double> shard;       // this rank's packed values (nranks > 1)
   // device structure for the BSR matvec
   mlk::DevBuf<int32_t> brow_d, bcol_d, owner_d;
-  mlk::DevBuf<int64_t> val_off_d, shard_off_d;
+  mlk::DevBuf<int64_t> val_off_d, piece_ptr_d, piece_off_d;
+  mlk::DevBuf<int32_t> piece_owner_d, reduce_d;
   mlk::DevBuf<int32_t> csc_ptr_d, csc_blk_d;   // blocks (r, c), r != c, grouped by column c
 };
 

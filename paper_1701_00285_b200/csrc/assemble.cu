@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <map>
 #include <memory>
 #include <set>
 
@@ -13,8 +14,11 @@
 #include "tile.cuh"
 
 namespace mlk {
+constexpr int64_t kRowChunk = 4096;  // rows per work unit / per piece of a block
+void reduce_pieces(Ctx& c, mlk_cw_s* cw, const double* gathered);
+// jobs: {a node, b node, destination pointer, ldc, store transposed, -, -, -}
 void assemble_dd(Ctx& c, const mlk_tree_s* tree, const mlk_basis_s* B, const mlk_kernel& k,
-                 const std::vector<std::array<int64_t, 8>>& jobs, double* values_base);
+                 const std::vector<std::array<int64_t, 8>>& jobs);
 namespace {
 
 struct SearchItem {
@@ -156,16 +160,33 @@ std::vector<std::pair<int, int>> admitted_pairs(Ctx& c, const mlk_tree_s* tree, 
   return out;
 }
 
-__global__ void k_unpack(const double* __restrict__ gathered, int64_t max_shard, const int32_t* __restrict__ owner,
-                         const int64_t* __restrict__ shard_off, const int64_t* __restrict__ val_off,
-                         double* __restrict__ values) {
-  int64_t k = blockIdx.x;
-  const double* src = gathered + owner[k] * max_shard + shard_off[k];
-  int64_t len = val_off[k + 1] - val_off[k];
-  for (int64_t e = threadIdx.x; e < len; e += blockDim.x) values[val_off[k] + e] = src[e];
+// values of the listed blocks = sum of their pieces in chunk order (pieces live in rank r's
+// shard at gathered + r * max_shard + piece_off)
+__global__ void k_reduce_pieces(const int32_t* __restrict__ blocks, const int64_t* __restrict__ piece_ptr,
+                                const int64_t* __restrict__ piece_off, const int32_t* __restrict__ piece_owner,
+                                const double* __restrict__ gathered, int64_t max_shard,
+                                const int64_t* __restrict__ val_off, double* __restrict__ values) {
+  const int64_t k = blocks[blockIdx.x];
+  const int64_t len = val_off[k + 1] - val_off[k];
+  const int64_t p0 = piece_ptr[k], p1 = piece_ptr[k + 1];
+  for (int64_t e = threadIdx.x; e < len; e += blockDim.x) {
+    double s = 0.0;
+    for (int64_t p = p0; p < p1; p++) s += gathered[piece_owner[p] * max_shard + piece_off[p] + e];
+    values[val_off[k] + e] = s;
+  }
 }
 
 }  // namespace
+
+void reduce_pieces(Ctx& c, mlk_cw_s* cw, const double* gathered) {
+  if (cw->reduce_blocks.empty()) return;
+  const int64_t ms = cw->nranks > 1 ? cw->max_shard_len : 0;
+  k_reduce_pieces<<<(unsigned)cw->reduce_blocks.size(), 256, 0, c.stream>>>(
+      cw->reduce_d.p, cw->piece_ptr_d.p, cw->piece_off_d.p, cw->piece_owner_d.p, gathered, ms, cw->val_off_d.p,
+      cw->values.p);
+  check_launch("k_reduce_pieces");
+}
+
 }  // namespace mlk
 
 using namespace mlk;
@@ -201,7 +222,16 @@ mlk_status mlk_assemble_cw(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const ml
   cw->bcol.resize(nb);
   cw->brow.resize(nb);
   cw->val_off.assign(nb + 1, 0);
-  std::vector<double> cost(nb), flops(nb), ent(nb);
+  // ---- per block: orientation.  b = the cell contracted first (its W_b multiplies C first),
+  // a = the other.  Ancestor pairs take b = the ancestor, so that U_ab = C(X_a, X_b) W_b^T is
+  // a row slice of V_b = C(X_b, X_b) W_b^T (X_a is a subset of X_b): every such block reuses
+  // the self-block intermediate of its ancestor.  Other pairs
+  // take the cheaper order of the two contractions.
+  auto is_anc = [](int anc, int q) {
+    while (q > anc) q = (q - 1) / 2;
+    return q == anc;
+  };
+  std::vector<int32_t> A(nb), Bc(nb);
   std::vector<int8_t> swap(nb);
   for (int64_t k = 0; k < nb; k++) {
     int r = pairs[k].first, cc = pairs[k].second;
@@ -212,102 +242,240 @@ mlk_status mlk_assemble_cw(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const ml
     double sr = (double)(tree->end[r] - tree->begin[r]), sc = (double)(tree->end[cc] - tree->begin[cc]);
     double qr = B->p[r], qc = B->p[cc];
     cw->val_off[k + 1] = cw->val_off[k] + (int64_t)B->p[r] * B->p[cc];
-    double f1 = 2 * sr * sc * qc + 2 * qr * sr * qc;  // a = row, b = col (contract col first)
-    double f2 = 2 * sc * sr * qr + 2 * qc * sc * qr;  // a = col, b = row
-    swap[k] = f2 < f1;
-    ent[k] = sr * sc;
-    cw->f_gram += 2.0 * d * sr * sc;
-    cw->f_c1 += swap[k] ? 2 * sc * sr * qr : 2 * sr * sc * qc;
-    cw->f_c2 += swap[k] ? 2 * qc * sc * qr : 2 * qr * sr * qc;
-    flops[k] = 2.0 * d * sr * sc + std::min(f1, f2);
-    cost[k] = flops[k] + 60.0 * sr * sc;
+    cw->entries += sr * sc;
+    bool sw;
+    if (r == cc || is_anc(cc, r)) sw = false;
+    else if (is_anc(r, cc)) sw = true;
+    else sw = (2 * sc * sr * qr + 2 * qc * sc * qr) < (2 * sr * sc * qc + 2 * qr * sr * qc);
+    swap[k] = sw;
+    A[k] = sw ? cc : r;
+    Bc[k] = sw ? r : cc;
   }
   for (int i = 0; i < cw->n_cells; i++) cw->brow_ptr[i + 1] += cw->brow_ptr[i];
   cw->nnz = cw->val_off[nb];
-  cw->owner.assign(nb, 0);
-  if (c.nranks > 1) partition_lpt(cost.data(), nb, c.nranks, cw->owner.data());
-  std::vector<int64_t> shard_fill(c.nranks, 0);
-  cw->shard_off.assign(nb, 0);
-  shard_plan(cw->val_off.data(), cw->owner.data(), nb, c.nranks, cw->shard_off.data(), shard_fill.data());
-  for (int64_t k = 0; k < nb; k++) {
-    int o = cw->owner[k];
-    cw->entries += ent[k];
-    cw->flops += flops[k];
-    if (o == c.rank) {
-      cw->own_entries += ent[k];
-      cw->own_flops += flops[k];
+  const bool dd = precision == MLK_PREC_DD;
+  auto S = [&](int q) { return tree->end[q] - tree->begin[q]; };
+
+  // ---- work units (column cell b, row chunk) and pieces (block, row chunk)
+  const int64_t CH = kRowChunk;
+  struct Unit {
+    int b;
+    int64_t chunk;
+    std::vector<std::pair<int64_t, int64_t>> rows;  // tree-position ranges inside the chunk
+    int64_t nrows = 0;
+    double cost = 0, flops_gram = 0, flops_c1 = 0, flops_c2 = 0;
+    int owner = 0;
+    int64_t v_off = 0;  // offset of this unit's V rows in the V buffer (doubles)
+  };
+  std::vector<Unit> units;
+  std::map<std::pair<int, int64_t>, int> unit_of;
+  struct Piece {
+    int64_t blk, chunk;
+    int unit;
+  };
+  std::vector<Piece> pieces;
+  std::vector<int64_t> piece_ptr(nb + 1, 0);
+  if (!dd) {
+    std::map<int, std::vector<std::pair<int64_t, int64_t>>> rowsets;
+    for (int64_t k = 0; k < nb; k++) rowsets[Bc[k]].push_back({tree->begin[A[k]], tree->end[A[k]]});
+    for (auto& kv : rowsets) {
+      int b = kv.first;
+      auto rg = kv.second;
+      rg.push_back({tree->begin[b], tree->end[b]});
+      std::sort(rg.begin(), rg.end());
+      std::vector<std::pair<int64_t, int64_t>> merged;
+      for (auto& x : rg) {
+        if (!merged.empty() && x.first <= merged.back().second) merged.back().second = std::max(merged.back().second, x.second);
+        else merged.push_back(x);
+      }
+      const double sb = (double)S(b);
+      const int rq = tile_rq_class(std::min(B->p[b], 8 * kTileMaxRQ));
+      for (auto& m : merged) {
+        for (int64_t c0 = m.first / CH; c0 * CH < m.second; c0++) {
+          int64_t lo = std::max(m.first, c0 * CH), hi = std::min(m.second, (c0 + 1) * CH);
+          auto key = std::make_pair(b, c0);
+          auto it = unit_of.find(key);
+          int ui;
+          if (it == unit_of.end()) {
+            ui = (int)units.size();
+            unit_of[key] = ui;
+            Unit u;
+            u.b = b;
+            u.chunk = c0;
+            units.push_back(u);
+          } else {
+            ui = it->second;
+          }
+          Unit& u = units[ui];
+          u.rows.push_back({lo, hi});
+          u.nrows += hi - lo;
+          u.flops_gram += 2.0 * d * (hi - lo) * sb;
+          u.flops_c1 += 2.0 * (hi - lo) * sb * B->p[b];
+          u.cost += (hi - lo) * sb * (2.0 * dp + 16.0 * rq + 60.0);
+        }
+      }
+    }
+    for (int64_t k = 0; k < nb; k++) {
+      int a = A[k], b = Bc[k];
+      for (int64_t c0 = tree->begin[a] / CH; c0 * CH < tree->end[a]; c0++) {
+        int ui = unit_of.at({b, c0});
+        int64_t lo = std::max(tree->begin[a], c0 * CH), hi = std::min(tree->end[a], (c0 + 1) * CH);
+        double f = 2.0 * B->p[a] * (double)(hi - lo) * B->p[b];
+        units[ui].flops_c2 += f;
+        units[ui].cost += f;
+        pieces.push_back({k, c0, ui});
+        piece_ptr[k + 1]++;
+      }
+    }
+  } else {
+    // DD mode: one unit and one piece per block
+    for (int64_t k = 0; k < nb; k++) {
+      Unit u;
+      u.b = Bc[k];
+      u.chunk = -1;
+      double sa = (double)S(A[k]), sb = (double)S(Bc[k]);
+      u.flops_gram = 3.0 * d * sa * sb;
+      u.flops_c1 = 2.0 * sa * sb * B->p[Bc[k]];
+      u.flops_c2 = 2.0 * B->p[A[k]] * sa * B->p[Bc[k]];
+      u.cost = sa * sb * (300.0 + 20.0 * B->p[Bc[k]]);
+      units.push_back(u);
+      pieces.push_back({k, 0, (int)k});
+      piece_ptr[k + 1] = 1;
     }
   }
+  for (int64_t k = 0; k < nb; k++) piece_ptr[k + 1] += piece_ptr[k];
+  const int64_t npc = (int64_t)pieces.size();
+  // ---- ownership: LPT over units; a piece belongs to its unit's owner
+  {
+    std::vector<double> uc(units.size());
+    for (size_t i = 0; i < units.size(); i++) uc[i] = units[i].cost;
+    std::vector<int32_t> own(units.size(), 0);
+    if (c.nranks > 1) partition_lpt(uc.data(), (int64_t)uc.size(), c.nranks, own.data());
+    for (size_t i = 0; i < units.size(); i++) units[i].owner = own[i];
+  }
+  for (auto& u : units) {
+    double f = u.flops_gram + u.flops_c1 + u.flops_c2;
+    cw->flops += f;
+    cw->f_gram += u.flops_gram;
+    cw->f_c1 += u.flops_c1;
+    cw->f_c2 += u.flops_c2;
+    if (u.owner == c.rank) {
+      cw->own_flops += f;
+      cw->own_entries += (double)u.nrows * (double)S(u.b);
+    }
+  }
+  cw->owner.assign(nb, 0);
+  for (int64_t k = 0; k < nb; k++) cw->owner[k] = units[pieces[piece_ptr[k]].unit].owner;
+  // a block computed by one rank in one piece is written straight into the BSR values when
+  // nranks == 1; everything else goes through per-rank piece shards reduced in chunk order
+  std::vector<int64_t> plen(npc + 1, 0);
+  std::vector<int32_t> powner(npc);
+  std::vector<int8_t> direct(nb, 0);
+  for (int64_t k = 0; k < nb; k++) direct[k] = (c.nranks == 1 && piece_ptr[k + 1] - piece_ptr[k] == 1);
+  for (int64_t i = 0; i < npc; i++) {
+    int64_t k = pieces[i].blk;
+    plen[i + 1] = plen[i] + (direct[k] ? 0 : cw->val_off[k + 1] - cw->val_off[k]);
+    powner[i] = units[pieces[i].unit].owner;
+  }
+  std::vector<int64_t> shard_fill(c.nranks, 0);
+  cw->piece_off.assign(npc, 0);
+  shard_plan(plen.data(), powner.data(), npc, c.nranks, cw->piece_off.data(), shard_fill.data());
+  cw->piece_ptr = piece_ptr;
+  cw->piece_owner = powner;
   cw->shard_len = shard_fill[c.rank];
   cw->max_shard_len = *std::max_element(shard_fill.begin(), shard_fill.end());
   cw->values.alloc(std::max<int64_t>(cw->nnz, 1), st);
-  double* dst_base;
-  if (c.nranks > 1) {
-    cw->values.zero();
-    cw->shard.alloc(std::max<int64_t>(cw->max_shard_len, 1), st);
-    cw->shard.zero();
-    dst_base = cw->shard.p;
-  } else {
-    dst_base = cw->values.p;
-  }
-  auto dst_of = [&](int64_t k) { return dst_base + (c.nranks > 1 ? cw->shard_off[k] : cw->val_off[k]); };
-
-  // own pairs, processed in batches that bound the U scratch
-  std::vector<int64_t> own;
+  if (c.nranks > 1) cw->values.zero();
+  cw->shard.alloc(std::max<int64_t>(cw->max_shard_len, 1), st);
   for (int64_t k = 0; k < nb; k++)
-    if (cw->owner[k] == c.rank) own.push_back(k);
+    if (!direct[k]) cw->reduce_blocks.push_back((int32_t)k);
+  auto piece_dst = [&](int64_t i) {
+    int64_t k = pieces[i].blk;
+    return direct[k] ? cw->values.p + cw->val_off[k] : cw->shard.p + cw->piece_off[i];
+  };
 
-  if (precision == MLK_PREC_DD) {
-    // jobs: a_node, b_node, dst offset, ld, trans
+  if (dd) {
     std::vector<std::array<int64_t, 8>> jobs;
-    for (int64_t k : own) {
-      int r = pairs[k].first, cc = pairs[k].second;
-      bool sw = swap[k];
-      int a = sw ? cc : r, b = sw ? r : cc;
-      jobs.push_back({a, b, (int64_t)(dst_of(k) - dst_base), (int64_t)B->p[cc], (int64_t)sw, 0, 0, 0});
+    for (int64_t i = 0; i < npc; i++) {
+      int64_t k = pieces[i].blk;
+      if (powner[i] != c.rank) continue;
+      jobs.push_back({A[k], Bc[k], (int64_t)reinterpret_cast<uintptr_t>(piece_dst(i)),
+                      (int64_t)B->p[pairs[k].second], (int64_t)swap[k], 0, 0, 0});
     }
-    assemble_dd(c, tree, B, *kernel, jobs, dst_base);
+    assemble_dd(c, tree, B, *kernel, jobs);
   } else {
     const KernelParams kp = make_kernel_params(*kernel);
+    // own units in batches that bound the V scratch
+    std::vector<int> mine;
+    for (size_t i = 0; i < units.size(); i++)
+      if (units[i].owner == c.rank) mine.push_back((int)i);
+    std::vector<std::vector<int64_t>> unit_pieces(units.size());
+    for (int64_t i = 0; i < npc; i++)
+      if (powner[i] == c.rank) unit_pieces[pieces[i].unit].push_back(i);
     size_t freeb = 0, totalb = 0;
     CUDA_CHECK(cudaMemGetInfo(&freeb, &totalb));
-    const int64_t budget = std::max<int64_t>((int64_t)(freeb / 3 / sizeof(double)), (int64_t)1 << 20);
+    const int64_t budget = std::max<int64_t>((int64_t)(freeb / 3 / sizeof(double)), (int64_t)1 << 22);
     size_t pos = 0;
-    while (pos < own.size()) {
-      // batch
+    while (pos < mine.size()) {
       int64_t need = 0;
       size_t end = pos;
-      while (end < own.size()) {
-        int64_t k = own[end];
-        int r = pairs[k].first, cc = pairs[k].second;
-        int a = swap[k] ? cc : r, b = swap[k] ? r : cc;
-        int64_t u = (tree->end[a] - tree->begin[a]) * (int64_t)B->p[b];
-        if (end > pos && need + u > budget) break;
-        need += u;
+      while (end < mine.size()) {
+        const Unit& u = units[mine[end]];
+        int64_t v = u.nrows * (int64_t)B->p[u.b];
+        if (end > pos && need + v > budget) break;
+        units[mine[end]].v_off = need;
+        need += v;
         end++;
       }
-      DevBuf<double> U(std::max<int64_t>(need, 1), st);
-      std::vector<TileUnit> units;
+      DevBuf<double> V(std::max<int64_t>(need, 1), st);
+      std::vector<TileUnit> tu;
       std::vector<GemmDesc> gd;
-      int64_t uoff = 0;
-      for (size_t i = pos; i < end; i++) {
-        int64_t k = own[i];
-        int r = pairs[k].first, cc = pairs[k].second;
-        bool sw = swap[k];
-        int a = sw ? cc : r, b = sw ? r : cc;
-        int32_t sa = (int32_t)(tree->end[a] - tree->begin[a]), sb = (int32_t)(tree->end[b] - tree->begin[b]);
-        int32_t pa = B->p[a], pb = B->p[b];
-        double* Up = U.p + uoff;
-        make_tile_units(units, tree->begin[a], sa, tree->begin[b], sb, B->W.p + B->w_off[b], sb, pb, Up, pb, 0, dp);
-        // B = W_a U  (pa x pb), stored transposed when a is the column cell
-        GemmDesc g{B->W.p + B->w_off[a], sa, Up, pb, dst_of(k), (int64_t)B->p[cc], pa, pb, sa, sw ? 1 : 0};
-        gd.push_back(g);
-        uoff += (int64_t)sa * pb;
+      for (size_t j = pos; j < end; j++) {
+        const Unit& u = units[mine[j]];
+        const int b = u.b;
+        const int32_t sb = (int32_t)S(b), pb = B->p[b];
+        int64_t roff = 0;
+        for (auto& rg : u.rows) {
+          make_tile_units(tu, rg.first, (int32_t)(rg.second - rg.first), tree->begin[b], sb, B->W.p + B->w_off[b],
+                          sb, pb, V.p + u.v_off + roff * pb, pb, 0, dp);
+          roff += rg.second - rg.first;
+        }
+        for (int64_t i : unit_pieces[mine[j]]) {
+          int64_t k = pieces[i].blk;
+          int a = A[k];
+          int64_t lo = std::max(tree->begin[a], u.chunk * CH), hi = std::min(tree->end[a], (u.chunk + 1) * CH);
+          // row offset of [lo, hi) inside this unit's compact V rows
+          int64_t off = 0;
+          for (auto& rg : u.rows) {
+            if (lo >= rg.first && hi <= rg.second) {
+              off += lo - rg.first;
+              break;
+            }
+            off += rg.second - rg.first;
+          }
+          const int32_t pa = B->p[a];
+          GemmDesc g{B->W.p + B->w_off[a] + (lo - tree->begin[a]), S(a), V.p + u.v_off + off * pb, pb, piece_dst(i),
+                     (int64_t)B->p[pairs[k].second], pa, pb, (int32_t)(hi - lo), swap[k] ? 1 : 0};
+          gd.push_back(g);
+        }
       }
-      run_tile_contract(c, tree, kp, units, "assemble_tile_contract");
+      run_tile_contract(c, tree, kp, tu, "assemble_tile_contract");
       gemm_batched(c, gd, "assemble_wa_gemm");
       pos = end;
     }
+  }
+  // piece structure on the device; nranks == 1: reduce the multi-piece blocks now
+  cw->piece_ptr_d.alloc(nb + 1, st);
+  cw->piece_ptr_d.upload(cw->piece_ptr);
+  cw->piece_off_d.alloc(std::max<int64_t>(npc, 1), st);
+  cw->piece_off_d.upload(cw->piece_off);
+  cw->piece_owner_d.alloc(std::max<int64_t>(npc, 1), st);
+  cw->piece_owner_d.upload(cw->piece_owner);
+  cw->reduce_d.alloc(std::max<size_t>(cw->reduce_blocks.size(), 1), st);
+  cw->reduce_d.upload(cw->reduce_blocks);
+  if (c.nranks == 1 && !cw->reduce_blocks.empty()) {
+    TimedLaunch tl(c, "assemble_piece_reduce");
+    reduce_pieces(c, cw.get(), cw->shard.p);
   }
   CUDA_CHECK(cudaStreamSynchronize(st));
   cw->complete = c.nranks == 1;
@@ -320,8 +488,6 @@ mlk_status mlk_assemble_cw(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const ml
   cw->owner_d.upload(cw->owner);
   cw->val_off_d.alloc(nb + 1, st);
   cw->val_off_d.upload(cw->val_off);
-  cw->shard_off_d.alloc(std::max<int64_t>(nb, 1), st);
-  cw->shard_off_d.upload(cw->shard_off);
   {
     std::vector<int32_t> cptr(cw->n_cells + 1, 0), cblk;
     for (int64_t k = 0; k < nb; k++)
@@ -352,7 +518,10 @@ void mlk_cw_free(mlk_cw cw) {
   cw->bcol_d.s = nullptr;
   cw->owner_d.s = nullptr;
   cw->val_off_d.s = nullptr;
-  cw->shard_off_d.s = nullptr;
+  cw->piece_ptr_d.s = nullptr;
+  cw->piece_off_d.s = nullptr;
+  cw->piece_owner_d.s = nullptr;
+  cw->reduce_d.s = nullptr;
   cw->csc_ptr_d.s = nullptr;
   cw->csc_blk_d.s = nullptr;
   delete cw;
@@ -415,7 +584,7 @@ mlk_status mlk_cw_pack(mlk_ctx ctx, mlk_cw cw, double* dst) {
   MLK_REQUIRE(is_device_ptr(dst), "dst must be device memory");
   if (cw->max_shard_len == 0) return MLK_OK;
   CUDA_CHECK(cudaMemsetAsync(dst, 0, sizeof(double) * cw->max_shard_len, c.stream));
-  const double* src = cw->nranks > 1 ? cw->shard.p : cw->values.p;
+  const double* src = cw->shard.p;
   if (cw->shard_len)
     CUDA_CHECK(cudaMemcpyAsync(dst, src, sizeof(double) * cw->shard_len, cudaMemcpyDeviceToDevice, c.stream));
   CUDA_CHECK(cudaStreamSynchronize(c.stream));
@@ -428,15 +597,12 @@ mlk_status mlk_cw_unpack(mlk_ctx ctx, mlk_cw cw, const double* gathered) {
   Ctx& c = ctx->c;
   CUDA_CHECK(cudaSetDevice(c.device));
   MLK_REQUIRE(is_device_ptr(gathered), "gathered must be device memory");
-  if (cw->n_blocks == 0) return MLK_OK;
-  {
+  if (cw->nranks > 1) {
     TimedLaunch tl(c, "cw_unpack");
-    k_unpack<<<(unsigned)cw->n_blocks, 256, 0, c.stream>>>(gathered, cw->max_shard_len, cw->owner_d.p,
-                                                           cw->shard_off_d.p, cw->val_off_d.p, cw->values.p);
-    check_launch("k_unpack");
+    reduce_pieces(c, cw, gathered);
   }
-  cw->complete = true;
   CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  cw->complete = true;
   MLK_API_END
 }
 

@@ -187,7 +187,7 @@ dd host_sqrt(double x) {
 }  // namespace
 
 void assemble_dd(Ctx& c, const mlk_tree_s* tree, const mlk_basis_s* B, const mlk_kernel& k,
-                 const std::vector<std::array<int64_t, 8>>& in, double* values_base) {
+                 const std::vector<std::array<int64_t, 8>>& in) {
   if (in.empty()) return;
   cudaStream_t st = c.stream;
   // 1/k! in double-double
@@ -232,7 +232,7 @@ void assemble_dd(Ctx& c, const mlk_tree_s* tree, const mlk_basis_s* B, const mlk
     x.u_off = uo;
     x.e_u = eu;
     x.e_b = eb;
-    x.dst = values_base + j[2];
+    x.dst = reinterpret_cast<double*>(static_cast<uintptr_t>(j[2]));
     x.ldc = j[3];
     x.trans = (int32_t)j[4];
     pre_u.push_back(eu);

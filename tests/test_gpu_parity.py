@@ -332,3 +332,44 @@ def test_matvec_cfg3_sampled_rows(mlk, ctx):
     assert np.linalg.norm(y - yr) <= 1e-12 * np.linalg.norm(yr)
     y2 = mlk.cw_matvec(ctx, g, gb, kern, None, mlk.MATVEC_EXACT, v)
     assert np.array_equal(y, y2)
+
+
+# --------------------------------------------------------------------------------- multi-rank
+@pytest.mark.parametrize("R", [2, 3, 8])
+def test_multirank_emulated_bit_identical(mlk, ctx, R):
+    """nranks = R contexts on one GPU, run one after another (no rank waits on another): each
+    assembles its LPT share, the shards are concatenated (what the NCCL all-gather does) and
+    unpacked; values must equal the nranks = 1 result bit for bit, and the partial C_W v of
+    the ranks must sum to the single-rank product."""
+    import torch
+    X, dirs = _setup(16384, 10, 256, 1)
+    kern = dict(family=OC.MATERN_32, rho=1.0)
+    sp = dict(mode=1, tau=1e-6)
+    g = mlk.build_tree(ctx, X, 256, 1, dirs)
+    gb = mlk.build_basis(ctx, g, 2)
+    ref = mlk.assemble_cw(ctx, g, gb, kern, sp).export()["values"]
+    v = wl.vectors(2, gb.dim, seed=3)
+    y1 = mlk.cw_matvec(ctx, g, gb, kern, None, mlk.MATVEC_EXACT, v)
+    ctxs = [mlk.Ctx(0, R, r) for r in range(R)]
+    trees = [mlk.build_tree(c, X, 256, 1, dirs) for c in ctxs]
+    bases = [mlk.build_basis(c, t, 2) for c, t in zip(ctxs, trees)]
+    cws = [mlk.assemble_cw(c, t, b, kern, sp) for c, t, b in zip(ctxs, trees, bases)]
+    mx = max(cw.shard_len()[1] for cw in cws)
+    assert all(cw.shard_len()[1] == mx for cw in cws)
+    shards = []
+    for c, cw in zip(ctxs, cws):
+        buf = torch.empty(max(mx, 1), dtype=torch.float64, device="cuda")
+        mlk.pack_cw(c, cw, buf)
+        shards.append(buf)
+    gathered = torch.cat(shards)
+    for c, cw in zip(ctxs, cws):
+        mlk.unpack_cw(c, cw, gathered)
+        assert np.array_equal(cw.export()["values"], ref)
+    assert abs(sum(cw.own_flops for cw in cws) - cws[0].flops) < 1e-6 * cws[0].flops
+    ys = [mlk.cw_matvec(c, t, b, kern, None, mlk.MATVEC_EXACT, v, allreduce=False)
+          for c, t, b in zip(ctxs, trees, bases)]
+    assert np.linalg.norm(sum(ys) - y1) <= 1e-13 * np.linalg.norm(y1)
+    yb1 = mlk.cw_matvec(ctx, g, gb, kern, mlk.assemble_cw(ctx, g, gb, kern, sp), mlk.MATVEC_BSR, v)
+    ybs = [mlk.cw_matvec(c, t, b, kern, cw, mlk.MATVEC_BSR, v, allreduce=False)
+           for c, t, b, cw in zip(ctxs, trees, bases, cws)]
+    assert np.linalg.norm(sum(ybs) - yb1) <= 1e-13 * np.linalg.norm(yb1)
