@@ -465,6 +465,8 @@ mlk_status mlk_assemble_cw(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const ml
     }
   }
   // piece structure on the device; nranks == 1: reduce the multi-piece blocks now
+  cw->val_off_d.alloc(nb + 1, st);
+  cw->val_off_d.upload(cw->val_off);
   cw->piece_ptr_d.alloc(nb + 1, st);
   cw->piece_ptr_d.upload(cw->piece_ptr);
   cw->piece_off_d.alloc(std::max<int64_t>(npc, 1), st);
@@ -486,8 +488,6 @@ mlk_status mlk_assemble_cw(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const ml
   cw->bcol_d.upload(cw->bcol);
   cw->owner_d.alloc(std::max<int64_t>(nb, 1), st);
   cw->owner_d.upload(cw->owner);
-  cw->val_off_d.alloc(nb + 1, st);
-  cw->val_off_d.upload(cw->val_off);
   {
     std::vector<int32_t> cptr(cw->n_cells + 1, 0), cblk;
     for (int64_t k = 0; k < nb; k++)
