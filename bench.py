@@ -13,7 +13,6 @@ back to host inside the timed region.
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -35,7 +34,8 @@ def fp64_peak():
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled through NVML every 100 ms during the timed region
+    (in-process, so the sampling does not stall the host thread that drives the GPU)."""
 
     def __init__(self, index):
         self.index = index
@@ -45,16 +45,18 @@ class ClockSampler:
 
     def start(self):
         def run():
-            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap")
+            try:
+                import pynvml
+                pynvml.nvmlInit()
+                h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+                mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            except Exception:
+                return
             while not self._stop.is_set():
                 try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + q,
-                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                         timeout=5).stdout.strip()
-                    if out:
-                        self.samples.append([x.strip() for x in out.split(",")])
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((sm, mx, rs))
                 except Exception:
                     pass
                 self._stop.wait(0.1)
@@ -68,13 +70,12 @@ class ClockSampler:
             self._t.join(timeout=10)
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i]
-                          and "Not" not in s[2 + i]})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        bits = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+                "sw_power_cap": 0x4}
+        reasons = sorted({k for _, _, rs in self.samples for k, b in bits.items() if rs & b})
+        return {"sm_mhz": float(np.median([s[0] for s in self.samples])),
+                "sm_max_mhz": float(max(s[1] for s in self.samples)), "reasons": reasons,
+                "samples": len(self.samples)}
 
 
 def dist_env():
@@ -190,20 +191,28 @@ def main():
     nvec = 1
     torch.cuda.synchronize()
 
+    api_ms = {}
+
+    def timed(name, fn, *a, **kw):
+        t0 = time.perf_counter()
+        r = fn(*a, **kw)
+        api_ms[name] = api_ms.get(name, 0.0) + (time.perf_counter() - t0) * 1e3
+        return r
+
     def step(X, D, v_host=None, out_vals=None, out_y=None):
-        tr = mlk.build_tree(ctx, X, c["leaf"], c["tree"], D)
-        B = mlk.build_basis(ctx, tr, c["w"])
-        cw = mlk.assemble_cw(ctx, tr, B, kern, spars)
+        tr = timed("build_tree", mlk.build_tree, ctx, X, c["leaf"], c["tree"], D)
+        B = timed("build_basis", mlk.build_basis, ctx, tr, c["w"])
+        cw = timed("assemble_cw", mlk.assemble_cw, ctx, tr, B, kern, spars)
         if ws > 1:
-            mlk.gather_cw(ctx, cw)
+            timed("gather_cw", mlk.gather_cw, ctx, cw)
         if v_host is None:
             v = torch.ones((nvec, B.dim), dtype=torch.float64, device=dev)
             y = torch.empty_like(v)
         else:
             v, y = v_host, out_y
-        mlk.cw_matvec(ctx, tr, B, kern, None, mlk.MATVEC_EXACT, v, out=y)
+        timed("cw_matvec", mlk.cw_matvec, ctx, tr, B, kern, None, mlk.MATVEC_EXACT, v, out=y)
         if out_vals is not None:
-            cw.export(out=out_vals)
+            timed("export", cw.export, out=out_vals)
         return tr, B, cw
 
     # L2 flush buffer (> 126 MB L2) written between timed steps, outside the timed events
@@ -228,6 +237,7 @@ def main():
     if sampler:
         sampler.start()
     launches0 = mlk.launch_count()
+    api_ms.clear()
     step_ms = []
     for _ in range(args.steps):
         flush.fill_(1.0)
@@ -243,6 +253,7 @@ def main():
         step_ms.append(e0.elapsed_time(e1))
     torch.cuda.synchronize()
     launches = mlk.launch_count() - launches0
+    api_timed = {k: v / args.steps for k, v in api_ms.items()}
     clocks = sampler.stop() if sampler else None
     stats = ctx.kernel_stats()
     ctx.set_timing(False)
@@ -311,6 +322,7 @@ def main():
                          "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_flops_per_step": k5_flops, "ms_per_step": k5_ms_per_step},
             "kernels_ms_per_step": {k: v["ms"] / args.steps for k, v in sorted(stats.items())},
+            "api_wall_ms_per_step": api_timed,
             "entries_per_step": entries, "blocks_nnz": nnz,
             "clocks": clocks, "gpu_launches": launches,
             "e2e": {"value": e2e_val, "unit": "covariance pairs/s", "h2d_bytes_per_step": int(h2d),

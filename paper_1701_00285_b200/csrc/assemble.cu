@@ -210,7 +210,9 @@ mlk_status mlk_assemble_cw(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const ml
   const mlk_basis_s* B = basis;
   const int dp = tree->d_pad, d = tree->d;
 
+  HostTrace trace("assemble");
   auto pairs = admitted_pairs(c, tree, B, *sparsity);
+  trace.mark("search");
   auto cw = std::make_unique<mlk_cw_s>();
   cw->device = c.device;
   cw->nranks = c.nranks;
@@ -253,6 +255,7 @@ mlk_status mlk_assemble_cw(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const ml
   }
   for (int i = 0; i < cw->n_cells; i++) cw->brow_ptr[i + 1] += cw->brow_ptr[i];
   cw->nnz = cw->val_off[nb];
+  trace.mark("orient");
   const bool dd = precision == MLK_PREC_DD;
   auto S = [&](int q) { return tree->end[q] - tree->begin[q]; };
 
@@ -394,6 +397,7 @@ mlk_status mlk_assemble_cw(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const ml
     return direct[k] ? cw->values.p + cw->val_off[k] : cw->shard.p + cw->piece_off[i];
   };
 
+  trace.mark("plan");
   if (dd) {
     std::vector<std::array<int64_t, 8>> jobs;
     for (int64_t i = 0; i < npc; i++) {
@@ -459,8 +463,11 @@ mlk_status mlk_assemble_cw(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const ml
           gd.push_back(g);
         }
       }
+      trace.mark("units");
       run_tile_contract(c, tree, kp, tu, "assemble_tile_contract");
+      trace.mark("k5a_launch");
       gemm_batched(c, gd, "assemble_wa_gemm");
+      trace.mark("k5b_launch");
       pos = end;
     }
   }
@@ -480,6 +487,7 @@ mlk_status mlk_assemble_cw(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const ml
     reduce_pieces(c, cw.get(), cw->shard.p);
   }
   CUDA_CHECK(cudaStreamSynchronize(st));
+  trace.mark("sync");
   cw->complete = c.nranks == 1;
   // device structure for the BSR matvec
   cw->brow_d.alloc(std::max<int64_t>(nb, 1), st);
@@ -503,6 +511,7 @@ mlk_status mlk_assemble_cw(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const ml
     cw->csc_blk_d.upload(cblk);
   }
   CUDA_CHECK(cudaStreamSynchronize(st));
+  trace.mark("structure");
   *out = cw.release();
   MLK_API_END
 }

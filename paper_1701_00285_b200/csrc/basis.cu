@@ -273,6 +273,7 @@ mlk_status mlk_build_basis(mlk_ctx ctx, mlk_tree tree, int32_t w, mlk_basis* out
   DevBuf<int32_t> facd(fh.size(), st);
   facd.upload(fh);
 
+  HostTrace trace("basis");
   // ---- leaves
   {
     std::vector<LeafJob> lj;
@@ -313,6 +314,7 @@ mlk_status mlk_build_basis(mlk_ctx ctx, mlk_tree tree, int32_t w, mlk_basis* out
     }
     run_qr(c, qj, M, flag.p, "basis_leaf_qr");
   }
+  trace.mark("leaves");
   // ---- internal levels, bottom-up
   DevBuf<double> Qt;
   DevBuf<double> Ast;
@@ -369,7 +371,9 @@ mlk_status mlk_build_basis(mlk_ctx ctx, mlk_tree tree, int32_t w, mlk_basis* out
     }
     gemm_batched(c, gd, "basis_transfer_gemm");
   }
+  trace.mark("levels");
   auto fl = flag.download(1);
+  trace.mark("sync");
   if (fl[0]) throw Error(MLK_ERR_RANK_DEFICIENT, "moment matrix is rank deficient (|R_kk| <= 1e-13 max|R_ii|)");
   CUDA_CHECK(cudaStreamSynchronize(st));
   *out = B.release();

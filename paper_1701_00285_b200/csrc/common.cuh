@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <chrono>
+#include <cstdlib>
 
 #include <cstdint>
 #include <cstdio>
@@ -179,6 +181,23 @@ struct DevOut {
 };
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Host-side phase timer, printed to stderr when MLK_TRACE is set (diagnostics only).
+struct HostTrace {
+  const char* what;
+  bool on;
+  std::chrono::steady_clock::time_point t0, last;
+  explicit HostTrace(const char* w) : what(w), on(std::getenv("MLK_TRACE") != nullptr) {
+    t0 = last = std::chrono::steady_clock::now();
+  }
+  void mark(const char* phase) {
+    if (!on) return;
+    auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[mlk] %s.%s %.3f ms\n", what, phase,
+                 std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
+  }
+};
 
 int num_sms(int device);
 

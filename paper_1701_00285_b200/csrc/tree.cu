@@ -309,6 +309,7 @@ mlk_status mlk_build_tree(mlk_ctx ctx, const double* X, int64_t n, int32_t d, in
   DevBuf<int32_t> seg_node_d(1, st), nodes_d(1, st);
   DevBuf<int8_t> seg_active_d(1, st);
 
+  HostTrace trace("tree");
   for (int dep = 0; dep < t; dep++) {
     // segments at this depth: nodes at depth dep and leaves above, left to right
     std::vector<std::pair<int64_t, int>> segs;
@@ -365,7 +366,9 @@ mlk_status mlk_build_tree(mlk_ctx ctx, const double* X, int64_t n, int32_t d, in
     k_dup_pairwise<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(tr->X.p, n, d, flag.p);
     check_launch("k_dup_pairwise");
   }
+  trace.mark("levels");
   auto fl = flag.download(1);
+  trace.mark("sync");
   if (fl[0]) throw Error(MLK_ERR_DUPLICATE_POINTS, "duplicate observation sites");
 
   tr->Xt.alloc((size_t)n * tr->d_pad, st);

@@ -18,6 +18,7 @@ timeout 300 $SHORT > $OUT/short_$TAG.log 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv $SHORT > $OUT/ncu_launch_$TAG.log 2>&1
 echo "ncu_launch_rc=$?" >> $OUT/short_$TAG.log
 timeout 300 $SHORT > $OUT/short2_$TAG.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_tile_contract<9" -s 0 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k k_tile_contract -s 1 -c 1 \
     -o $OUT/k5a_$TAG -f $SHORT > $OUT/ncu_full_$TAG.log 2>&1
 echo "ncu_full_rc=$?" >> $OUT/short2_$TAG.log
+MLK_TRACE=1 timeout 300 python bench.py --steps 2 --warmup 3 --e2e-steps 1 --no-cpu-baseline > $OUT/trace_$TAG.log 2>&1
