@@ -106,6 +106,14 @@ mlk_status mlk_ctx_create(int device, int nranks, int rank, void* cuda_stream, m
   CUDA_CHECK(cudaGetDeviceCount(&ndev));
   MLK_REQUIRE(device >= 0 && device < ndev, "invalid device ordinal");
   CUDA_CHECK(cudaSetDevice(device));
+  {
+    // keep freed stream-ordered memory in the pool across synchronisations (the default
+    // threshold 0 returns it to the OS at every sync and re-maps it at the next allocation)
+    cudaMemPool_t pool;
+    CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  }
   auto* h = new mlk_ctx_s();
   h->c.device = device;
   h->c.nranks = nranks;
