@@ -101,6 +101,7 @@ struct GemmDesc {
   int64_t ldc;
   int32_t m, n, k;
   int32_t trans_c;
+  int64_t diag = -1;  // >= 0: store [i + diag == j] - (A B)[i][j] instead of (A B)[i][j]
 };
 // Launch all products on the context stream with FP64 DMMA tiles (64 x 64 x 16); large k
 // is split into fixed chunks whose partial tiles are reduced in chunk order (deterministic).

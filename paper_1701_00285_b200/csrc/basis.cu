@@ -61,11 +61,14 @@ __global__ void k_monomials(const double* __restrict__ Xt, int dp, const LeafJob
 }
 
 struct QrJob {
-  double* A;      // m x nc column-major (lda = m), overwritten by the Householder vectors
+  double* A;      // m x nc column-major (lda = m); factorised in place
   int32_t m, nc;
   double* R;      // nc x nc row-major output
-  double* qlo;    // columns j < nc of Q (each a contiguous row of length m at qlo + j*ldq)
-  double* qhi;    // columns j >= nc of Q at qhi + (j - nc)*ldq
+  double* V;      // scratch m x nc row-major: unit lower-trapezoidal Householder vectors
+  double* T;      // scratch nc x nc: the upper-triangular factor of Q = I - V T V^T
+  double* W1T;    // scratch nc x m row-major: T^T V^T
+  double* qlo;    // rows j < nc of Q^T (row j at qlo + j*ldq)
+  double* qhi;    // rows j >= nc of Q^T at qhi + (j - nc)*ldq
   int64_t ldq;
 };
 
@@ -81,23 +84,27 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return s;
 }
 
-__device__ __forceinline__ double* qcol(const QrJob& jb, int j) {
-  return j < jb.nc ? jb.qlo + (int64_t)j * jb.ldq : jb.qhi + (int64_t)(j - jb.nc) * jb.ldq;
-}
+constexpr int kQrSmemLimit = 200 * 1024;
 
-// Complete Householder QR of one matrix per CTA (LAPACK dgeqr2 + dorg2r conventions:
-// beta = -sign(alpha) ||(alpha, x)||, tau = (beta - alpha) / beta, v = x / (alpha - beta),
-// tau = 0 when x = 0).  Q = H_0 H_1 ... H_{nc-1} is formed explicitly.
-__global__ void __launch_bounds__(256) k_qr(const QrJob* __restrict__ jobs, int* __restrict__ rank_flag) {
-  extern __shared__ double sh[];
+// Householder QR of one matrix per CTA in the LAPACK dgeqr2 convention (beta = -sign(alpha)
+// ||(alpha, x)||, tau = (beta - alpha)/beta, v = x/(alpha - beta), tau = 0 when x = 0), then the
+// compact-WY factor T of Q = H_0 ... H_{nc-1} = I - V T V^T (dlarft, forward, columnwise) and
+// W1T = T^T V^T; Q^T = I - V W1T is then formed by the DMMA GEMM (gemm.cu).  The matrix lives
+// in shared memory when it fits.
+template <bool SMEM>
+__global__ void __launch_bounds__(256) k_qr_wy(const QrJob* __restrict__ jobs, int* __restrict__ rank_flag) {
+  extern __shared__ __align__(16) double sh[];
   __shared__ double s_scal;
+  __shared__ double red[32];
   const QrJob jb = jobs[blockIdx.x];
   const int m = jb.m, nc = jb.nc;
-  double* taus = sh;              // nc
-  double* red = sh + nc;          // 32
-  double* A = jb.A;
+  double* taus = sh;                        // nc
+  double* A = SMEM ? sh + nc + (nc & 1) : jb.A;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-
+  if (SMEM) {
+    for (int64_t e = threadIdx.x; e < (int64_t)m * nc; e += blockDim.x) A[e] = jb.A[e];
+    __syncthreads();
+  }
   for (int k = 0; k < nc; k++) {
     double* ak = A + (int64_t)k * m;
     double part = 0.0;
@@ -116,7 +123,7 @@ __global__ void __launch_bounds__(256) k_qr(const QrJob* __restrict__ jobs, int*
       ak[k] = beta;
     }
     __syncthreads();
-    double scal = s_scal, tau = taus[k];
+    const double scal = s_scal, tau = taus[k];
     for (int i = k + 1 + threadIdx.x; i < m; i += blockDim.x) ak[i] *= scal;
     __syncthreads();
     if (tau != 0.0) {
@@ -127,17 +134,21 @@ __global__ void __launch_bounds__(256) k_qr(const QrJob* __restrict__ jobs, int*
         for (int i = k + 1 + lane; i < m; i += 32) s = fma(ak[i], aj[i], s);
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         s += akj;
-        double f = tau * s;
+        const double f = tau * s;
         if (lane == 0) aj[k] -= f;
         for (int i = k + 1 + lane; i < m; i += 32) aj[i] = fma(-f, ak[i], aj[i]);
       }
     }
     __syncthreads();
   }
-  // R and the rank test (reading R9)
+  // R, rank test (reading R9), V row-major with the unit diagonal made explicit
   for (int e = threadIdx.x; e < nc * nc; e += blockDim.x) {
-    int i = e / nc, j = e % nc;
+    int i = e / nc, j = e - i * nc;
     jb.R[e] = j >= i ? A[(int64_t)j * m + i] : 0.0;
+  }
+  for (int64_t e = threadIdx.x; e < (int64_t)m * nc; e += blockDim.x) {
+    int i = (int)(e / nc), l = (int)(e - (int64_t)i * nc);
+    jb.V[e] = i == l ? 1.0 : (i > l ? A[(int64_t)l * m + i] : 0.0);
   }
   if (threadIdx.x == 0) {
     double mx = 0.0, mn = INFINITY;
@@ -149,28 +160,38 @@ __global__ void __launch_bounds__(256) k_qr(const QrJob* __restrict__ jobs, int*
     if (!(mn > 1e-13 * mx)) atomicExch(rank_flag, 1);
   }
   __syncthreads();
-  // Q = I, then apply H_k for k = nc-1 .. 0 to columns k..m-1 (columns j < k stay e_j)
-  for (int j = warp; j < m; j += nw) {
-    double* q = qcol(jb, j);
-    for (int i = lane; i < m; i += 32) q[i] = (i == j) ? 1.0 : 0.0;
+  // G = V^T V (strict upper part needed), held in T's storage first
+  double* T = jb.T;
+  for (int e = warp; e < nc * nc; e += nw) {
+    int l = e / nc, j = e - l * nc;
+    if (l >= j) continue;
+    double s = 0.0;
+    for (int i = j + lane; i < m; i += 32) s = fma(jb.V[(int64_t)i * nc + l], jb.V[(int64_t)i * nc + j], s);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) T[(int64_t)l * nc + j] = s;
   }
   __syncthreads();
-  for (int k = nc - 1; k >= 0; k--) {
-    double tau = taus[k];
-    if (tau == 0.0) continue;
-    const double* ak = A + (int64_t)k * m;
-    for (int j = k + warp; j < m; j += nw) {
-      double* q = qcol(jb, j);
-      const double qk = q[k];
+  // T[0:j, j] = -tau_j T[0:j, 0:j] G[0:j, j];  T[j, j] = tau_j  (dlarft, forward columnwise)
+  for (int j = 0; j < nc; j++) {
+    const double tj = taus[j];
+    double val = 0.0;
+    int l = threadIdx.x;
+    if (l < j) {
       double s = 0.0;
-      for (int i = k + 1 + lane; i < m; i += 32) s = fma(ak[i], q[i], s);
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      s += qk;
-      double f = tau * s;
-      if (lane == 0) q[k] -= f;
-      for (int i = k + 1 + lane; i < m; i += 32) q[i] = fma(-f, ak[i], q[i]);
+      for (int q = l; q < j; q++) s = fma(T[(int64_t)l * nc + q], T[(int64_t)q * nc + j], s);
+      val = -tj * s;
     }
     __syncthreads();
+    if (l < j) T[(int64_t)l * nc + j] = val;
+    if (threadIdx.x == 0) T[(int64_t)j * nc + j] = tj;
+    __syncthreads();
+  }
+  // W1T = T^T V^T: W1T[l][i] = sum_{q <= l} T[q][l] V[i][q]
+  for (int64_t e = threadIdx.x; e < (int64_t)nc * m; e += blockDim.x) {
+    int l = (int)(e / m), i = (int)(e - (int64_t)l * m);
+    double s = 0.0;
+    for (int q = 0; q <= l; q++) s = fma(T[(int64_t)q * nc + l], jb.V[(int64_t)i * nc + q], s);
+    jb.W1T[e] = s;
   }
 }
 
@@ -188,14 +209,52 @@ __global__ void k_stack_r(const StackJob* __restrict__ jobs, int M) {
   }
 }
 
-void run_qr(Ctx& c, const std::vector<QrJob>& jobs, int nc, int* flag, const char* name) {
+// QR of every job (one CTA each), then Q^T = I - V W1T on the DMMA GEMM, rows < nc to qlo and
+// rows >= nc to qhi.
+void run_qr(Ctx& c, std::vector<QrJob>& jobs, int nc, int* flag, const char* name) {
   if (jobs.empty()) return;
+  int m_max = 0;
+  for (auto& j : jobs) m_max = std::max(m_max, j.m);
+  // scratch for V, T, W1T
+  int64_t per = 0;
+  for (auto& j : jobs) per += 2 * (int64_t)j.m * nc + (int64_t)nc * nc;
+  DevBuf<double> scratch(per, c.stream);
+  int64_t off = 0;
+  for (auto& j : jobs) {
+    j.V = scratch.p + off;
+    off += (int64_t)j.m * nc;
+    j.W1T = scratch.p + off;
+    off += (int64_t)j.m * nc;
+    j.T = scratch.p + off;
+    off += (int64_t)nc * nc;
+  }
   DevBuf<QrJob> dj(jobs.size(), c.stream);
   dj.upload(jobs);
-  size_t smem = (size_t)(nc + 32) * sizeof(double);
-  TimedLaunch tl(c, name);
-  k_qr<<<(unsigned)jobs.size(), 256, smem, c.stream>>>(dj.p, flag);
-  check_launch("k_qr");
+  {
+    TimedLaunch tl(c, name);
+    size_t smem = sizeof(double) * ((size_t)nc + 1 + (size_t)m_max * nc);
+    if (smem <= (size_t)kQrSmemLimit) {
+      CUDA_CHECK(cudaFuncSetAttribute(k_qr_wy<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      k_qr_wy<true><<<(unsigned)jobs.size(), 256, smem, c.stream>>>(dj.p, flag);
+    } else {
+      size_t sm2 = sizeof(double) * ((size_t)nc + 1);
+      k_qr_wy<false><<<(unsigned)jobs.size(), 256, sm2, c.stream>>>(dj.p, flag);
+    }
+    check_launch("k_qr_wy");
+  }
+  std::vector<GemmDesc> gd;
+  for (auto& j : jobs) {
+    GemmDesc lo{j.V, nc, j.W1T, j.m, j.qlo, j.ldq, nc, j.m, nc, 0};
+    lo.diag = 0;
+    gd.push_back(lo);
+    if (j.m > nc) {
+      GemmDesc hi{j.V + (int64_t)nc * nc, nc, j.W1T, j.m, j.qhi, j.ldq, j.m - nc, j.m, nc, 0};
+      hi.diag = nc;
+      gd.push_back(hi);
+    }
+  }
+  std::string gname = std::string(name) + "_formq";
+  gemm_batched(c, gd, gname.c_str());
 }
 
 }  // namespace

@@ -102,8 +102,10 @@ __global__ void __launch_bounds__(128) k_gemm(const GemmDesc* __restrict__ descs
         } else {
           int gm = job.m0 + r, gn = job.n0 + cc;
           if (gm < g.m && gn < g.n) {
-            if (g.trans_c) g.C[(int64_t)gn * g.ldc + gm] = acc[i][j][e];
-            else g.C[(int64_t)gm * g.ldc + gn] = acc[i][j][e];
+            double v = acc[i][j][e];
+            if (g.diag >= 0) v = ((int64_t)gm + g.diag == gn ? 1.0 : 0.0) - v;
+            if (g.trans_c) g.C[(int64_t)gn * g.ldc + gm] = v;
+            else g.C[(int64_t)gm * g.ldc + gn] = v;
           }
         }
       }
@@ -126,6 +128,7 @@ __global__ void k_gemm_reduce(const GemmDesc* __restrict__ descs, const ReduceJo
     if (gm >= g.m || gn >= g.n) continue;
     double s = 0.0;
     for (int p = 0; p < job.nparts; p++) s += partials[(job.first + p) * BM * BN + e];
+    if (g.diag >= 0) s = ((int64_t)gm + g.diag == gn ? 1.0 : 0.0) - s;
     if (g.trans_c) g.C[(int64_t)gn * g.ldc + gm] = s;
     else g.C[(int64_t)gm * g.ldc + gn] = s;
   }
