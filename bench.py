@@ -318,7 +318,8 @@ def main():
                      "tflops_assembly": flops / (asm_ms * 1e-3) / 1e12 if asm_ms > 0 else None,
                      "pct_of_peak_step": 100.0 * flops / (ms_per_step * 1e-3) / 1e12 / peak,
                      "peak_tflops": peak, "peak_source": "measured, profiles/fp64_peak_r01.json (DMMA loop)"},
-            "roofline": {"kernel": "assemble_tile_contract (K5a)", "bound": "fp64", "achieved": achieved,
+            "roofline": {"kernel": "assemble_tile_contract (K5a)", "bound": "tensor",
+                         "pipe": "FP64 DMMA.8x8x4 (shares the FP64 pipe with DFMA, DESIGN.md section 6)", "achieved": achieved,
                          "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_flops_per_step": k5_flops, "ms_per_step": k5_ms_per_step},
             "kernels_ms_per_step": {k: v["ms"] / args.steps for k, v in sorted(stats.items())},
