@@ -72,127 +72,157 @@ struct QrJob {
   int64_t ldq;
 };
 
-__device__ __forceinline__ double block_sum(double v, double* red) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __syncthreads();
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  double s = 0.0;
-  int nw = blockDim.x >> 5;
-  for (int i = 0; i < nw; i++) s += red[i];
-  return s;
-}
-
-constexpr int kQrSmemLimit = 200 * 1024;
+constexpr int kQrSmemLimit = 225 * 1024;
 
 // Householder QR of one matrix per CTA in the LAPACK dgeqr2 convention (beta = -sign(alpha)
 // ||(alpha, x)||, tau = (beta - alpha)/beta, v = x/(alpha - beta), tau = 0 when x = 0), then the
 // compact-WY factor T of Q = H_0 ... H_{nc-1} = I - V T V^T (dlarft, forward, columnwise) and
-// W1T = T^T V^T; Q^T = I - V W1T is then formed by the DMMA GEMM (gemm.cu).  The matrix lives
-// in shared memory when it fits.
-template <bool SMEM>
+// W1T = T^T V^T; Q^T = I - V W1T is then formed by the DMMA GEMM (gemm.cu).
+// Column step k takes two barriers: (1) every thread computes partial dot products
+// x . a_j over a chunk of rows for the columns j >= k (j = k gives |x|^2); (2) every thread
+// derives beta, tau and the scale redundantly and applies H_k to its (column, chunk) items,
+// reading the unscaled x (the scaling of column k and beta are stored in the next step).
+// SMEM: the matrix (whose strict lower part becomes V) lives in shared memory with an odd
+// column stride; TS: the Gram matrix G = V^T V (transposed) and T live there too.
+template <bool SMEM, bool TS>
 __global__ void __launch_bounds__(256) k_qr_wy(const QrJob* __restrict__ jobs, int* __restrict__ rank_flag) {
   extern __shared__ __align__(16) double sh[];
-  __shared__ double s_scal;
-  __shared__ double red[32];
   const QrJob jb = jobs[blockIdx.x];
   const int m = jb.m, nc = jb.nc;
-  double* taus = sh;                        // nc
-  double* A = SMEM ? sh + nc + (nc & 1) : jb.A;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nch = min(16, (m + 31) / 32);          // row chunks of the column items
+  const int L = (m + nch - 1) / nch;
+  const int lda = SMEM ? (m | 1) : m;
+  double* taus = sh;                                // nc
+  double* rowk = taus + nc;                         // nc: row k of the trailing columns
+  double* part = rowk + nc;                         // nc * nch partial dot products
+  double* A = SMEM ? part + nc * nch : jb.A;
+  double* T = TS ? A + (int64_t)lda * nc : jb.T;    // T[l][j], row-major nc x nc
+  double* Gt = TS ? T + (int64_t)nc * nc : jb.W1T;  // Gt[j][l] = G[l][j] (scratch)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   if (SMEM) {
-    for (int64_t e = threadIdx.x; e < (int64_t)m * nc; e += blockDim.x) A[e] = jb.A[e];
-    __syncthreads();
-  }
-  for (int k = 0; k < nc; k++) {
-    double* ak = A + (int64_t)k * m;
-    double part = 0.0;
-    for (int i = k + 1 + threadIdx.x; i < m; i += blockDim.x) part = fma(ak[i], ak[i], part);
-    double xn2 = block_sum(part, red);
-    if (threadIdx.x == 0) {
-      double alpha = ak[k];
-      double tau = 0.0, scal = 1.0, beta = alpha;
-      if (xn2 > 0.0) {
-        beta = -copysign(sqrt(fma(alpha, alpha, xn2)), alpha);
-        tau = (beta - alpha) / beta;
-        scal = 1.0 / (alpha - beta);
-      }
-      taus[k] = tau;
-      s_scal = scal;
-      ak[k] = beta;
+    for (int64_t e = tid; e < (int64_t)m * nc; e += blockDim.x) {
+      const int j = (int)(e / m), i = (int)(e - (int64_t)j * m);
+      A[(int64_t)j * lda + i] = jb.A[e];
     }
     __syncthreads();
-    const double scal = s_scal, tau = taus[k];
-    for (int i = k + 1 + threadIdx.x; i < m; i += blockDim.x) ak[i] *= scal;
+  }
+  double scal_prev = 1.0, beta_prev = 0.0;
+  for (int k = 0; k <= nc; k++) {
+    // finish column k - 1: store beta on the diagonal, scale x into v
+    if (k > 0) {
+      double* ap = A + (int64_t)(k - 1) * lda;
+      for (int i = k + tid; i < m; i += blockDim.x) ap[i] *= scal_prev;
+      if (tid == 0) ap[k - 1] = beta_prev;
+    }
+    if (k == nc) break;
+    const double* ak = A + (int64_t)k * lda;
+    // (1) partial dots for columns j >= k over rows i > k, and a copy of row k
+    const int nitem = (nc - k) * nch;
+    for (int it = tid; it < nitem; it += blockDim.x) {
+      const int c = it % nch, jj = it / nch;
+      const double* aj = A + (int64_t)(k + jj) * lda;
+      const int i0 = max(k + 1, c * L), i1 = min(m, (c + 1) * L);
+      double s = 0.0;
+      for (int i = i0; i < i1; i++) s = fma(ak[i], aj[i], s);
+      part[jj * nch + c] = s;
+      if (c == 0) rowk[jj] = aj[k];
+    }
     __syncthreads();
+    // (2) reflector (redundantly per thread) and its application to columns j > k
+    double xn2 = 0.0;
+    for (int c = 0; c < nch; c++) xn2 += part[c];
+    const double alpha = rowk[0];
+    double tau = 0.0, scal = 1.0, beta = alpha;
+    if (xn2 > 0.0) {
+      beta = -copysign(sqrt(fma(alpha, alpha, xn2)), alpha);
+      tau = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    if (tid == 0) taus[k] = tau;
     if (tau != 0.0) {
-      for (int j = k + 1 + warp; j < nc; j += nw) {
-        double* aj = A + (int64_t)j * m;
-        const double akj = aj[k];  // read before the warp reduction (lane 0 writes it after)
-        double s = 0.0;
-        for (int i = k + 1 + lane; i < m; i += 32) s = fma(ak[i], aj[i], s);
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        s += akj;
-        const double f = tau * s;
-        if (lane == 0) aj[k] -= f;
-        for (int i = k + 1 + lane; i < m; i += 32) aj[i] = fma(-f, ak[i], aj[i]);
+      const int nup = (nc - k - 1) * nch;
+      for (int it = tid; it < nup; it += blockDim.x) {
+        const int c = it % nch, jj = 1 + it / nch;
+        double* aj = A + (int64_t)(k + jj) * lda;
+        double dsum = 0.0;
+        for (int c2 = 0; c2 < nch; c2++) dsum += part[jj * nch + c2];
+        const double akj = rowk[jj];
+        const double f = tau * fma(scal, dsum, akj);
+        const double g = f * scal;
+        const int i0 = max(k + 1, c * L), i1 = min(m, (c + 1) * L);
+        for (int i = i0; i < i1; i++) aj[i] = fma(-g, ak[i], aj[i]);
+        if (c == 0) aj[k] = akj - f;
       }
     }
+    scal_prev = scal;
+    beta_prev = beta;
     __syncthreads();
   }
+  __syncthreads();
   // R, rank test (reading R9), V row-major with the unit diagonal made explicit
-  for (int e = threadIdx.x; e < nc * nc; e += blockDim.x) {
+  for (int e = tid; e < nc * nc; e += blockDim.x) {
     int i = e / nc, j = e - i * nc;
-    jb.R[e] = j >= i ? A[(int64_t)j * m + i] : 0.0;
+    jb.R[e] = j >= i ? A[(int64_t)j * lda + i] : 0.0;
   }
-  for (int64_t e = threadIdx.x; e < (int64_t)m * nc; e += blockDim.x) {
+  for (int64_t e = tid; e < (int64_t)m * nc; e += blockDim.x) {
     int i = (int)(e / nc), l = (int)(e - (int64_t)i * nc);
-    jb.V[e] = i == l ? 1.0 : (i > l ? A[(int64_t)l * m + i] : 0.0);
+    jb.V[e] = i == l ? 1.0 : (i > l ? A[(int64_t)l * lda + i] : 0.0);
   }
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     double mx = 0.0, mn = INFINITY;
     for (int i = 0; i < nc; i++) {
-      double v = fabs(A[(int64_t)i * m + i]);
+      double v = fabs(A[(int64_t)i * lda + i]);
       mx = fmax(mx, v);
       mn = fmin(mn, v);
     }
     if (!(mn > 1e-13 * mx)) atomicExch(rank_flag, 1);
   }
-  __syncthreads();
-  // G = V^T V (strict upper part needed), held in T's storage first
-  double* T = jb.T;
-  for (int e = warp; e < nc * nc; e += nw) {
-    int l = e / nc, j = e - l * nc;
+  // G[l][j] = (V^T V)[l][j] for l < j: column l of V is (0.., 1 at l, A[l*lda + i] for i > l),
+  // so G[l][j] = A[l*lda + j] + sum_{i > j} A[l*lda + i] A[j*lda + i]; stored as Gt[j][l].
+  // One thread per pair, serial over rows.
+  for (int e = tid; e < nc * nc; e += blockDim.x) {
+    const int j = e / nc, l = e - j * nc;
     if (l >= j) continue;
-    double s = 0.0;
-    for (int i = j + lane; i < m; i += 32) s = fma(jb.V[(int64_t)i * nc + l], jb.V[(int64_t)i * nc + j], s);
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) T[(int64_t)l * nc + j] = s;
+    const double* vl = A + (int64_t)l * lda;
+    const double* vj = A + (int64_t)j * lda;
+    double s = vl[j];
+    for (int i = j + 1; i < m; i++) s = fma(vl[i], vj[i], s);
+    Gt[(int64_t)j * nc + l] = s;
   }
   __syncthreads();
-  // T[0:j, j] = -tau_j T[0:j, 0:j] G[0:j, j];  T[j, j] = tau_j  (dlarft, forward columnwise)
+  // T[0:j, j] = -tau_j T[0:j, 0:j] G[0:j, j];  T[j, j] = tau_j  (dlarft, forward columnwise):
+  // warp per row l, lanes over q in [l, j)
   for (int j = 0; j < nc; j++) {
     const double tj = taus[j];
-    double val = 0.0;
-    int l = threadIdx.x;
-    if (l < j) {
+    const double* gj = Gt + (int64_t)j * nc;
+    for (int l = warp; l < j; l += nw) {
+      const double* tl = T + (int64_t)l * nc;
       double s = 0.0;
-      for (int q = l; q < j; q++) s = fma(T[(int64_t)l * nc + q], T[(int64_t)q * nc + j], s);
-      val = -tj * s;
+      for (int q = l + lane; q < j; q += 32) s = fma(tl[q], gj[q], s);
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) T[(int64_t)l * nc + j] = -tj * s;
     }
-    __syncthreads();
-    if (l < j) T[(int64_t)l * nc + j] = val;
-    if (threadIdx.x == 0) T[(int64_t)j * nc + j] = tj;
+    if (tid == 0) T[(int64_t)j * nc + j] = tj;
     __syncthreads();
   }
-  // W1T = T^T V^T: W1T[l][i] = sum_{q <= l} T[q][l] V[i][q]
-  for (int64_t e = threadIdx.x; e < (int64_t)nc * m; e += blockDim.x) {
+  // W1T = T^T V^T: W1T[l][i] = sum_{q <= min(l, i)} T[q][l] V[i][q], V[i][q] = A[q*lda + i] (i > q)
+  for (int64_t e = tid; e < (int64_t)nc * m; e += blockDim.x) {
     int l = (int)(e / m), i = (int)(e - (int64_t)l * m);
     double s = 0.0;
-    for (int q = 0; q <= l; q++) s = fma(T[(int64_t)q * nc + l], jb.V[(int64_t)i * nc + q], s);
+    const int qe = min(l, i - 1);
+    for (int q = 0; q <= qe; q++) s = fma(T[(int64_t)q * nc + l], A[(int64_t)q * lda + i], s);
+    if (i <= l) s += T[(int64_t)i * nc + l];
     jb.W1T[e] = s;
   }
+}
+
+// dynamic shared memory of k_qr_wy: taus, rowk, partials (+ A) (+ T, Gt)
+inline size_t qr_smem(int m, int nc, bool a_in, bool t_in) {
+  const int nch = std::min(16, (m + 31) / 32);
+  size_t d = 2 * (size_t)nc + (size_t)nc * nch;
+  if (a_in) d += (size_t)(m | 1) * nc;
+  if (t_in) d += 2 * (size_t)nc * nc;
+  return d * sizeof(double);
 }
 
 // [R_L; R_R] (2M x M, column-major) for every internal cell of a level
@@ -232,13 +262,17 @@ void run_qr(Ctx& c, std::vector<QrJob>& jobs, int nc, int* flag, const char* nam
   dj.upload(jobs);
   {
     TimedLaunch tl(c, name);
-    size_t smem = sizeof(double) * ((size_t)nc + 1 + (size_t)m_max * nc);
-    if (smem <= (size_t)kQrSmemLimit) {
-      CUDA_CHECK(cudaFuncSetAttribute(k_qr_wy<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      k_qr_wy<true><<<(unsigned)jobs.size(), 256, smem, c.stream>>>(dj.p, flag);
+    const size_t s_full = qr_smem(m_max, nc, true, true), s_a = qr_smem(m_max, nc, true, false);
+    if (s_full <= (size_t)kQrSmemLimit) {
+      CUDA_CHECK(cudaFuncSetAttribute(k_qr_wy<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_full));
+      k_qr_wy<true, true><<<(unsigned)jobs.size(), 256, s_full, c.stream>>>(dj.p, flag);
+    } else if (s_a <= (size_t)kQrSmemLimit) {
+      CUDA_CHECK(cudaFuncSetAttribute(k_qr_wy<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_a));
+      k_qr_wy<true, false><<<(unsigned)jobs.size(), 256, s_a, c.stream>>>(dj.p, flag);
     } else {
-      size_t sm2 = sizeof(double) * ((size_t)nc + 1);
-      k_qr_wy<false><<<(unsigned)jobs.size(), 256, sm2, c.stream>>>(dj.p, flag);
+      const size_t s0 = qr_smem(m_max, nc, false, false);
+      CUDA_CHECK(cudaFuncSetAttribute(k_qr_wy<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s0));
+      k_qr_wy<false, false><<<(unsigned)jobs.size(), 256, s0, c.stream>>>(dj.p, flag);
     }
     check_launch("k_qr_wy");
   }

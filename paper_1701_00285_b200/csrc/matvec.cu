@@ -156,6 +156,9 @@ void cov_matvec_dev(Ctx& c, const mlk_tree_s* tree, const mlk_kernel& k, const d
   std::vector<TileUnit> units;
   // rows r0..r1 as an a range; b range = all points; W_b = the vectors a (nvec x n)
   make_tile_units(units, r0, (int32_t)(r1 - r0), 0, (int32_t)n, a, n, nvec, b + r0, n, 1, tree->d_pad);
+  // up to 4 vectors: lane-local DFMA contraction instead of 8-column DMMAs (tile.cu, NV)
+  if (nvec <= 4)
+    for (auto& u : units) u.rq = nvec == 1 ? -1 : nvec == 2 ? -2 : -4;
   run_tile_contract(c, tree, make_kernel_params(k), units, "cov_matvec_tile");
 }
 

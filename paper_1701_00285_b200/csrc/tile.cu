@@ -1,11 +1,15 @@
 // K5a: fused covariance-tile generation + first contraction on FP64 DMMA (see tile.cuh).
 //
-// CTA = 4 warps, 32 rows of the a range (8 per warp).  The b range is streamed in stages of
-// BN points (cp.async double buffering): the stage holds the b coordinates (BN x dp), their
-// squared norms and the W_b columns (8 RQ rows x BN, 16-byte chunks XOR-swizzled so the
+// CTA = 4 warps, 32 rows of the a range (8 per warp).  Coordinates enter as augmented,
+// pre-scaled rows (k_tile_aug): Pa = [u, |u|^2, 1], Pb = [-2u, 1, |u|^2] with u = scale * x, so
+// the Gram DMMAs produce z^2 = |u_a - u_b|^2 directly (no norm loads, no FP64 fix-up).  The
+// b range is streamed in stages of BN points (cp.async double buffering): the stage holds the
+// b rows (BN x dpa) and the W_b columns (8 RQ rows x BN, 16-byte chunks XOR-swizzled so the
 // B-fragment loads are bank-conflict free).  Per 8-point sub-tile a warp
-//   1. forms S = X_a X_b^T with dp/4 DMMA.8x8x4 (k = coordinates),
-//   2. turns its two accumulator entries into covariances in registers,
+//   1. forms z^2 with dpa/4 DMMA.8x8x4,
+//   2. turns its two accumulator entries into correlations in registers (fastmath.cuh; the
+//      same-site entry is set to 1 + nugget/sigma2 exactly, sigma2 is applied once in the
+//      epilogue),
 //   3. feeds them straight back as DMMA A-fragments: accumulator column 2(lane%4)+s is the
 //      A element k = lane%4 of k-step s, provided W_b is read with the same point
 //      permutation -- no shuffles between the two products,
@@ -25,12 +29,16 @@ KernelParams make_kernel_params(const mlk_kernel& k) {
   p.family = k.family;
   p.sigma2 = k.sigma2;
   p.nugget = k.nugget;
+  p.same_val = 1.0 + k.nugget / k.sigma2;
   switch (k.family) {
     case MLK_MATERN_12: p.c1 = 1.0 / k.rho; break;
     case MLK_MATERN_32: p.c1 = std::sqrt(3.0) / k.rho; break;
     case MLK_MATERN_52: p.c1 = std::sqrt(5.0) / k.rho; break;
     default: p.c1 = 1.0 / (k.rho * k.rho); break;
   }
+  // coordinates are pre-scaled so that the augmented Gram product is z^2 = (c1 r)^2
+  // (Matern) or r^2 / rho^2 (Gaussian)
+  p.scale = k.family == MLK_GAUSSIAN ? 1.0 / k.rho : p.c1;
   return p;
 }
 
@@ -74,39 +82,73 @@ void make_tile_units(std::vector<TileUnit>& out, int64_t a_begin, int32_t s_a, i
 
 namespace {
 
+// correlation phi from the augmented Gram value x = z^2 (Matern, z = sqrt(2 nu) r / rho) or
+// x = r^2 / rho^2 (Gaussian); R16, R17
 template <int FAM>
-__device__ __forceinline__ double corr(double r2, double c1, const double* tab) {
-  if (FAM == MLK_GAUSSIAN) return exp_neg(-r2 * c1, tab);
-  double z = sqrt_pos(r2) * c1;
-  double e = exp_neg(-z, tab);
+__device__ __forceinline__ double corr(double x, const double* tab) {
+  if (FAM == MLK_GAUSSIAN) return exp_neg(x, tab);  // x >= -O(u|y|^2): e^{-x} stays ~1
+  x = clamp_pos(x);
+  const double z = sqrt_pos(x);
+  const double e = exp_neg(z, tab);
   if (FAM == MLK_MATERN_12) return e;
   if (FAM == MLK_MATERN_32) return fma(z, e, e);                  // (1 + z) e^{-z}
-  return fma(z, fma(z, 1.0 / 3.0, 1.0), 1.0) * e;                // (1 + z + z^2/3) e^{-z}
+  return fma(e, fma(x, 1.0 / 3.0, z), e);                         // (1 + z + z^2/3) e^{-z}
 }
 
 template <int RQ>
 struct TileCfg {
-  static constexpr int BN = RQ >= 6 ? 16 : 32;  // b points per stage
+  static constexpr int BN = RQ >= 6 ? 16 : 32;   // b points per stage
   static constexpr int WROWS = 8 * RQ;
+  static constexpr int G = RQ <= 12 ? RQ : 8;    // W_b fragments held per DMMA group
 };
 
-__host__ __device__ constexpr int stage_doubles(int rq, int bn, int dp) { return bn * dp + bn + 8 * rq * bn; }
+__host__ __device__ constexpr int stage_doubles(int rq, int bn, int sdp) { return bn * sdp + 8 * rq * bn; }
 
-template <int RQ, int FAM>
-__global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4) k_tile_contract(const TileUnit* __restrict__ units, int n_units,
-                                                       int* __restrict__ counter, const double* __restrict__ Xt,
-                                                       const double* __restrict__ norm2, int dp, KernelParams kp) {
+// Augmented, pre-scaled coordinates (x in tree order, s = kp.scale, u = s x):
+//   Pa[i] = [u_i, |u_i|^2, 1, 0...],  Pb[i] = [-2 u_i, 1, |u_i|^2, 0...]
+// so that one DMMA dot product gives Pa[i].Pb[j] = |u_i - u_j|^2 (the Gram identity) directly.
+__global__ void k_tile_aug(const double* __restrict__ Xt, int dpt, int d, int64_t n, double s,
+                           double* __restrict__ Pa, double* __restrict__ Pb, int dpa) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* x = Xt + i * dpt;
+  double* pa = Pa + i * dpa;
+  double* pb = Pb + i * dpa;
+  double nn = 0.0;
+  for (int k = 0; k < d; k++) {
+    const double u = s * x[k];
+    nn = fma(u, u, nn);
+    pa[k] = u;
+    pb[k] = -2.0 * u;
+  }
+  pa[d] = nn;
+  pa[d + 1] = 1.0;
+  pb[d] = 1.0;
+  pb[d + 1] = nn;
+  for (int k = d + 2; k < dpa; k++) pa[k] = pb[k] = 0.0;
+}
+
+// NV > 0 (with RQ = 1): the contraction has NV <= 4 columns (C a for a few vectors) and is done
+// with DFMAs per lane instead of 8-column DMMAs; the four lanes of a quad hold disjoint column
+// subsets of a row and are summed by two shuffles in the epilogue (fixed order).
+template <int RQ, int FAM, int NV>
+__global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4)
+    k_tile_contract(const TileUnit* __restrict__ units, int n_units, int* __restrict__ counter,
+                    const double* __restrict__ Pa, const double* __restrict__ Pb, int dpa, int sdp,
+                    KernelParams kp) {
   constexpr int BN = TileCfg<RQ>::BN;
   constexpr int WROWS = TileCfg<RQ>::WROWS;
+  constexpr int G = TileCfg<RQ>::G;
+  constexpr int T = BN / 8;
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_unit;
-  __shared__ double s_tab[16];
-  if (threadIdx.x < 16) s_tab[threadIdx.x] = kExp2Tab16[threadIdx.x];
-  const int sd = stage_doubles(RQ, BN, dp);
-  double* As = sm;                  // 32 x dp
-  double* An = sm + 32 * dp;        // 32
-  double* St = sm + 32 * dp + 32;   // 2 stages
+  __shared__ double s_tab[64];
+  if (threadIdx.x < 64) s_tab[threadIdx.x] = kExp2Tab64[threadIdx.x];
+  const int sd = stage_doubles(RQ, BN, sdp);
+  double* As = sm;                  // 32 x sdp
+  double* St = sm + 32 * sdp;       // 2 stages
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ks_n = dpa >> 2;
 
   while (true) {
     __syncthreads();
@@ -117,40 +159,38 @@ __global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4) k_tile_contract(const T
     const TileUnit u = units[ui];
     const int64_t a0 = u.a_begin + u.row0;
     const int rows = min(32, u.s_a - u.row0);
-    // a tile (rows x dp) + norms
-    for (int e = tid; e < 32 * dp; e += 128) {
-      int r = e / dp;
-      As[e] = r < rows ? Xt[(a0 + r) * dp + (e - r * dp)] : 0.0;
+    // a tile (rows x dpa); rows past the range are zero (their outputs are discarded)
+    {
+      const int cpr = dpa >> 1;
+      for (int e = tid; e < 32 * cpr; e += 128) {
+        const int r = e / cpr, ch = e - r * cpr;
+        const bool ok = r < rows;
+        cp_async16(As + r * sdp + 2 * ch, ok ? Pa + (a0 + r) * dpa + 2 * ch : Pa, ok);
+      }
     }
-    if (tid < 32) An[tid] = tid < rows ? norm2[a0 + tid] : 0.0;
 
     auto load_stage = [&](int st, int b0) {
       double* Xs = St + st * sd;
-      double* Ns = Xs + BN * dp;
-      double* Ws = Ns + BN;
+      double* Ws = Xs + BN * sdp;
       const int nb = min(BN, u.s_b - b0);
-      // coordinates: rows of dp doubles, 16-byte chunks
-      const int cpr = dp / 2;
+      // b coordinates: rows of dpa doubles, 16-byte chunks; rows past the range are zero
+      const int cpr = dpa >> 1;
       for (int e = tid; e < BN * cpr; e += 128) {
-        int y = e / cpr, ch = e - y * cpr;
-        bool ok = y < nb;
-        const double* src = ok ? Xt + (u.b_begin + b0 + y) * dp + 2 * ch : Xt;
-        cp_async16(Xs + y * dp + 2 * ch, src, ok);
+        const int y = e / cpr, ch = e - y * cpr;
+        const bool ok = y < nb;
+        cp_async16(Xs + y * sdp + 2 * ch, ok ? Pb + (u.b_begin + b0 + y) * dpa + 2 * ch : Pb, ok);
       }
-      for (int y = tid; y < BN; y += 128) {
-        bool ok = y < nb;
-        cp_async8(Ns + y, ok ? norm2 + u.b_begin + b0 + y : norm2, ok);
-      }
-      // W_b columns b0..b0+BN of rows c0..c0+8RQ, chunk c of row rho at (c ^ 4(rho&1))
+      // W_b columns b0..b0+BN of rows c0..c0+8RQ, chunk c of row rho at (c ^ 4(rho&1));
+      // missing rows / columns are zero, so padded points contribute nothing
       constexpr int CH = BN / 2;
       for (int e = tid; e < WROWS * CH; e += 128) {
-        int rho = e / CH, ch = e - rho * CH;
-        int phys = ch ^ ((rho & 1) << 2);
+        const int rho = e / CH, ch = e - rho * CH;
+        const int phys = ch ^ ((rho & 1) << 2);
         double* dst = Ws + rho * BN + 2 * phys;
-        int y = b0 + 2 * ch;
-        bool rowok = rho < u.qc;
+        const int y = b0 + 2 * ch;
+        const bool rowok = rho < u.qc;
         const double* src = u.Wb + (int64_t)(u.c0 + rho) * u.ldw + y;
-        bool ok0 = rowok && (y < u.s_b), ok1 = rowok && (y + 1 < u.s_b);
+        const bool ok0 = rowok && (y < u.s_b), ok1 = rowok && (y + 1 < u.s_b);
         if (ok0 && ok1 && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
           cp_async16(dst, src, true);
         } else {
@@ -163,87 +203,110 @@ __global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4) k_tile_contract(const T
     double acc[RQ][2];
 #pragma unroll
     for (int i = 0; i < RQ; i++) acc[i][0] = acc[i][1] = 0.0;
+    double accv[NV > 0 ? NV : 1];
+#pragma unroll
+    for (int i = 0; i < (NV > 0 ? NV : 1); i++) accv[i] = 0.0;
 
     const int nst = (u.s_b + BN - 1) / BN;
     load_stage(0, 0);
     cp_async_commit();
-    __syncthreads();  // As/An visible
     const int ar = warp * 8 + (lane >> 2);
-    const double na = An[ar];
     const int64_t ga = a0 + ar;
-    const int ks_n = dp >> 2;
     for (int s = 0; s < nst; s++) {
       if (s + 1 < nst) load_stage((s + 1) & 1, (s + 1) * BN);
       cp_async_commit();
       cp_async_wait<1>();
       __syncthreads();
       const double* Xs = St + (s & 1) * sd;
-      const double* Ns = Xs + BN * dp;
-      const double* Ws = Ns + BN;
-      const int b0 = s * BN;
-      constexpr int T = BN / 8;
-      // 1. Gram S = X_a X_b^T for the T sub-tiles (independent accumulator chains)
+      const double* Ws = Xs + BN * sdp;
+      const int64_t gb0 = u.b_begin + s * BN;
+      // 1. augmented Gram: g = |u_a - u_b|^2 for the T sub-tiles (independent chains)
       double g[T][2];
 #pragma unroll
       for (int t = 0; t < T; t++) g[t][0] = g[t][1] = 0.0;
+      const double* ap = As + ar * sdp + (lane & 3);
+      const double* bp = Xs + (lane >> 2) * sdp + (lane & 3);
+#pragma unroll 4
       for (int ks = 0; ks < ks_n; ks++) {
-        const double a = As[ar * dp + 4 * ks + (lane & 3)];
+        const double a = ap[4 * ks];
 #pragma unroll
-        for (int t = 0; t < T; t++) {
-          const double b = Xs[(8 * t + (lane >> 2)) * dp + 4 * ks + (lane & 3)];
-          dmma_8x8x4(g[t][0], g[t][1], a, b);
-        }
+        for (int t = 0; t < T; t++) dmma_8x8x4(g[t][0], g[t][1], a, bp[8 * t * sdp + 4 * ks]);
       }
-      // 2. covariances in registers (Gram identity, clamp, same-site fix, closed form)
+      // 2. covariances in registers: closed form, same-site entries exactly 1 + nugget/sigma2
       double cv[T][2];
 #pragma unroll
       for (int t = 0; t < T; t++) {
-        const int col = 8 * t + 2 * (lane & 3);
+        const int64_t gcol = gb0 + 8 * t + 2 * (lane & 3);
 #pragma unroll
         for (int e = 0; e < 2; e++) {
-          double r2 = fmax(fma(-2.0, g[t][e], na + Ns[col + e]), 0.0);
-          const bool same = (u.b_begin + b0 + col + e) == ga;
-          if (same) r2 = 0.0;
-          double v = kp.sigma2 * corr<FAM>(r2, kp.c1, s_tab);
-          cv[t][e] = same ? v + kp.nugget : v;
+          const double v = corr<FAM>(g[t][e], s_tab);
+          cv[t][e] = (gcol + e == ga) ? kp.same_val : v;
         }
       }
-      // 3./4. accumulator entries are the A fragments of k-steps s = 0, 1; W_b fragments
-      // are loaded 4 n-tiles at a time so consecutive DMMAs are independent
+      if constexpr (NV > 0) {
+        // 3'. C a for NV vectors: lane-local DFMAs over the lane's two columns per sub-tile
 #pragma unroll
-      for (int t = 0; t < T; t++) {
+        for (int t = 0; t < T; t++) {
+          const int ch = 4 * t + (lane & 3);
 #pragma unroll
-        for (int q0 = 0; q0 < RQ; q0 += 4) {
-          double2 w[4];
-#pragma unroll
-          for (int qq = 0; qq < 4; qq++) {
-            if (q0 + qq < RQ) {
-              const int rho = 8 * (q0 + qq) + (lane >> 2);
-              const int ch = 4 * t + (lane & 3);
-              w[qq] = *reinterpret_cast<const double2*>(Ws + rho * BN + 2 * (ch ^ ((rho & 1) << 2)));
-            }
+          for (int l = 0; l < NV; l++) {
+            const double2 wv = *reinterpret_cast<const double2*>(Ws + l * BN + 2 * (ch ^ ((l & 1) << 2)));
+            accv[l] = fma(cv[t][0], wv.x, accv[l]);
+            accv[l] = fma(cv[t][1], wv.y, accv[l]);
           }
+        }
+      } else {
+        // 3./4. the accumulator entries are the A fragments of k-steps 0, 1 (no shuffles); W_b
+        // fragments for G n-tiles are held in registers so the G DMMAs of a k-step are
+        // independent of each other
 #pragma unroll
-          for (int qq = 0; qq < 4; qq++)
-            if (q0 + qq < RQ) dmma_8x8x4(acc[q0 + qq][0], acc[q0 + qq][1], cv[t][0], w[qq].x);
+        for (int t = 0; t < T; t++) {
 #pragma unroll
-          for (int qq = 0; qq < 4; qq++)
-            if (q0 + qq < RQ) dmma_8x8x4(acc[q0 + qq][0], acc[q0 + qq][1], cv[t][1], w[qq].y);
+          for (int q0 = 0; q0 < RQ; q0 += G) {
+            double2 w[G];
+#pragma unroll
+            for (int qq = 0; qq < G; qq++) {
+              if (q0 + qq < RQ) {
+                const int rho = 8 * (q0 + qq) + (lane >> 2);
+                const int ch = 4 * t + (lane & 3);
+                w[qq] = *reinterpret_cast<const double2*>(Ws + rho * BN + 2 * (ch ^ ((rho & 1) << 2)));
+              }
+            }
+#pragma unroll
+            for (int qq = 0; qq < G; qq++)
+              if (q0 + qq < RQ) dmma_8x8x4(acc[q0 + qq][0], acc[q0 + qq][1], cv[t][0], w[qq].x);
+#pragma unroll
+            for (int qq = 0; qq < G; qq++)
+              if (q0 + qq < RQ) dmma_8x8x4(acc[q0 + qq][0], acc[q0 + qq][1], cv[t][1], w[qq].y);
+          }
         }
       }
       __syncthreads();
     }
-    // epilogue
+    // epilogue: U = sigma2 * acc
     const int r = u.row0 + ar;
-    if (r < u.s_a) {
+    if constexpr (NV > 0) {
+#pragma unroll
+      for (int l = 0; l < NV; l++) {
+        double v = accv[l];
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        if ((lane & 3) == 0 && r < u.s_a && l < u.qc) {
+          v *= kp.sigma2;
+          if (u.trans) u.U[(int64_t)(u.c0 + l) * u.ldu + r] = v;
+          else u.U[(int64_t)r * u.ldu + u.c0 + l] = v;
+        }
+      }
+    } else if (r < u.s_a) {
 #pragma unroll
       for (int q = 0; q < RQ; q++) {
 #pragma unroll
         for (int e = 0; e < 2; e++) {
-          int l = 8 * q + 2 * (lane & 3) + e;
+          const int l = 8 * q + 2 * (lane & 3) + e;
           if (l < u.qc) {
-            if (u.trans) u.U[(int64_t)(u.c0 + l) * u.ldu + r] = acc[q][e];
-            else u.U[(int64_t)r * u.ldu + u.c0 + l] = acc[q][e];
+            const double v = kp.sigma2 * acc[q][e];
+            if (u.trans) u.U[(int64_t)(u.c0 + l) * u.ldu + r] = v;
+            else u.U[(int64_t)r * u.ldu + u.c0 + l] = v;
           }
         }
       }
@@ -251,36 +314,44 @@ __global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4) k_tile_contract(const T
   }
 }
 
-template <int RQ, int FAM>
-void launch_class(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, const TileUnit* units, int n, int* counter) {
+struct AugArgs {
+  const double* Pa;
+  const double* Pb;
+  int dpa, sdp;
+};
+
+template <int RQ, int FAM, int NV = 0>
+void launch_class(Ctx& c, const AugArgs& ag, const KernelParams& kp, const TileUnit* units, int n, int* counter) {
   constexpr int BN = TileCfg<RQ>::BN;
-  const int dp = tree->d_pad;
-  size_t smem = sizeof(double) * (size_t)(32 * dp + 32 + 2 * stage_doubles(RQ, BN, dp));
-  auto fn = k_tile_contract<RQ, FAM>;
+  size_t smem = sizeof(double) * (size_t)(32 * ag.sdp + 2 * stage_doubles(RQ, BN, ag.sdp));
+  auto fn = k_tile_contract<RQ, FAM, NV>;
   CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
   CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 128, smem));
   occ = std::max(occ, 1);
   int grid = std::min<int64_t>(n, (int64_t)num_sms(c.device) * occ);
-  fn<<<grid, 128, smem, c.stream>>>(units, n, counter, tree->Xt.p, tree->norm2.p, dp, kp);
+  fn<<<grid, 128, smem, c.stream>>>(units, n, counter, ag.Pa, ag.Pb, ag.dpa, ag.sdp, kp);
   check_launch("k_tile_contract");
 }
 
 template <int FAM>
-void launch_fam(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, int rq, const TileUnit* units, int n,
+void launch_fam(Ctx& c, const AugArgs& ag, const KernelParams& kp, int rq, const TileUnit* units, int n,
                 int* counter) {
   switch (rq) {
-    case 1: launch_class<1, FAM>(c, tree, kp, units, n, counter); break;
-    case 2: launch_class<2, FAM>(c, tree, kp, units, n, counter); break;
-    case 3: launch_class<3, FAM>(c, tree, kp, units, n, counter); break;
-    case 4: launch_class<4, FAM>(c, tree, kp, units, n, counter); break;
-    case 6: launch_class<6, FAM>(c, tree, kp, units, n, counter); break;
-    case 7: launch_class<7, FAM>(c, tree, kp, units, n, counter); break;
-    case 9: launch_class<9, FAM>(c, tree, kp, units, n, counter); break;
-    case 12: launch_class<12, FAM>(c, tree, kp, units, n, counter); break;
-    case 16: launch_class<16, FAM>(c, tree, kp, units, n, counter); break;
-    case 20: launch_class<20, FAM>(c, tree, kp, units, n, counter); break;
-    case 24: launch_class<24, FAM>(c, tree, kp, units, n, counter); break;
+    case -1: launch_class<1, FAM, 1>(c, ag, kp, units, n, counter); break;
+    case -2: launch_class<1, FAM, 2>(c, ag, kp, units, n, counter); break;
+    case -4: launch_class<1, FAM, 4>(c, ag, kp, units, n, counter); break;
+    case 1: launch_class<1, FAM>(c, ag, kp, units, n, counter); break;
+    case 2: launch_class<2, FAM>(c, ag, kp, units, n, counter); break;
+    case 3: launch_class<3, FAM>(c, ag, kp, units, n, counter); break;
+    case 4: launch_class<4, FAM>(c, ag, kp, units, n, counter); break;
+    case 6: launch_class<6, FAM>(c, ag, kp, units, n, counter); break;
+    case 7: launch_class<7, FAM>(c, ag, kp, units, n, counter); break;
+    case 9: launch_class<9, FAM>(c, ag, kp, units, n, counter); break;
+    case 12: launch_class<12, FAM>(c, ag, kp, units, n, counter); break;
+    case 16: launch_class<16, FAM>(c, ag, kp, units, n, counter); break;
+    case 20: launch_class<20, FAM>(c, ag, kp, units, n, counter); break;
+    case 24: launch_class<24, FAM>(c, ag, kp, units, n, counter); break;
     default: throw Error(MLK_ERR_INVALID_ARG, "bad rq class");
   }
 }
@@ -303,15 +374,27 @@ void run_tile_contract(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, s
   starts.push_back((int)units.size());
   DevBuf<int> counters(starts.size(), c.stream);
   counters.zero();
+  // augmented, pre-scaled coordinates (k_tile_aug); the smem row stride avoids 2-way bank
+  // conflicts of the fragment loads when dpa/4 is even
+  AugArgs ag;
+  ag.dpa = pad4(tree->d + 2);
+  ag.sdp = ((ag.dpa >> 2) & 1) ? ag.dpa : ag.dpa + 4;
+  DevBuf<double> aug((size_t)2 * tree->n * ag.dpa, c.stream);
+  ag.Pa = aug.p;
+  ag.Pb = aug.p + (size_t)tree->n * ag.dpa;
   TimedLaunch tl(c, name);
+  k_tile_aug<<<(unsigned)ceil_div(tree->n, 256), 256, 0, c.stream>>>(tree->Xt.p, tree->d_pad, tree->d, tree->n,
+                                                                     kp.scale, aug.p, aug.p + (size_t)tree->n * ag.dpa,
+                                                                     ag.dpa);
+  check_launch("k_tile_aug");
   for (size_t g = 0; g + 1 < starts.size(); g++) {
     int s0 = starts[g], n = starts[g + 1] - starts[g];
     int rq = units[s0].rq;
     switch (kp.family) {
-      case MLK_MATERN_12: launch_fam<MLK_MATERN_12>(c, tree, kp, rq, du.p + s0, n, counters.p + g); break;
-      case MLK_MATERN_32: launch_fam<MLK_MATERN_32>(c, tree, kp, rq, du.p + s0, n, counters.p + g); break;
-      case MLK_MATERN_52: launch_fam<MLK_MATERN_52>(c, tree, kp, rq, du.p + s0, n, counters.p + g); break;
-      default: launch_fam<MLK_GAUSSIAN>(c, tree, kp, rq, du.p + s0, n, counters.p + g); break;
+      case MLK_MATERN_12: launch_fam<MLK_MATERN_12>(c, ag, kp, rq, du.p + s0, n, counters.p + g); break;
+      case MLK_MATERN_32: launch_fam<MLK_MATERN_32>(c, ag, kp, rq, du.p + s0, n, counters.p + g); break;
+      case MLK_MATERN_52: launch_fam<MLK_MATERN_52>(c, ag, kp, rq, du.p + s0, n, counters.p + g); break;
+      default: launch_fam<MLK_GAUSSIAN>(c, ag, kp, rq, du.p + s0, n, counters.p + g); break;
     }
   }
 }

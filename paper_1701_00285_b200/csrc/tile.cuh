@@ -17,7 +17,7 @@ struct TileUnit {
   int32_t c0, qc;            // first column of W_b rows handled, and how many (<= 8 RQ)
   int32_t p_b;               // rows of W_b
   int32_t trans;             // 0: U[r * ldu + c0 + l]; 1: U[(c0 + l) * ldu + r]
-  int32_t rq;                // instantiation class (columns padded to 8 rq)
+  int32_t rq;                // instantiation class (columns padded to 8 rq); -NV: DFMA contraction of NV <= 4 columns
   const double* Wb;          // W_b[l][y] at Wb + l * ldw + y
   int64_t ldw;
   double* U;                 // base of this pair's U
@@ -27,9 +27,11 @@ struct TileUnit {
 
 struct KernelParams {
   int32_t family;
-  double c1;      // sqrt(2 nu) / rho (Matern) or 1 / rho^2 (Gaussian)
+  double c1;        // sqrt(2 nu) / rho (Matern) or 1 / rho^2 (Gaussian)
   double sigma2;
   double nugget;
+  double same_val;  // 1 + nugget / sigma2: the correlation of a site with itself (R18)
+  double scale;     // coordinate pre-scale of the augmented Gram product (c1, or 1 / rho)
 };
 
 KernelParams make_kernel_params(const mlk_kernel& k);
