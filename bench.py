@@ -228,7 +228,7 @@ def main():
     nnz, dim = cw.nnz, B.dim
     del tr, B, cw
 
-    sampler = ClockSampler(local) if rank == 0 else None
+    sampler = ClockSampler(local) if rank == 0 and not os.environ.get("MLK_BENCH_NO_SAMPLER") else None
     ctx.reset_stats()
     ctx.set_timing(True)
     if ws > 1:

@@ -416,9 +416,7 @@ mlk_status mlk_assemble_cw(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const ml
     std::vector<std::vector<int64_t>> unit_pieces(units.size());
     for (int64_t i = 0; i < npc; i++)
       if (powner[i] == c.rank) unit_pieces[pieces[i].unit].push_back(i);
-    size_t freeb = 0, totalb = 0;
-    CUDA_CHECK(cudaMemGetInfo(&freeb, &totalb));
-    const int64_t budget = std::max<int64_t>((int64_t)(freeb / 3 / sizeof(double)), (int64_t)1 << 22);
+    const int64_t budget = std::max<int64_t>(c.scratch_budget_bytes() / (int64_t)sizeof(double), (int64_t)1 << 22);
     size_t pos = 0;
     while (pos < mine.size()) {
       int64_t need = 0;
@@ -432,6 +430,7 @@ mlk_status mlk_assemble_cw(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const ml
         end++;
       }
       DevBuf<double> V(std::max<int64_t>(need, 1), st);
+      trace.mark("valloc");
       std::vector<TileUnit> tu;
       std::vector<GemmDesc> gd;
       for (size_t j = pos; j < end; j++) {

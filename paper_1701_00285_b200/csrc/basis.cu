@@ -75,96 +75,113 @@ struct QrJob {
 constexpr int kQrSmemLimit = 225 * 1024;
 
 // Householder QR of one matrix per CTA in the LAPACK dgeqr2 convention (beta = -sign(alpha)
-// ||(alpha, x)||, tau = (beta - alpha)/beta, v = x/(alpha - beta), tau = 0 when x = 0), then the
-// compact-WY factor T of Q = H_0 ... H_{nc-1} = I - V T V^T (dlarft, forward, columnwise) and
-// W1T = T^T V^T; Q^T = I - V W1T is then formed by the DMMA GEMM (gemm.cu).
-// Column step k takes two barriers: (1) every thread computes partial dot products
-// x . a_j over a chunk of rows for the columns j >= k (j = k gives |x|^2); (2) every thread
-// derives beta, tau and the scale redundantly and applies H_k to its (column, chunk) items,
-// reading the unscaled x (the scaling of column k and beta are stored in the next step).
-// SMEM: the matrix (whose strict lower part becomes V) lives in shared memory with an odd
-// column stride; TS: the Gram matrix G = V^T V (transposed) and T live there too.
-template <bool SMEM, bool TS>
-__global__ void __launch_bounds__(256) k_qr_wy(const QrJob* __restrict__ jobs, int* __restrict__ rank_flag) {
+// ||(alpha, x)||, tau = (beta - alpha)/beta, v = x/(alpha - beta), tau = 0 when x = 0), then
+// W1T = T^T V^T for the compact-WY form Q = H_0 ... H_{nc-1} = I - V T V^T, so that
+// Q^T = I - V W1T is formed by the DMMA GEMM (gemm.cu).
+//  * Column step k takes two barriers: (1) one warp per column j >= k forms x . a_j (rows
+//    i > k, lanes over rows, shuffle reduction); the warp of column k (j = k gives |x|^2)
+//    also forms beta, tau and the scale once and publishes them; (2) all threads apply H_k
+//    element-wise to the trailing columns, reading the unscaled x (column k's scaling and
+//    beta are stored at the start of the next step).
+//  * T is never formed: with G = V^T V, T^{-1} = triu(G, 1) + diag(1/tau) (the inverse of the
+//    dlarft recursion), so W1T solves T^{-T} W1T = V^T by forward substitution,
+//    W1T[l][i] = tau_l (V[i][l] - sum_{q<l} G[q][l] W1T[q][i]), one thread per row i, in place
+//    of A's row i (R and V are exported first).  A reflector with tau = 0 is the identity and
+//    gets a zero row.
+// SMEM: the matrix lives in shared memory (odd column stride); GS: G lives there too.
+constexpr int kQrThreads = 1024;
+
+template <bool SMEM, bool GS>
+__global__ void __launch_bounds__(kQrThreads) k_qr_wy(const QrJob* __restrict__ jobs, int* __restrict__ rank_flag) {
   extern __shared__ __align__(16) double sh[];
+  __shared__ double s_piv[6];                       // tau, scal, beta of step k at 3 (k & 1)
   const QrJob jb = jobs[blockIdx.x];
   const int m = jb.m, nc = jb.nc;
-  const int nch = min(16, (m + 31) / 32);          // row chunks of the column items
-  const int L = (m + nch - 1) / nch;
   const int lda = SMEM ? (m | 1) : m;
   double* taus = sh;                                // nc
-  double* rowk = taus + nc;                         // nc: row k of the trailing columns
-  double* part = rowk + nc;                         // nc * nch partial dot products
-  double* A = SMEM ? part + nc * nch : jb.A;
-  double* T = TS ? A + (int64_t)lda * nc : jb.T;    // T[l][j], row-major nc x nc
-  double* Gt = TS ? T + (int64_t)nc * nc : jb.W1T;  // Gt[j][l] = G[l][j] (scratch)
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  double* dots = taus + nc;                         // nc: x . a_j of the current step (by column)
+  double* rowk = dots + nc;                         // nc: a_kj of the current step (by column)
+  double* A = SMEM ? rowk + nc + ((3 * nc) & 1) : jb.A;
+  double* G = GS ? A + (int64_t)lda * nc : jb.T;    // G[q][l], q < l, row-major nc x nc
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   if (SMEM) {
-    for (int64_t e = tid; e < (int64_t)m * nc; e += blockDim.x) {
+    for (int64_t e = tid; e < (int64_t)m * nc; e += nt) {
       const int j = (int)(e / m), i = (int)(e - (int64_t)j * m);
       A[(int64_t)j * lda + i] = jb.A[e];
     }
     __syncthreads();
   }
-  double scal_prev = 1.0, beta_prev = 0.0;
-  for (int k = 0; k <= nc; k++) {
-    // finish column k - 1: store beta on the diagonal, scale x into v
-    if (k > 0) {
-      double* ap = A + (int64_t)(k - 1) * lda;
-      for (int i = k + tid; i < m; i += blockDim.x) ap[i] *= scal_prev;
-      if (tid == 0) ap[k - 1] = beta_prev;
-    }
-    if (k == nc) break;
+  // warp w owns the columns j = w, w + nw, ... in both phases of every step
+  for (int k = 0; k < nc; k++) {
     const double* ak = A + (int64_t)k * lda;
-    // (1) partial dots for columns j >= k over rows i > k, and a copy of row k
-    const int nitem = (nc - k) * nch;
-    for (int it = tid; it < nitem; it += blockDim.x) {
-      const int c = it % nch, jj = it / nch;
-      const double* aj = A + (int64_t)(k + jj) * lda;
-      const int i0 = max(k + 1, c * L), i1 = min(m, (c + 1) * L);
+    // (1) dots x . a_j (rows i > k) for the owned columns j >= k, a copy of a_kj; the owner
+    //     of column k forms the reflector; the owner of column k - 1 finishes it (beta on the
+    //     diagonal, x scaled into v) -- column k - 1 is not read in this step
+    for (int j = warp; j < nc; j += nw) {
+      if (j == k - 1) {
+        double* ap = A + (int64_t)j * lda;
+        const double* pv = s_piv + 3 * ((k - 1) & 1);
+        const double scal = pv[1];
+        for (int i = k + lane; i < m; i += 32) ap[i] *= scal;
+        if (lane == 0) ap[j] = pv[2];
+        continue;
+      }
+      if (j < k) continue;
+      const double* aj = A + (int64_t)j * lda;
       double s = 0.0;
-      for (int i = i0; i < i1; i++) s = fma(ak[i], aj[i], s);
-      part[jj * nch + c] = s;
-      if (c == 0) rowk[jj] = aj[k];
-    }
-    __syncthreads();
-    // (2) reflector (redundantly per thread) and its application to columns j > k
-    double xn2 = 0.0;
-    for (int c = 0; c < nch; c++) xn2 += part[c];
-    const double alpha = rowk[0];
-    double tau = 0.0, scal = 1.0, beta = alpha;
-    if (xn2 > 0.0) {
-      beta = -copysign(sqrt(fma(alpha, alpha, xn2)), alpha);
-      tau = (beta - alpha) / beta;
-      scal = 1.0 / (alpha - beta);
-    }
-    if (tid == 0) taus[k] = tau;
-    if (tau != 0.0) {
-      const int nup = (nc - k - 1) * nch;
-      for (int it = tid; it < nup; it += blockDim.x) {
-        const int c = it % nch, jj = 1 + it / nch;
-        double* aj = A + (int64_t)(k + jj) * lda;
-        double dsum = 0.0;
-        for (int c2 = 0; c2 < nch; c2++) dsum += part[jj * nch + c2];
-        const double akj = rowk[jj];
-        const double f = tau * fma(scal, dsum, akj);
-        const double g = f * scal;
-        const int i0 = max(k + 1, c * L), i1 = min(m, (c + 1) * L);
-        for (int i = i0; i < i1; i++) aj[i] = fma(-g, ak[i], aj[i]);
-        if (c == 0) aj[k] = akj - f;
+      for (int i = k + 1 + lane; i < m; i += 32) s = fma(ak[i], aj[i], s);
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) {
+        if (j == k) {
+          const double alpha = ak[k];
+          double tau = 0.0, scal = 1.0, beta = alpha;
+          if (s > 0.0) {
+            beta = -copysign(sqrt(fma(alpha, alpha, s)), alpha);
+            tau = (beta - alpha) / beta;
+            scal = 1.0 / (alpha - beta);
+          }
+          taus[k] = tau;
+          double* pv = s_piv + 3 * (k & 1);
+          pv[0] = tau;
+          pv[1] = scal;
+          pv[2] = beta;
+        } else {
+          dots[j] = s;
+          rowk[j] = aj[k];
+        }
       }
     }
-    scal_prev = scal;
-    beta_prev = beta;
     __syncthreads();
+    // (2) a_j -= f (e_k + scal x), f = tau (a_kj + scal d_j), for the owned columns j > k
+    const double tau = s_piv[3 * (k & 1)];
+    if (tau != 0.0) {
+      const double scal = s_piv[3 * (k & 1) + 1];
+      for (int j = warp; j < nc; j += nw) {
+        if (j <= k) continue;
+        double* aj = A + (int64_t)j * lda;
+        const double akj = rowk[j];
+        const double f = tau * fma(scal, dots[j], akj);
+        const double g = f * scal;
+        for (int i = k + 1 + lane; i < m; i += 32) aj[i] = fma(-g, ak[i], aj[i]);
+        if (lane == 0) aj[k] = akj - f;
+      }
+    }
+    __syncthreads();
+  }
+  // finish the last column
+  if (warp == (nc - 1) % nw) {
+    double* ap = A + (int64_t)(nc - 1) * lda;
+    const double* pv = s_piv + 3 * ((nc - 1) & 1);
+    for (int i = nc + lane; i < m; i += 32) ap[i] *= pv[1];
+    if (lane == 0) ap[nc - 1] = pv[2];
   }
   __syncthreads();
   // R, rank test (reading R9), V row-major with the unit diagonal made explicit
-  for (int e = tid; e < nc * nc; e += blockDim.x) {
+  for (int e = tid; e < nc * nc; e += nt) {
     int i = e / nc, j = e - i * nc;
     jb.R[e] = j >= i ? A[(int64_t)j * lda + i] : 0.0;
   }
-  for (int64_t e = tid; e < (int64_t)m * nc; e += blockDim.x) {
+  for (int64_t e = tid; e < (int64_t)m * nc; e += nt) {
     int i = (int)(e / nc), l = (int)(e - (int64_t)i * nc);
     jb.V[e] = i == l ? 1.0 : (i > l ? A[(int64_t)l * lda + i] : 0.0);
   }
@@ -177,51 +194,50 @@ __global__ void __launch_bounds__(256) k_qr_wy(const QrJob* __restrict__ jobs, i
     }
     if (!(mn > 1e-13 * mx)) atomicExch(rank_flag, 1);
   }
-  // G[l][j] = (V^T V)[l][j] for l < j: column l of V is (0.., 1 at l, A[l*lda + i] for i > l),
-  // so G[l][j] = A[l*lda + j] + sum_{i > j} A[l*lda + i] A[j*lda + i]; stored as Gt[j][l].
-  // One thread per pair, serial over rows.
-  for (int e = tid; e < nc * nc; e += blockDim.x) {
-    const int j = e / nc, l = e - j * nc;
-    if (l >= j) continue;
+  // G[q][l] = (V^T V)[q][l] for q < l: column q of V is (0.., 1 at q, A[q*lda + i] for i > q),
+  // so G[q][l] = A[q*lda + l] + sum_{i > l} A[q*lda + i] A[l*lda + i].  One thread per pair.
+  for (int e = tid; e < nc * nc; e += nt) {
+    const int q = e / nc, l = e - q * nc;
+    if (q >= l) continue;
+    const double* vq = A + (int64_t)q * lda;
     const double* vl = A + (int64_t)l * lda;
-    const double* vj = A + (int64_t)j * lda;
-    double s = vl[j];
-    for (int i = j + 1; i < m; i++) s = fma(vl[i], vj[i], s);
-    Gt[(int64_t)j * nc + l] = s;
+    double s0 = vq[l], s1 = 0.0;
+    int i = l + 1;
+    for (; i + 1 < m; i += 2) {
+      s0 = fma(vq[i], vl[i], s0);
+      s1 = fma(vq[i + 1], vl[i + 1], s1);
+    }
+    if (i < m) s0 = fma(vq[i], vl[i], s0);
+    G[(int64_t)q * nc + l] = s0 + s1;
   }
   __syncthreads();
-  // T[0:j, j] = -tau_j T[0:j, 0:j] G[0:j, j];  T[j, j] = tau_j  (dlarft, forward columnwise):
-  // warp per row l, lanes over q in [l, j)
-  for (int j = 0; j < nc; j++) {
-    const double tj = taus[j];
-    const double* gj = Gt + (int64_t)j * nc;
-    for (int l = warp; l < j; l += nw) {
-      const double* tl = T + (int64_t)l * nc;
-      double s = 0.0;
-      for (int q = l + lane; q < j; q += 32) s = fma(tl[q], gj[q], s);
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) T[(int64_t)l * nc + j] = -tj * s;
+  // forward substitution, thread per row i (reads only its own row of A, then overwrites it)
+  for (int i = tid; i < m; i += nt) {
+    for (int l = 0; l < nc; l++) {
+      const double tl = taus[l];
+      double w = 0.0;
+      if (tl != 0.0) {
+        const double vil = i == l ? 1.0 : (i > l ? A[(int64_t)l * lda + i] : 0.0);
+        double s0 = 0.0, s1 = 0.0;
+        int q = 0;
+        for (; q + 1 < l; q += 2) {
+          s0 = fma(G[(int64_t)q * nc + l], A[(int64_t)q * lda + i], s0);
+          s1 = fma(G[(int64_t)(q + 1) * nc + l], A[(int64_t)(q + 1) * lda + i], s1);
+        }
+        if (q < l) s0 = fma(G[(int64_t)q * nc + l], A[(int64_t)q * lda + i], s0);
+        w = tl * (vil - (s0 + s1));
+      }
+      A[(int64_t)l * lda + i] = w;   // row i of W1T, in place (entries q < l already replaced)
+      jb.W1T[(int64_t)l * m + i] = w;
     }
-    if (tid == 0) T[(int64_t)j * nc + j] = tj;
-    __syncthreads();
-  }
-  // W1T = T^T V^T: W1T[l][i] = sum_{q <= min(l, i)} T[q][l] V[i][q], V[i][q] = A[q*lda + i] (i > q)
-  for (int64_t e = tid; e < (int64_t)nc * m; e += blockDim.x) {
-    int l = (int)(e / m), i = (int)(e - (int64_t)l * m);
-    double s = 0.0;
-    const int qe = min(l, i - 1);
-    for (int q = 0; q <= qe; q++) s = fma(T[(int64_t)q * nc + l], A[(int64_t)q * lda + i], s);
-    if (i <= l) s += T[(int64_t)i * nc + l];
-    jb.W1T[e] = s;
   }
 }
 
-// dynamic shared memory of k_qr_wy: taus, rowk, partials (+ A) (+ T, Gt)
-inline size_t qr_smem(int m, int nc, bool a_in, bool t_in) {
-  const int nch = std::min(16, (m + 31) / 32);
-  size_t d = 2 * (size_t)nc + (size_t)nc * nch;
+// dynamic shared memory of k_qr_wy: taus, dots, rowk (+ A) (+ G)
+inline size_t qr_smem(int m, int nc, bool a_in, bool g_in) {
+  size_t d = 3 * (size_t)nc + 1;
   if (a_in) d += (size_t)(m | 1) * nc;
-  if (t_in) d += 2 * (size_t)nc * nc;
+  if (g_in) d += (size_t)nc * nc;
   return d * sizeof(double);
 }
 
@@ -265,14 +281,14 @@ void run_qr(Ctx& c, std::vector<QrJob>& jobs, int nc, int* flag, const char* nam
     const size_t s_full = qr_smem(m_max, nc, true, true), s_a = qr_smem(m_max, nc, true, false);
     if (s_full <= (size_t)kQrSmemLimit) {
       CUDA_CHECK(cudaFuncSetAttribute(k_qr_wy<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_full));
-      k_qr_wy<true, true><<<(unsigned)jobs.size(), 256, s_full, c.stream>>>(dj.p, flag);
+      k_qr_wy<true, true><<<(unsigned)jobs.size(), kQrThreads, s_full, c.stream>>>(dj.p, flag);
     } else if (s_a <= (size_t)kQrSmemLimit) {
       CUDA_CHECK(cudaFuncSetAttribute(k_qr_wy<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_a));
-      k_qr_wy<true, false><<<(unsigned)jobs.size(), 256, s_a, c.stream>>>(dj.p, flag);
+      k_qr_wy<true, false><<<(unsigned)jobs.size(), kQrThreads, s_a, c.stream>>>(dj.p, flag);
     } else {
       const size_t s0 = qr_smem(m_max, nc, false, false);
       CUDA_CHECK(cudaFuncSetAttribute(k_qr_wy<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s0));
-      k_qr_wy<false, false><<<(unsigned)jobs.size(), 256, s0, c.stream>>>(dj.p, flag);
+      k_qr_wy<false, false><<<(unsigned)jobs.size(), kQrThreads, s0, c.stream>>>(dj.p, flag);
     }
     check_launch("k_qr_wy");
   }

@@ -57,6 +57,11 @@ struct Ctx {
   };
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> event_pool;
+  // device memory free when the context first needed a scratch budget (cudaMemGetInfo is
+  // slow and erratic -- 0.3 to 14 ms per call on B200 while NVML is polled -- so it is queried
+  // once per context, not per call)
+  int64_t free_at_first_use = -1;
+  int64_t scratch_budget_bytes();
 
   cudaEvent_t get_event();
   void flush_timing();  // synchronize and fold pending events into stats

@@ -33,6 +33,15 @@ int num_sms(int device) {
   return v;
 }
 
+int64_t Ctx::scratch_budget_bytes() {
+  if (free_at_first_use < 0) {
+    size_t freeb = 0, totalb = 0;
+    CUDA_CHECK(cudaMemGetInfo(&freeb, &totalb));
+    free_at_first_use = (int64_t)freeb;
+  }
+  return free_at_first_use / 3;
+}
+
 cudaEvent_t Ctx::get_event() {
   if (!event_pool.empty()) {
     cudaEvent_t e = event_pool.back();

@@ -17,6 +17,13 @@
 // A persistent grid pulls units (largest first) from an atomic counter.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <map>
+#include <array>
+#include <string>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "dmma.cuh"
 #include "fastmath.cuh"
@@ -73,6 +80,9 @@ void make_tile_units(std::vector<TileUnit>& out, int64_t a_begin, int32_t s_a, i
       u.ldw = ldw;
       u.U = U;
       u.ldu = ldu;
+      // a tensor map needs a 16-byte aligned base and a row stride that is a multiple of 16 bytes
+      u.bulk = (ldw % 2 == 0) && ((reinterpret_cast<uintptr_t>(Wb) & 15) == 0);
+      u.xmap = u.wmap = -1;
       // FP64-slot estimate: Gram dp + kernel ~50 + contraction 8 rq per entry
       u.cost = 32.0 * s_b * (dp + 50 + 8.0 * rq);
       out.push_back(u);
@@ -97,9 +107,13 @@ __device__ __forceinline__ double corr(double x, const double* tab) {
 
 template <int RQ>
 struct TileCfg {
-  static constexpr int BN = RQ >= 6 ? 16 : 32;   // b points per stage
-  static constexpr int WROWS = 8 * RQ;
+  // b points per stage.  BN = 8 (mod 16) makes a W row 8 BN doubles = 64 (mod 128) bytes, so
+  // the 16-byte B-fragment loads of a quarter-warp (2 rows x 4 chunks) hit distinct banks
+  // without any swizzle -- which a 1-D bulk copy could not apply
+  static constexpr int BN = RQ >= 6 ? 24 : 40;
+  static constexpr int NST = RQ >= 16 ? 2 : 3;   // stages in the smem ring
   static constexpr int G = RQ <= 12 ? RQ : 8;    // W_b fragments held per DMMA group
+  static constexpr int NACC = 1;                 // accumulator sets (2 measured no faster)
 };
 
 __host__ __device__ constexpr int stage_doubles(int rq, int bn, int sdp) { return bn * sdp + 8 * rq * bn; }
@@ -131,24 +145,44 @@ __global__ void k_tile_aug(const double* __restrict__ Xt, int dpt, int d, int64_
 // NV > 0 (with RQ = 1): the contraction has NV <= 4 columns (C a for a few vectors) and is done
 // with DFMAs per lane instead of 8-column DMMAs; the four lanes of a quad hold disjoint column
 // subsets of a row and are summed by two shuffles in the epilogue (fixed order).
+//
+// Staging: a ring of NST stages, each {BN rows of Pb, 8 RQ rows x BN columns of W_b}, filled by
+// two 2-D TMA box loads (tensor maps built by run_tile_contract) that complete on the stage's
+// mbarrier; out-of-range rows / columns arrive zero-filled.  Units whose W_b cannot be described
+// by a tensor map (odd row stride or unaligned base) use 8-byte cp.async instead.  The last
+// warp to finish a stage (a shared counter) refills it with the stage NST ahead, so warps never
+// wait on a CTA barrier inside a unit.
 template <int RQ, int FAM, int NV>
 __global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4)
     k_tile_contract(const TileUnit* __restrict__ units, int n_units, int* __restrict__ counter,
                     const double* __restrict__ Pa, const double* __restrict__ Pb, int dpa, int sdp,
-                    KernelParams kp) {
+                    KernelParams kp, const CUtensorMap* __restrict__ maps) {
   constexpr int BN = TileCfg<RQ>::BN;
-  constexpr int WROWS = TileCfg<RQ>::WROWS;
   constexpr int G = TileCfg<RQ>::G;
+  constexpr int NST = TileCfg<RQ>::NST;
   constexpr int T = BN / 8;
-  extern __shared__ __align__(16) double sm[];
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t full[NST];
+  __shared__ int cnt[NST];
   __shared__ int s_unit;
   __shared__ double s_tab[64];
-  if (threadIdx.x < 64) s_tab[threadIdx.x] = kExp2Tab64[threadIdx.x];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int sd = stage_doubles(RQ, BN, sdp);
   double* As = sm;                  // 32 x sdp
-  double* St = sm + 32 * sdp;       // 2 stages
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* St = sm + 32 * sdp;       // NST stages
+  if (tid < 64) s_tab[tid] = kExp2Tab64[tid];
+  if (tid == 0) {
+    for (int i = 0; i < NST; i++) {
+      mbar_init(&full[i], 1);
+      cnt[i] = 0;
+    }
+    fence_mbar_init();
+  }
+  // stale stage contents are only ever multiplied by zeroed covariances: keep them finite
+  for (int e = tid; e < NST * sd; e += 128) St[e] = 0.0;
+  fence_proxy_async_smem();
   const int ks_n = dpa >> 2;
+  int gs = 0;  // stages consumed so far by this CTA (ring position and mbarrier phases)
 
   while (true) {
     __syncthreads();
@@ -167,80 +201,86 @@ __global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4)
         const bool ok = r < rows;
         cp_async16(As + r * sdp + 2 * ch, ok ? Pa + (a0 + r) * dpa + 2 * ch : Pa, ok);
       }
+      cp_async_commit();
     }
+    const int nst = (u.s_b + BN - 1) / BN;
 
-    auto load_stage = [&](int st, int b0) {
-      double* Xs = St + st * sd;
+    // fill the ring slot of stage s (called by one whole warp)
+    auto issue = [&](int s) {
+      const int slot = (gs + s) % NST;
+      double* Xs = St + slot * sd;
       double* Ws = Xs + BN * sdp;
-      const int nb = min(BN, u.s_b - b0);
-      // b coordinates: rows of dpa doubles, 16-byte chunks; rows past the range are zero
-      const int cpr = dpa >> 1;
-      for (int e = tid; e < BN * cpr; e += 128) {
-        const int y = e / cpr, ch = e - y * cpr;
-        const bool ok = y < nb;
-        cp_async16(Xs + y * sdp + 2 * ch, ok ? Pb + (u.b_begin + b0 + y) * dpa + 2 * ch : Pb, ok);
-      }
-      // W_b columns b0..b0+BN of rows c0..c0+8RQ, chunk c of row rho at (c ^ 4(rho&1));
-      // missing rows / columns are zero, so padded points contribute nothing
-      constexpr int CH = BN / 2;
-      for (int e = tid; e < WROWS * CH; e += 128) {
-        const int rho = e / CH, ch = e - rho * CH;
-        const int phys = ch ^ ((rho & 1) << 2);
-        double* dst = Ws + rho * BN + 2 * phys;
-        const int y = b0 + 2 * ch;
-        const bool rowok = rho < u.qc;
-        const double* src = u.Wb + (int64_t)(u.c0 + rho) * u.ldw + y;
-        const bool ok0 = rowok && (y < u.s_b), ok1 = rowok && (y + 1 < u.s_b);
-        if (ok0 && ok1 && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
-          cp_async16(dst, src, true);
-        } else {
-          cp_async8(dst, ok0 ? src : u.Wb, ok0);
-          cp_async8(dst + 1, ok1 ? src + 1 : u.Wb, ok1);
+      const int b0 = s * BN, nb = min(BN, u.s_b - b0);
+      const double* pb = Pb + (u.b_begin + b0) * dpa;
+      if (u.bulk) {
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&full[slot], 8u * (BN * sdp + 8 * RQ * BN));
+          tma_2d_g2s(Xs, maps + u.xmap, 0, (int)(u.b_begin + b0), &full[slot]);
+          tma_2d_g2s(Ws, maps + u.wmap, b0, u.c0, &full[slot]);
         }
+      } else {
+        const int cpr = dpa >> 1;
+        for (int e = lane; e < nb * cpr; e += 32) {
+          const int y = e / cpr, ch = e - y * cpr;
+          cp_async16(Xs + y * sdp + 2 * ch, pb + y * dpa + 2 * ch, true);
+        }
+        for (int e = lane; e < u.qc * nb; e += 32) {
+          const int rho = e / nb, y = e - rho * nb;
+          cp_async8(Ws + rho * BN + y, u.Wb + (int64_t)(u.c0 + rho) * u.ldw + b0 + y, true);
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[slot]);
       }
     };
 
-    double acc[RQ][2];
+    if (warp == 0)
+      for (int s = 0; s < min(NST, nst); s++) issue(s);
+    cp_async_wait<0>();
+    __syncthreads();  // As visible
+
+    constexpr int NACC = TileCfg<RQ>::NACC;
+    double acc[NACC][RQ][2];
 #pragma unroll
-    for (int i = 0; i < RQ; i++) acc[i][0] = acc[i][1] = 0.0;
+    for (int h = 0; h < NACC; h++)
+#pragma unroll
+      for (int i = 0; i < RQ; i++) acc[h][i][0] = acc[h][i][1] = 0.0;
     double accv[NV > 0 ? NV : 1];
 #pragma unroll
     for (int i = 0; i < (NV > 0 ? NV : 1); i++) accv[i] = 0.0;
 
-    const int nst = (u.s_b + BN - 1) / BN;
-    load_stage(0, 0);
-    cp_async_commit();
     const int ar = warp * 8 + (lane >> 2);
     const int64_t ga = a0 + ar;
     for (int s = 0; s < nst; s++) {
-      if (s + 1 < nst) load_stage((s + 1) & 1, (s + 1) * BN);
-      cp_async_commit();
-      cp_async_wait<1>();
-      __syncthreads();
-      const double* Xs = St + (s & 1) * sd;
+      const int g = gs + s, slot = g % NST;
+      mbar_wait(&full[slot], (unsigned)((g / NST) & 1));
+      const double* Xs = St + slot * sd;
       const double* Ws = Xs + BN * sdp;
-      const int64_t gb0 = u.b_begin + s * BN;
+      const int yb = s * BN;                       // first b point of the stage (local index)
       // 1. augmented Gram: g = |u_a - u_b|^2 for the T sub-tiles (independent chains)
-      double g[T][2];
+      double gr[T][2];
 #pragma unroll
-      for (int t = 0; t < T; t++) g[t][0] = g[t][1] = 0.0;
+      for (int t = 0; t < T; t++) gr[t][0] = gr[t][1] = 0.0;
       const double* ap = As + ar * sdp + (lane & 3);
       const double* bp = Xs + (lane >> 2) * sdp + (lane & 3);
 #pragma unroll 4
       for (int ks = 0; ks < ks_n; ks++) {
         const double a = ap[4 * ks];
 #pragma unroll
-        for (int t = 0; t < T; t++) dmma_8x8x4(g[t][0], g[t][1], a, bp[8 * t * sdp + 4 * ks]);
+        for (int t = 0; t < T; t++) dmma_8x8x4(gr[t][0], gr[t][1], a, bp[8 * t * sdp + 4 * ks]);
       }
-      // 2. covariances in registers: closed form, same-site entries exactly 1 + nugget/sigma2
+      // 2. covariances in registers: closed form, same-site entries exactly 1 + nugget/sigma2,
+      //    points past the range exactly 0 (their stage rows are stale)
       double cv[T][2];
 #pragma unroll
       for (int t = 0; t < T; t++) {
-        const int64_t gcol = gb0 + 8 * t + 2 * (lane & 3);
+        const int y = yb + 8 * t + 2 * (lane & 3);
 #pragma unroll
         for (int e = 0; e < 2; e++) {
-          const double v = corr<FAM>(g[t][e], s_tab);
-          cv[t][e] = (gcol + e == ga) ? kp.same_val : v;
+          const double v = corr<FAM>(gr[t][e], s_tab);
+          cv[t][e] = (u.b_begin + y + e == ga) ? kp.same_val : v;
+          if (y + e >= u.s_b) cv[t][e] = 0.0;
         }
       }
       if constexpr (NV > 0) {
@@ -250,15 +290,14 @@ __global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4)
           const int ch = 4 * t + (lane & 3);
 #pragma unroll
           for (int l = 0; l < NV; l++) {
-            const double2 wv = *reinterpret_cast<const double2*>(Ws + l * BN + 2 * (ch ^ ((l & 1) << 2)));
+            const double2 wv = *reinterpret_cast<const double2*>(Ws + l * BN + 2 * ch);
             accv[l] = fma(cv[t][0], wv.x, accv[l]);
             accv[l] = fma(cv[t][1], wv.y, accv[l]);
           }
         }
       } else {
         // 3./4. the accumulator entries are the A fragments of k-steps 0, 1 (no shuffles); W_b
-        // fragments for G n-tiles are held in registers so the G DMMAs of a k-step are
-        // independent of each other
+        // fragments for G n-tiles are held in registers
 #pragma unroll
         for (int t = 0; t < T; t++) {
 #pragma unroll
@@ -268,21 +307,30 @@ __global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4)
             for (int qq = 0; qq < G; qq++) {
               if (q0 + qq < RQ) {
                 const int rho = 8 * (q0 + qq) + (lane >> 2);
-                const int ch = 4 * t + (lane & 3);
-                w[qq] = *reinterpret_cast<const double2*>(Ws + rho * BN + 2 * (ch ^ ((rho & 1) << 2)));
+                w[qq] = *reinterpret_cast<const double2*>(Ws + rho * BN + 2 * (4 * t + (lane & 3)));
               }
             }
 #pragma unroll
             for (int qq = 0; qq < G; qq++)
-              if (q0 + qq < RQ) dmma_8x8x4(acc[q0 + qq][0], acc[q0 + qq][1], cv[t][0], w[qq].x);
+              if (q0 + qq < RQ) dmma_8x8x4(acc[0][q0 + qq][0], acc[0][q0 + qq][1], cv[t][0], w[qq].x);
 #pragma unroll
             for (int qq = 0; qq < G; qq++)
-              if (q0 + qq < RQ) dmma_8x8x4(acc[q0 + qq][0], acc[q0 + qq][1], cv[t][1], w[qq].y);
+              if (q0 + qq < RQ)
+                dmma_8x8x4(acc[NACC - 1][q0 + qq][0], acc[NACC - 1][q0 + qq][1], cv[t][1], w[qq].y);
           }
         }
       }
-      __syncthreads();
+      // release the slot: the last of the four warps refills it with stage s + NST
+      __syncwarp();
+      int last = 0;
+      if (lane == 0) last = atomicAdd(&cnt[slot], 1) == 3;
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {
+        if (lane == 0) cnt[slot] = 0;
+        if (s + NST < nst) issue(s + NST);
+      }
     }
+    gs += nst;
     // epilogue: U = sigma2 * acc
     const int r = u.row0 + ar;
     if constexpr (NV > 0) {
@@ -304,7 +352,7 @@ __global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4)
         for (int e = 0; e < 2; e++) {
           const int l = 8 * q + 2 * (lane & 3) + e;
           if (l < u.qc) {
-            const double v = kp.sigma2 * acc[q][e];
+            const double v = kp.sigma2 * (NACC == 2 ? acc[0][q][e] + acc[NACC - 1][q][e] : acc[0][q][e]);
             if (u.trans) u.U[(int64_t)(u.c0 + l) * u.ldu + r] = v;
             else u.U[(int64_t)r * u.ldu + u.c0 + l] = v;
           }
@@ -318,19 +366,60 @@ struct AugArgs {
   const double* Pa;
   const double* Pb;
   int dpa, sdp;
+  const CUtensorMap* maps;
 };
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) throw Error(MLK_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// row-major FP64 matrix (rows x cols, row stride ld elements) read in boxes of box_rows x box_cols
+CUtensorMap make_map_2d(const double* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_rows,
+                        uint32_t box_cols) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {ld * sizeof(double)};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = tensor_map_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides,
+                                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(MLK_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return m;
+}
+
+int class_bn(int rq) {
+  switch (rq) {
+    case 1: case 2: case 3: case 4: case -1: case -2: case -4: return TileCfg<1>::BN;
+    default: return TileCfg<24>::BN;
+  }
+}
 
 template <int RQ, int FAM, int NV = 0>
 void launch_class(Ctx& c, const AugArgs& ag, const KernelParams& kp, const TileUnit* units, int n, int* counter) {
   constexpr int BN = TileCfg<RQ>::BN;
-  size_t smem = sizeof(double) * (size_t)(32 * ag.sdp + 2 * stage_doubles(RQ, BN, ag.sdp));
+  size_t smem = sizeof(double) * (size_t)(32 * ag.sdp + TileCfg<RQ>::NST * stage_doubles(RQ, BN, ag.sdp));
   auto fn = k_tile_contract<RQ, FAM, NV>;
-  CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int occ = 0;
-  CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 128, smem));
-  occ = std::max(occ, 1);
+  // attribute / occupancy queries are driver round trips: once per instantiation and size
+  static size_t smem_set = 0;
+  static int occ = 0;
+  if (smem != smem_set) {
+    CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 128, smem));
+    occ = std::max(occ, 1);
+    smem_set = smem;
+  }
   int grid = std::min<int64_t>(n, (int64_t)num_sms(c.device) * occ);
-  fn<<<grid, 128, smem, c.stream>>>(units, n, counter, ag.Pa, ag.Pb, ag.dpa, ag.sdp, kp);
+  fn<<<grid, 128, smem, c.stream>>>(units, n, counter, ag.Pa, ag.Pb, ag.dpa, ag.sdp, kp, ag.maps);
   check_launch("k_tile_contract");
 }
 
@@ -366,8 +455,6 @@ void run_tile_contract(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, s
     if (a.rq != b.rq) return a.rq > b.rq;
     return a.cost > b.cost;
   });
-  DevBuf<TileUnit> du(units.size(), c.stream);
-  du.upload(units);
   std::vector<int> starts;
   for (size_t i = 0; i < units.size(); i++)
     if (i == 0 || units[i].rq != units[i - 1].rq) starts.push_back((int)i);
@@ -382,6 +469,40 @@ void run_tile_contract(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, s
   DevBuf<double> aug((size_t)2 * tree->n * ag.dpa, c.stream);
   ag.Pa = aug.p;
   ag.Pb = aug.p + (size_t)tree->n * ag.dpa;
+  // tensor maps: one for the b rows per stage width, one per distinct W_b (base, shape, box)
+  std::vector<CUtensorMap> maps;
+  {
+    std::map<std::array<int64_t, 6>, int> idx;
+    auto get = [&](const double* base, int64_t rows, int64_t cols, int64_t ld, int br, int bc) {
+      std::array<int64_t, 6> key{(int64_t)reinterpret_cast<uintptr_t>(base), rows, cols, ld, br, bc};
+      auto it = idx.find(key);
+      if (it != idx.end()) return it->second;
+      int k = (int)maps.size();
+      maps.push_back(make_map_2d(base, rows, cols, ld, br, bc));
+      idx[key] = k;
+      return k;
+    };
+    const TileUnit* prev = nullptr;  // consecutive units mostly share W_b: skip the lookup
+    for (auto& u : units) {
+      if (!u.bulk) continue;
+      if (prev && prev->Wb == u.Wb && prev->rq == u.rq && prev->p_b == u.p_b && prev->s_b == u.s_b &&
+          prev->ldw == u.ldw) {
+        u.xmap = prev->xmap;
+        u.wmap = prev->wmap;
+      } else {
+        const int bn = class_bn(u.rq);
+        const int wrows = u.rq > 0 ? 8 * u.rq : 8;
+        u.xmap = get(ag.Pb, tree->n, ag.dpa, ag.dpa, bn, ag.sdp);
+        u.wmap = get(u.Wb, u.p_b, u.s_b, u.ldw, wrows, bn);
+      }
+      prev = &u;
+    }
+  }
+  DevBuf<CUtensorMap> maps_d(std::max<size_t>(maps.size(), 1), c.stream);
+  maps_d.upload(maps);
+  ag.maps = maps_d.p;
+  DevBuf<TileUnit> du(units.size(), c.stream);
+  du.upload(units);
   TimedLaunch tl(c, name);
   k_tile_aug<<<(unsigned)ceil_div(tree->n, 256), 256, 0, c.stream>>>(tree->Xt.p, tree->d_pad, tree->d, tree->n,
                                                                      kp.scale, aug.p, aug.p + (size_t)tree->n * ag.dpa,

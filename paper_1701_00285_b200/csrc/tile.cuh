@@ -23,6 +23,8 @@ struct TileUnit {
   double* U;                 // base of this pair's U
   int64_t ldu;
   double cost;               // for scheduling
+  int32_t bulk;              // stages filled by 2-D TMA (else 8-byte cp.async): W_b 16-byte aligned, ldw even
+  int32_t xmap, wmap;        // tensor maps of the b rows and of W_b (run_tile_contract)
 };
 
 struct KernelParams {
