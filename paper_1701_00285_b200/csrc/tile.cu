@@ -49,12 +49,25 @@ KernelParams make_kernel_params(const mlk_kernel& k) {
   return p;
 }
 
-static const int kRQ[] = {1, 2, 3, 4, 6, 7, 9, 12, 16, 20, 24};
+static const int kRQ[] = {1, 2, 3, 4, 6, 7, 8, 9, 12, 16, 20, 24};
 
 int tile_rq_class(int qc) {
   for (int r : kRQ)
     if (8 * r >= qc) return r;
   return kTileMaxRQ;
+}
+
+// (rq, nr) for a chunk of qc columns: 8 rq DMMA columns plus nr <= kTileMaxNR DFMA columns when
+// qc = 8 rq + nr with rq a class, else rq = the padding class and nr = 0
+static void tile_split(int qc, int& rq, int& nr) {
+  const int lo = qc / 8, rem = qc % 8;
+  if (lo >= 1 && lo <= 12 && rem >= 1 && rem <= kTileMaxNR && tile_rq_class(8 * lo) == lo) {
+    rq = lo;
+    nr = rem;
+  } else {
+    rq = tile_rq_class(qc);
+    nr = 0;
+  }
 }
 
 void make_tile_units(std::vector<TileUnit>& out, int64_t a_begin, int32_t s_a, int64_t b_begin, int32_t s_b,
@@ -63,7 +76,8 @@ void make_tile_units(std::vector<TileUnit>& out, int64_t a_begin, int32_t s_a, i
   int width = (int)ceil_div(ceil_div(p_b, nch), 8) * 8;
   for (int c0 = 0; c0 < p_b; c0 += width) {
     int qc = std::min(width, p_b - c0);
-    int rq = tile_rq_class(qc);
+    int rq, nr;
+    tile_split(qc, rq, nr);
     for (int32_t r0 = 0; r0 < s_a; r0 += 32) {
       TileUnit u;
       u.a_begin = a_begin;
@@ -76,6 +90,7 @@ void make_tile_units(std::vector<TileUnit>& out, int64_t a_begin, int32_t s_a, i
       u.p_b = p_b;
       u.trans = trans;
       u.rq = rq;
+      u.nr = nr;
       u.Wb = Wb;
       u.ldw = ldw;
       u.U = U;
@@ -84,7 +99,7 @@ void make_tile_units(std::vector<TileUnit>& out, int64_t a_begin, int32_t s_a, i
       u.bulk = (ldw % 2 == 0) && ((reinterpret_cast<uintptr_t>(Wb) & 15) == 0);
       u.xmap = u.wmap = -1;
       // FP64-slot estimate: Gram dp + kernel ~50 + contraction 8 rq per entry
-      u.cost = 32.0 * s_b * (dp + 50 + 8.0 * rq);
+      u.cost = 32.0 * s_b * (dp + 50 + 8.0 * rq + nr);
       out.push_back(u);
     }
   }
@@ -116,7 +131,11 @@ struct TileCfg {
   static constexpr int NACC = 1;                 // accumulator sets (2 measured no faster)
 };
 
-__host__ __device__ constexpr int stage_doubles(int rq, int bn, int sdp) { return bn * sdp + 8 * rq * bn; }
+// stage size rounded to 128 bytes: 2-D TMA writes need 128-byte aligned shared destinations
+// (the W part starts BN sdp doubles in, a multiple of 128 bytes since sdp is a multiple of 4)
+__host__ __device__ constexpr int stage_doubles(int rq, int bn, int sdp) {
+  return (bn * sdp + (8 * rq + kTileMaxNR) * bn + 15) / 16 * 16;
+}
 
 // Augmented, pre-scaled coordinates (x in tree order, s = kp.scale, u = s x):
 //   Pa[i] = [u_i, |u_i|^2, 1, 0...],  Pb[i] = [-2 u_i, 1, |u_i|^2, 0...]
@@ -214,7 +233,7 @@ __global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4)
       const double* pb = Pb + (u.b_begin + b0) * dpa;
       if (u.bulk) {
         if (lane == 0) {
-          mbar_arrive_expect_tx(&full[slot], 8u * (BN * sdp + 8 * RQ * BN));
+          mbar_arrive_expect_tx(&full[slot], 8u * BN * (sdp + u.wrows));
           tma_2d_g2s(Xs, maps + u.xmap, 0, (int)(u.b_begin + b0), &full[slot]);
           tma_2d_g2s(Ws, maps + u.wmap, b0, u.c0, &full[slot]);
         }
@@ -249,6 +268,13 @@ __global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4)
     double accv[NV > 0 ? NV : 1];
 #pragma unroll
     for (int i = 0; i < (NV > 0 ? NV : 1); i++) accv[i] = 0.0;
+    // DFMA remainder columns 8 RQ .. 8 RQ + nr - 1 (lane-partial sums); classes above 12 have
+    // no remainder (tile_split), which keeps their register budget
+    constexpr int NRMAX = (NV > 0 || RQ > 12) ? 0 : kTileMaxNR;
+    double accr[NRMAX > 0 ? NRMAX : 1];
+#pragma unroll
+    for (int i = 0; i < (NRMAX > 0 ? NRMAX : 1); i++) accr[i] = 0.0;
+    const int nr = NRMAX > 0 ? u.nr : 0;
 
     const int ar = warp * 8 + (lane >> 2);
     const int64_t ga = a0 + ar;
@@ -318,6 +344,18 @@ __global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4)
               if (q0 + qq < RQ)
                 dmma_8x8x4(acc[NACC - 1][q0 + qq][0], acc[NACC - 1][q0 + qq][1], cv[t][1], w[qq].y);
           }
+          // remainder columns on DFMA: every lane of a quad reads the same W row (broadcast)
+          if (NRMAX > 0 && nr > 0) {
+#pragma unroll
+            for (int l = 0; l < NRMAX; l++) {
+              if (l < nr) {
+                const double2 wv =
+                    *reinterpret_cast<const double2*>(Ws + (8 * RQ + l) * BN + 2 * (4 * t + (lane & 3)));
+                accr[l] = fma(cv[t][0], wv.x, accr[l]);
+                accr[l] = fma(cv[t][1], wv.y, accr[l]);
+              }
+            }
+          }
         }
       }
       // release the slot: the last of the four warps refills it with stage s + NST
@@ -345,7 +383,22 @@ __global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4)
           else u.U[(int64_t)r * u.ldu + u.c0 + l] = v;
         }
       }
-    } else if (r < u.s_a) {
+    } else {
+      if (NRMAX > 0 && nr > 0) {
+#pragma unroll
+        for (int l = 0; l < NRMAX; l++) {
+          double v = accr[l];
+          v += __shfl_xor_sync(0xffffffffu, v, 1);
+          v += __shfl_xor_sync(0xffffffffu, v, 2);
+          if ((lane & 3) == 0 && r < u.s_a && l < nr) {
+            v *= kp.sigma2;
+            const int col = u.c0 + 8 * RQ + l;
+            if (u.trans) u.U[(int64_t)col * u.ldu + r] = v;
+            else u.U[(int64_t)r * u.ldu + col] = v;
+          }
+        }
+      }
+      if (r < u.s_a) {
 #pragma unroll
       for (int q = 0; q < RQ; q++) {
 #pragma unroll
@@ -357,6 +410,7 @@ __global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4)
             else u.U[(int64_t)r * u.ldu + u.c0 + l] = v;
           }
         }
+      }
       }
     }
   }
@@ -436,6 +490,7 @@ void launch_fam(Ctx& c, const AugArgs& ag, const KernelParams& kp, int rq, const
     case 4: launch_class<4, FAM>(c, ag, kp, units, n, counter); break;
     case 6: launch_class<6, FAM>(c, ag, kp, units, n, counter); break;
     case 7: launch_class<7, FAM>(c, ag, kp, units, n, counter); break;
+    case 8: launch_class<8, FAM>(c, ag, kp, units, n, counter); break;
     case 9: launch_class<9, FAM>(c, ag, kp, units, n, counter); break;
     case 12: launch_class<12, FAM>(c, ag, kp, units, n, counter); break;
     case 16: launch_class<16, FAM>(c, ag, kp, units, n, counter); break;
@@ -485,15 +540,15 @@ void run_tile_contract(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, s
     const TileUnit* prev = nullptr;  // consecutive units mostly share W_b: skip the lookup
     for (auto& u : units) {
       if (!u.bulk) continue;
-      if (prev && prev->Wb == u.Wb && prev->rq == u.rq && prev->p_b == u.p_b && prev->s_b == u.s_b &&
-          prev->ldw == u.ldw) {
+      u.wrows = u.rq > 0 ? 8 * u.rq + u.nr : 8;
+      if (prev && prev->Wb == u.Wb && prev->rq == u.rq && prev->nr == u.nr && prev->p_b == u.p_b &&
+          prev->s_b == u.s_b && prev->ldw == u.ldw) {
         u.xmap = prev->xmap;
         u.wmap = prev->wmap;
       } else {
         const int bn = class_bn(u.rq);
-        const int wrows = u.rq > 0 ? 8 * u.rq : 8;
         u.xmap = get(ag.Pb, tree->n, ag.dpa, ag.dpa, bn, ag.sdp);
-        u.wmap = get(u.Wb, u.p_b, u.s_b, u.ldw, wrows, bn);
+        u.wmap = get(u.Wb, u.p_b, u.s_b, u.ldw, u.wrows, bn);
       }
       prev = &u;
     }

@@ -25,6 +25,8 @@ struct TileUnit {
   double cost;               // for scheduling
   int32_t bulk;              // stages filled by 2-D TMA (else 8-byte cp.async): W_b 16-byte aligned, ldw even
   int32_t xmap, wmap;        // tensor maps of the b rows and of W_b (run_tile_contract)
+  int32_t nr;                // columns 8 rq .. 8 rq + nr - 1 of the chunk are done with DFMAs
+  int32_t wrows;             // W_b rows staged per stage (8 rq + nr)
 };
 
 struct KernelParams {
@@ -40,6 +42,7 @@ KernelParams make_kernel_params(const mlk_kernel& k);
 // column-class instantiations available to the planner
 int tile_rq_class(int qc);  // smallest available rq with 8 rq >= qc
 constexpr int kTileMaxRQ = 24;
+constexpr int kTileMaxNR = 3;  // at most this many remainder columns go to DFMA instead of padding
 // Run all units (any mix of rq classes) on the context stream.
 void run_tile_contract(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, std::vector<TileUnit>& units,
                        const char* name);

@@ -13,6 +13,6 @@ echo "ncu_launch_rc=$?" >> $OUT/short_$TAG.log
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_tile_contract -s 1 -c 1 \
     -o $OUT/k5a_$TAG -f $SHORT > $OUT/ncu_k5a_$TAG.log 2>&1
 echo "ncu_k5a_rc=$?" >> $OUT/short_$TAG.log
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_qr_wy -s 8 -c 8 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_qr_wy -s 15 -c 1 \
     -o $OUT/qr_$TAG -f $SHORT > $OUT/ncu_qr_$TAG.log 2>&1
 echo "ncu_qr_rc=$?" >> $OUT/short_$TAG.log
