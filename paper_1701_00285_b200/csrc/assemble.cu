@@ -27,55 +27,97 @@ struct SearchItem {
   uint32_t mask;  // target depths still searched through q
 };
 
-// One CTA per item: emit (a, q) if depth(q) is a target, then min/max of the projections of
-// a's points onto v_q and the symmetric rule of reading R12 for every remaining target depth.
-__global__ void k_search_level(const SearchItem* __restrict__ cur, int n_cur, SearchItem* __restrict__ next,
-                               int* __restrict__ n_next, int2* __restrict__ pairs, int* __restrict__ n_pairs,
-                               const double* __restrict__ Xt, int dp, int d, const int64_t* __restrict__ nbeg,
-                               const int64_t* __restrict__ nend, const int8_t* __restrict__ state,
-                               const int32_t* __restrict__ depth, const double* __restrict__ thr,
-                               const double* __restrict__ dirs, const double* __restrict__ tau_tab) {
-  __shared__ double smn[32], smx[32];
-  const SearchItem it = cur[blockIdx.x];
-  const int dq = depth[it.q];
-  if (threadIdx.x == 0 && ((it.mask >> dq) & 1u)) {
-    int k = atomicAdd(n_pairs, 1);
-    pairs[k] = make_int2(it.a, it.q);
+// Projection extrema of every cell onto every internal node direction, mm[cell][q] =
+// (min, max) of x . v_q over the cell's points with the R6 arithmetic (products and sums rounded
+// separately, left to right).  Leaves: one CTA per (leaf, 8 directions); internal cells: the
+// exact min / max of their children (k_minmax_up), so every entry equals the direct value.
+constexpr int kMmQ = 8;
+__global__ void k_proj_minmax(const double* __restrict__ Xt, int dp, int d, const int64_t* __restrict__ lbeg,
+                              const int64_t* __restrict__ lend, const int32_t* __restrict__ lnode,
+                              const int8_t* __restrict__ state, const double* __restrict__ dirs, int n_int,
+                              double2* __restrict__ mm) {
+  extern __shared__ double sv[];  // kMmQ x d directions
+  __shared__ double smn[kMmQ][4], smx[kMmQ][4];
+  const int leaf = blockIdx.x, q0 = blockIdx.y * kMmQ;
+  const int nq = min(kMmQ, n_int - q0);
+  for (int e = threadIdx.x; e < nq * d; e += blockDim.x) sv[e] = dirs[(int64_t)q0 * d + e];
+  __syncthreads();
+  double mn[kMmQ], mx[kMmQ];
+#pragma unroll
+  for (int i = 0; i < kMmQ; i++) {
+    mn[i] = INFINITY;
+    mx[i] = -INFINITY;
   }
-  const uint32_t rest = it.mask & ~((2u << dq) - 1u);
-  if (rest == 0u || state[it.q] != 0) return;
-  const double* v = dirs + (int64_t)it.q * d;
-  double mn = INFINITY, mx = -INFINITY;
-  for (int64_t k = nbeg[it.a] + threadIdx.x; k < nend[it.a]; k += blockDim.x) {
+  for (int64_t k = lbeg[leaf] + threadIdx.x; k < lend[leaf]; k += blockDim.x) {
     const double* x = Xt + k * dp;
-    double acc = __dmul_rn(x[0], v[0]);
-    for (int j = 1; j < d; j++) acc = __dadd_rn(acc, __dmul_rn(x[j], v[j]));
-    mn = fmin(mn, acc);
-    mx = fmax(mx, acc);
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+#pragma unroll
+    for (int i = 0; i < kMmQ; i++) {
+      if (i < nq) {
+        const double* v = sv + i * d;
+        double acc = __dmul_rn(x[0], v[0]);
+        for (int j = 1; j < d; j++) acc = __dadd_rn(acc, __dmul_rn(x[j], v[j]));
+        mn[i] = fmin(mn[i], acc);
+        mx[i] = fmax(mx[i], acc);
+      }
+    }
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) {
-    smn[warp] = mn;
-    smx[warp] = mx;
+#pragma unroll
+  for (int i = 0; i < kMmQ; i++) {
+    for (int o = 16; o > 0; o >>= 1) {
+      mn[i] = fmin(mn[i], __shfl_xor_sync(0xffffffffu, mn[i], o));
+      mx[i] = fmax(mx[i], __shfl_xor_sync(0xffffffffu, mx[i], o));
+    }
+    if (lane == 0) {
+      smn[i][warp] = mn[i];
+      smx[i][warp] = mx[i];
+    }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < nq) {
+    const int i = threadIdx.x;
+    double a = smn[i][0], b = smx[i][0];
     for (int w = 1; w < (int)(blockDim.x >> 5); w++) {
-      mn = fmin(mn, smn[w]);
-      mx = fmax(mx, smx[w]);
+      a = fmin(a, smn[i][w]);
+      b = fmax(b, smx[i][w]);
     }
+    if (state[q0 + i] == 0) mm[(int64_t)lnode[leaf] * n_int + q0 + i] = make_double2(a, b);
+  }
+}
+
+__global__ void k_minmax_up(const int32_t* __restrict__ nodes, int cnt, int n_int, double2* __restrict__ mm) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= (int64_t)cnt * n_int) return;
+  const int c = nodes[e / n_int], q = (int)(e % n_int);
+  const double2 l = mm[(int64_t)(2 * c + 1) * n_int + q], r = mm[(int64_t)(2 * c + 2) * n_int + q];
+  mm[(int64_t)c * n_int + q] = make_double2(fmin(l.x, r.x), fmax(l.y, r.y));
+}
+
+// One level of every search at once, one thread per item (grid-stride, count read on the
+// device): emit (a, q) if depth(q) is a target, then the symmetric rule of reading R12 on the
+// tabulated extrema for every remaining target depth; surviving children are appended to the
+// next level's item region.  No host round trip between levels.
+__global__ void k_search_level(const SearchItem* __restrict__ cur, const int* __restrict__ n_cur_p,
+                               SearchItem* __restrict__ next, int* __restrict__ n_next, int2* __restrict__ pairs,
+                               int* __restrict__ n_pairs, const double2* __restrict__ mm, int n_int,
+                               const int8_t* __restrict__ state, const int32_t* __restrict__ depth,
+                               const double* __restrict__ thr, const double* __restrict__ tau_tab) {
+  const int n_cur = *n_cur_p;
+  for (int item = blockIdx.x * blockDim.x + threadIdx.x; item < n_cur; item += gridDim.x * blockDim.x) {
+    const SearchItem it = cur[item];
+    const int dq = depth[it.q];
+    if ((it.mask >> dq) & 1u) pairs[atomicAdd(n_pairs, 1)] = make_int2(it.a, it.q);
+    const uint32_t rest = it.mask & ~((2u << dq) - 1u);
+    if (rest == 0u || state[it.q] != 0) continue;
+    const double2 e = mm[(int64_t)it.a * n_int + it.q];
     const int i = depth[it.a];
     const double th = thr[it.q];
     uint32_t lm = 0, rm = 0;
     for (int j = 0; j < 32; j++) {
       if (!((rest >> j) & 1u)) continue;
       const double tau = tau_tab[i * 32 + j];
-      if (__dsub_rn(mn, tau) <= th) lm |= 1u << j;
-      if (__dadd_rn(mx, tau) > th) rm |= 1u << j;
+      if (__dsub_rn(e.x, tau) <= th) lm |= 1u << j;
+      if (__dadd_rn(e.y, tau) > th) rm |= 1u << j;
     }
     if (lm) next[atomicAdd(n_next, 1)] = SearchItem{it.a, 2 * it.q + 1, lm};
     if (rm) next[atomicAdd(n_next, 1)] = SearchItem{it.a, 2 * it.q + 2, rm};
@@ -121,33 +163,69 @@ std::vector<std::pair<int, int>> admitted_pairs(Ctx& c, const mlk_tree_s* tree, 
         for (int j = i; j <= t; j++) tab[i * 32 + j] = tau_ij(sp.tau, t, i, j);
       DevBuf<double> tab_d(tab.size(), st);
       tab_d.upload(tab);
-      DevBuf<int64_t> nb(nn, st), ne(nn, st);
-      nb.upload(tree->begin);
-      ne.upload(tree->end);
       DevBuf<int8_t> state(nn, st);
       state.upload(tree->state);
       DevBuf<int32_t> dep(nn, st);
       dep.upload(tree->depth);
-      DevBuf<SearchItem> cur(init.size(), st), nxt;
-      cur.upload(init);
-      int n_cur = (int)init.size();
-      DevBuf<int> counts(2, st);
-      std::vector<int2> all_pairs;
-      TimedLaunch tl(c, "search");
-      for (int level = 0; level <= t && n_cur > 0; level++) {
-        nxt.alloc((size_t)2 * n_cur, st);
-        DevBuf<int2> pr(n_cur, st);
-        counts.zero();
-        k_search_level<<<n_cur, 128, 0, st>>>(cur.p, n_cur, nxt.p, counts.p, pr.p, counts.p + 1, tree->Xt.p,
-                                              tree->d_pad, tree->d, nb.p, ne.p, state.p, dep.p, tree->thr_d.p,
-                                              tree->dir_d.p, tab_d.p);
-        check_launch("k_search_level");
-        auto cnt = counts.download(2);
-        auto ph = pr.download(cnt[1]);
-        all_pairs.insert(all_pairs.end(), ph.begin(), ph.end());
-        std::swap(cur, nxt);
-        n_cur = cnt[0];
+      // level L holds items (a, q) with depth(q) = L: at most |init| 2^L of them
+      std::vector<int64_t> off(t + 2, 0);
+      for (int L = 0; L <= t; L++) off[L + 1] = off[L] + (int64_t)init.size() * ((int64_t)1 << L);
+      DevBuf<SearchItem> items(off[t + 1], st);
+      CUDA_CHECK(cudaMemcpyAsync(items.p, init.data(), init.size() * sizeof(SearchItem), cudaMemcpyHostToDevice, st));
+      DevBuf<int2> pr(off[t + 1], st);
+      std::vector<int> cnt0(t + 3, 0);
+      cnt0[0] = (int)init.size();
+      DevBuf<int> counts(t + 3, st);  // items per level, then the pair count
+      counts.upload(cnt0);
+      {
+        TimedLaunch tl(c, "search");
+        // projection extrema table: leaves directly, internal cells bottom-up
+        const int n_int = (1 << t) - 1;
+        DevBuf<double2> mm((size_t)nn * n_int, st);
+        std::vector<int64_t> lb, le;
+        std::vector<int32_t> ln;
+        std::vector<std::vector<int32_t>> internal_at(t + 1);
+        for (int q = 0; q < nn; q++) {
+          if (tree->state[q] == 1) {
+            lb.push_back(tree->begin[q]);
+            le.push_back(tree->end[q]);
+            ln.push_back(q);
+          } else if (tree->state[q] == 0) {
+            internal_at[tree->depth[q]].push_back(q);
+          }
+        }
+        DevBuf<int64_t> lbd(lb.size(), st), led(le.size(), st);
+        DevBuf<int32_t> lnd(ln.size(), st);
+        lbd.upload(lb);
+        led.upload(le);
+        lnd.upload(ln);
+        const int d = tree->d;
+        const size_t vsm = sizeof(double) * kMmQ * d;
+        if (vsm > 48 * 1024) CUDA_CHECK(cudaFuncSetAttribute(k_proj_minmax, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vsm));
+        k_proj_minmax<<<dim3((unsigned)ln.size(), (unsigned)ceil_div(n_int, kMmQ)), 128, vsm, st>>>(
+            tree->Xt.p, tree->d_pad, d, lbd.p, led.p, lnd.p, state.p, tree->dir_d.p, n_int, mm.p);
+        check_launch("k_proj_minmax");
+        std::vector<DevBuf<int32_t>> lvl_nodes(t + 1);
+        for (int L = t; L >= 1; L--) {
+          if (internal_at[L].empty()) continue;
+          lvl_nodes[L].alloc(internal_at[L].size(), st);
+          lvl_nodes[L].upload(internal_at[L]);
+          const int64_t cntL = (int64_t)internal_at[L].size() * n_int;
+          k_minmax_up<<<(unsigned)ceil_div(cntL, 256), 256, 0, st>>>(lvl_nodes[L].p, (int)internal_at[L].size(), n_int,
+                                                                    mm.p);
+          check_launch("k_minmax_up");
+        }
+        for (int L = 0; L <= t; L++) {
+          const int64_t cap = off[L + 1] - off[L];
+          const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(cap, 128), 8 * (int64_t)num_sms(c.device));
+          k_search_level<<<grid, 128, 0, st>>>(items.p + off[L], counts.p + L, items.p + off[std::min(L + 1, t)],
+                                               counts.p + L + 1, pr.p, counts.p + t + 2, mm.p, n_int, state.p, dep.p,
+                                               tree->thr_d.p, tab_d.p);
+          check_launch("k_search_level");
+        }
       }
+      auto cnt = counts.download(t + 3);
+      std::vector<int2> all_pairs = pr.download(cnt[t + 2]);
       for (auto& p : all_pairs) add(p.x, p.y);
     }
   }

@@ -73,21 +73,29 @@ __device__ __forceinline__ void cas(SortKey* a, int i, int l, bool asc) {
   }
 }
 
-// Bitonic steps inside one tile of `tile` elements: if full, stages k = 2..tile; otherwise
-// stage k (global) strides j0..1.
-__global__ void k_bitonic_smem(SortKey* __restrict__ keys, int tile, int64_t k_stage, int j0, int full) {
+// Bitonic network that sorts every aligned block of kfinal elements independently (kfinal =
+// the whole padded array at the root; smaller below, where no segment straddles a block):
+// merge stages k < kfinal alternate direction as usual, stage kfinal is ascending everywhere.
+__device__ __forceinline__ bool bitonic_asc(int64_t i, int64_t k, int64_t kfinal) {
+  return k == kfinal || (i & k) == 0;
+}
+
+// Bitonic steps inside one tile of `tile` elements: if full, stages k = 2..min(tile, kfinal);
+// otherwise stage k (global) strides j0..1.
+__global__ void k_bitonic_smem(SortKey* __restrict__ keys, int tile, int64_t k_stage, int j0, int full,
+                               int64_t kfinal) {
   __shared__ SortKey sh[TILE];
   int64_t base = (int64_t)blockIdx.x * tile;
   for (int i = threadIdx.x; i < tile; i += blockDim.x) sh[i] = keys[base + i];
   __syncthreads();
   int half = tile >> 1;
   if (full) {
-    for (int k = 2; k <= tile; k <<= 1) {
+    const int kmax = (int)std::min<int64_t>(tile, kfinal);
+    for (int k = 2; k <= kmax; k <<= 1) {
       for (int j = k >> 1; j > 0; j >>= 1) {
         for (int t = threadIdx.x; t < half; t += blockDim.x) {
           int i = 2 * j * (t / j) + (t % j);
-          bool asc = (((base + i) & k) == 0);
-          cas(sh, i, i + j, asc);
+          cas(sh, i, i + j, bitonic_asc(base + i, k, kfinal));
         }
         __syncthreads();
       }
@@ -96,8 +104,7 @@ __global__ void k_bitonic_smem(SortKey* __restrict__ keys, int tile, int64_t k_s
     for (int j = j0; j > 0; j >>= 1) {
       for (int t = threadIdx.x; t < half; t += blockDim.x) {
         int i = 2 * j * (t / j) + (t % j);
-        bool asc = (((base + i) & k_stage) == 0);
-        cas(sh, i, i + j, asc);
+        cas(sh, i, i + j, bitonic_asc(base + i, k_stage, kfinal));
       }
       __syncthreads();
     }
@@ -105,12 +112,13 @@ __global__ void k_bitonic_smem(SortKey* __restrict__ keys, int tile, int64_t k_s
   for (int i = threadIdx.x; i < tile; i += blockDim.x) keys[base + i] = sh[i];
 }
 
-__global__ void k_bitonic_global(SortKey* __restrict__ keys, int64_t npad, int64_t k_stage, int64_t j) {
+__global__ void k_bitonic_global(SortKey* __restrict__ keys, int64_t npad, int64_t k_stage, int64_t j,
+                                 int64_t kfinal) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= npad / 2) return;
   int64_t i = 2 * j * (t / j) + (t % j);
   int64_t l = i + j;
-  bool asc = ((i & k_stage) == 0);
+  bool asc = bitonic_asc(i, k_stage, kfinal);
   SortKey x = keys[i], y = keys[l];
   bool sw = asc ? key_less(y, x) : key_less(x, y);
   if (sw) {
@@ -179,19 +187,21 @@ __global__ void k_tree_gather(const double* __restrict__ X, int d, int dp, int64
   norm2[k] = s;
 }
 
-void bitonic_sort(Ctx& c, SortKey* keys, int64_t npad) {
+// Sort keys by (segment, projection, id) within aligned blocks of kfinal elements; every
+// segment lies inside one block, so this equals the full sort of the array.
+void bitonic_sort(Ctx& c, SortKey* keys, int64_t npad, int64_t kfinal) {
   TimedLaunch tl(c, "tree_sort");
   int tile = (int)std::min<int64_t>(TILE, npad);
   int threads = std::min(1024, std::max(1, tile / 2));
-  k_bitonic_smem<<<(unsigned)(npad / tile), threads, 0, c.stream>>>(keys, tile, 0, 0, 1);
+  k_bitonic_smem<<<(unsigned)(npad / tile), threads, 0, c.stream>>>(keys, tile, 0, 0, 1, kfinal);
   check_launch("k_bitonic_smem");
-  for (int64_t k = 2 * (int64_t)tile; k <= npad; k <<= 1) {
+  for (int64_t k = 2 * (int64_t)tile; k <= kfinal; k <<= 1) {
     for (int64_t j = k >> 1; j >= tile; j >>= 1) {
       int64_t pairs = npad / 2;
-      k_bitonic_global<<<(unsigned)ceil_div(pairs, 256), 256, 0, c.stream>>>(keys, npad, k, j);
+      k_bitonic_global<<<(unsigned)ceil_div(pairs, 256), 256, 0, c.stream>>>(keys, npad, k, j, kfinal);
       check_launch("k_bitonic_global");
     }
-    k_bitonic_smem<<<(unsigned)(npad / tile), threads, 0, c.stream>>>(keys, tile, k, tile / 2, 0);
+    k_bitonic_smem<<<(unsigned)(npad / tile), threads, 0, c.stream>>>(keys, tile, k, tile / 2, 0, kfinal);
     check_launch("k_bitonic_smem");
   }
 }
@@ -348,7 +358,21 @@ mlk_status mlk_build_tree(mlk_ctx ctx, const double* X, int64_t n, int32_t d, in
                                                                 tr->dir_d.p, keys.p);
       check_launch("k_tree_keys");
     }
-    bitonic_sort(c, keys.p, npad);
+    // smallest power-of-two block that no segment straddles (positions past n sort last)
+    int64_t kfinal = 2;
+    for (;;) {
+      bool ok = kfinal >= npad;
+      if (!ok) {
+        ok = true;
+        for (size_t i = 0; i < sb.size() && ok; i++) {
+          const int64_t e = (i + 1 < sb.size() ? sb[i + 1] : n) - 1;
+          ok = sb[i] / kfinal == e / kfinal;
+        }
+      }
+      if (ok) break;
+      kfinal <<= 1;
+    }
+    bitonic_sort(c, keys.p, npad, std::min(kfinal, npad));
     {
       TimedLaunch tl(c, "tree_split");
       k_tree_perm<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(keys.p, n, tr->perm_d.p);
