@@ -185,6 +185,14 @@ mlk_status mlk_cw_info(mlk_cw cw, int32_t* n_cells, int64_t* n_blocks, int64_t* 
  * values are complete only after mlk_cw_unpack. */
 mlk_status mlk_cw_export(mlk_cw cw, int32_t* brow_ptr, int32_t* bcol, int64_t* val_off,
                          double* values);
+/* Asynchronous export of all nnz BSR values into `values` (host or device memory): the copy is
+ * enqueued on the context's copy stream behind the work already enqueued on the context stream,
+ * and the call returns without waiting, so the transfer overlaps later calls (e.g. the C_W v
+ * product).  Pinned host memory gives a true DMA overlap.  mlk_ctx_wait_copies blocks until
+ * every copy enqueued this way has landed; `values` and `cw` must stay valid until then.  With
+ * nranks > 1 call it after mlk_cw_unpack. */
+mlk_status mlk_cw_export_async(mlk_ctx ctx, mlk_cw cw, double* values);
+mlk_status mlk_ctx_wait_copies(mlk_ctx ctx);
 /* Executed FP64 flops by stage (all ranks): gram = 2 d per evaluated covariance entry,
  * contract1 = the fused tile products V_b = C W_b^T (2 p_b per entry), contract2 = the
  * products W_a V_b[X_a] (2 p_a |X_a| p_b per block). */

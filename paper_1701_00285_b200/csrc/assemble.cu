@@ -638,6 +638,23 @@ mlk_status mlk_cw_export(mlk_cw cw, int32_t* brow_ptr, int32_t* bcol, int64_t* v
   MLK_API_END
 }
 
+mlk_status mlk_cw_export_async(mlk_ctx ctx, mlk_cw cw, double* values) {
+  MLK_API_BEGIN
+  MLK_REQUIRE(ctx && cw && values, "NULL argument");
+  Ctx& c = ctx->c;
+  CUDA_CHECK(cudaSetDevice(c.device));
+  MLK_REQUIRE(cw->device == c.device, "cw lives on another device");
+  if (!c.copy_stream) {
+    CUDA_CHECK(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
+    CUDA_CHECK(cudaEventCreateWithFlags(&c.copy_ready, cudaEventDisableTiming));
+  }
+  CUDA_CHECK(cudaEventRecord(c.copy_ready, c.stream));
+  CUDA_CHECK(cudaStreamWaitEvent(c.copy_stream, c.copy_ready, 0));
+  if (cw->nnz > 0)
+    CUDA_CHECK(cudaMemcpyAsync(values, cw->values.p, sizeof(double) * cw->nnz, cudaMemcpyDefault, c.copy_stream));
+  MLK_API_END
+}
+
 mlk_status mlk_cw_flops(mlk_cw cw, double* gram, double* contract1, double* contract2) {
   MLK_API_BEGIN
   MLK_REQUIRE(cw, "cw is NULL");

@@ -70,6 +70,7 @@ struct QrJob {
   double* qlo;    // rows j < nc of Q^T (row j at qlo + j*ldq)
   double* qhi;    // rows j >= nc of Q^T at qhi + (j - nc)*ldq
   int64_t ldq;
+  int32_t stacked;  // 1: A = [R_L; R_R] (m = 2 nc, both upper triangular), see k_qr_wy
 };
 
 constexpr int kQrSmemLimit = 225 * 1024;
@@ -111,43 +112,66 @@ __global__ void __launch_bounds__(kQrThreads) k_qr_wy(const QrJob* __restrict__ 
     }
     __syncthreads();
   }
-  // warp w owns the columns j = w, w + nw, ... in both phases of every step
+  // Rows a reflector touches: dense, x = rows k+1..m-1; stacked [R_L; R_R] (both upper
+  // triangular), x has nonzeros only in rows nc..nc+k and the structure is preserved, so
+  // rows nc..nc+k (exactly the entries LAPACK's dense sweep would change).
+  const bool stk = jb.stacked != 0;
+  // warp w owns the columns j = w, w + nw, ... in both phases of every step; a warp's columns
+  // are processed CB at a time so their dot reductions share the shuffle rounds
+  constexpr int CB = 4;
   for (int k = 0; k < nc; k++) {
     const double* ak = A + (int64_t)k * lda;
-    // (1) dots x . a_j (rows i > k) for the owned columns j >= k, a copy of a_kj; the owner
+    const int lo = stk ? nc : k + 1, hi = stk ? nc + k + 1 : m;
+    // (1) dots x . a_j (rows lo..hi-1) for the owned columns j >= k, a copy of a_kj; the owner
     //     of column k forms the reflector; the owner of column k - 1 finishes it (beta on the
     //     diagonal, x scaled into v) -- column k - 1 is not read in this step
-    for (int j = warp; j < nc; j += nw) {
-      if (j == k - 1) {
-        double* ap = A + (int64_t)j * lda;
-        const double* pv = s_piv + 3 * ((k - 1) & 1);
-        const double scal = pv[1];
-        for (int i = k + lane; i < m; i += 32) ap[i] *= scal;
-        if (lane == 0) ap[j] = pv[2];
-        continue;
+    if (k > 0 && warp == (k - 1) % nw) {
+      double* ap = A + (int64_t)(k - 1) * lda;
+      const double* pv = s_piv + 3 * ((k - 1) & 1);
+      const int plo = stk ? nc : k, phi = stk ? nc + k : m;
+      for (int i = plo + lane; i < phi; i += 32) ap[i] *= pv[1];
+      if (lane == 0) ap[k - 1] = pv[2];
+    }
+    const int jfirst = warp + ((k - warp + nw - 1) / nw) * nw;  // first owned column >= k
+    for (int j0 = jfirst; j0 < nc; j0 += CB * nw) {
+      double sum[CB];
+      const double* aj[CB];
+#pragma unroll
+      for (int c = 0; c < CB; c++) {
+        sum[c] = 0.0;
+        aj[c] = A + (int64_t)min(j0 + c * nw, nc - 1) * lda;
       }
-      if (j < k) continue;
-      const double* aj = A + (int64_t)j * lda;
-      double s = 0.0;
-      for (int i = k + 1 + lane; i < m; i += 32) s = fma(ak[i], aj[i], s);
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      for (int i = lo + lane; i < hi; i += 32) {
+        const double x = ak[i];
+#pragma unroll
+        for (int c = 0; c < CB; c++) sum[c] = fma(x, aj[c][i], sum[c]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int c = 0; c < CB; c++) sum[c] += __shfl_xor_sync(0xffffffffu, sum[c], o);
       if (lane == 0) {
-        if (j == k) {
-          const double alpha = ak[k];
-          double tau = 0.0, scal = 1.0, beta = alpha;
-          if (s > 0.0) {
-            beta = -copysign(sqrt(fma(alpha, alpha, s)), alpha);
-            tau = (beta - alpha) / beta;
-            scal = 1.0 / (alpha - beta);
+#pragma unroll
+        for (int c = 0; c < CB; c++) {
+          const int j = j0 + c * nw;
+          if (j >= nc) break;
+          if (j == k) {
+            const double alpha = ak[k], xn2 = sum[c];
+            double tau = 0.0, scal = 1.0, beta = alpha;
+            if (xn2 > 0.0) {
+              beta = -copysign(sqrt(fma(alpha, alpha, xn2)), alpha);
+              tau = (beta - alpha) / beta;
+              scal = 1.0 / (alpha - beta);
+            }
+            taus[k] = tau;
+            double* pv = s_piv + 3 * (k & 1);
+            pv[0] = tau;
+            pv[1] = scal;
+            pv[2] = beta;
+          } else {
+            dots[j] = sum[c];
+            rowk[j] = aj[c][k];
           }
-          taus[k] = tau;
-          double* pv = s_piv + 3 * (k & 1);
-          pv[0] = tau;
-          pv[1] = scal;
-          pv[2] = beta;
-        } else {
-          dots[j] = s;
-          rowk[j] = aj[k];
         }
       }
     }
@@ -156,14 +180,25 @@ __global__ void __launch_bounds__(kQrThreads) k_qr_wy(const QrJob* __restrict__ 
     const double tau = s_piv[3 * (k & 1)];
     if (tau != 0.0) {
       const double scal = s_piv[3 * (k & 1) + 1];
-      for (int j = warp; j < nc; j += nw) {
-        if (j <= k) continue;
-        double* aj = A + (int64_t)j * lda;
-        const double akj = rowk[j];
-        const double f = tau * fma(scal, dots[j], akj);
-        const double g = f * scal;
-        for (int i = k + 1 + lane; i < m; i += 32) aj[i] = fma(-g, ak[i], aj[i]);
-        if (lane == 0) aj[k] = akj - f;
+      const int jnext = warp + ((k + 1 - warp + nw - 1) / nw) * nw;  // first owned column > k
+      for (int j0 = jnext; j0 < nc; j0 += CB * nw) {
+        double g[CB];
+        double* aj[CB];
+#pragma unroll
+        for (int c = 0; c < CB; c++) {
+          const int j = min(j0 + c * nw, nc - 1);
+          aj[c] = A + (int64_t)j * lda;
+          const double akj = rowk[j];
+          const double f = j0 + c * nw < nc ? tau * fma(scal, dots[j], akj) : 0.0;
+          g[c] = f * scal;
+          if (lane == 0 && j0 + c * nw < nc) aj[c][k] = akj - f;
+        }
+        for (int i = lo + lane; i < hi; i += 32) {
+          const double x = ak[i];
+#pragma unroll
+          for (int c = 0; c < CB; c++)
+            if (j0 + c * nw < nc) aj[c][i] = fma(-g[c], x, aj[c][i]);
+        }
       }
     }
     __syncthreads();
@@ -172,7 +207,8 @@ __global__ void __launch_bounds__(kQrThreads) k_qr_wy(const QrJob* __restrict__ 
   if (warp == (nc - 1) % nw) {
     double* ap = A + (int64_t)(nc - 1) * lda;
     const double* pv = s_piv + 3 * ((nc - 1) & 1);
-    for (int i = nc + lane; i < m; i += 32) ap[i] *= pv[1];
+    const int plo = stk ? nc : nc, phi = stk ? 2 * nc : m;
+    for (int i = plo + lane; i < phi; i += 32) ap[i] *= pv[1];
     if (lane == 0) ap[nc - 1] = pv[2];
   }
   __syncthreads();
@@ -202,12 +238,13 @@ __global__ void __launch_bounds__(kQrThreads) k_qr_wy(const QrJob* __restrict__ 
     const double* vq = A + (int64_t)q * lda;
     const double* vl = A + (int64_t)l * lda;
     double s0 = vq[l], s1 = 0.0;
-    int i = l + 1;
-    for (; i + 1 < m; i += 2) {
+    int i = stk ? nc : l + 1;
+    const int iend = stk ? nc + q + 1 : m;   // stacked: column q of V is zero past row nc + q
+    for (; i + 1 < iend; i += 2) {
       s0 = fma(vq[i], vl[i], s0);
       s1 = fma(vq[i + 1], vl[i + 1], s1);
     }
-    if (i < m) s0 = fma(vq[i], vl[i], s0);
+    if (i < iend) s0 = fma(vq[i], vl[i], s0);
     G[(int64_t)q * nc + l] = s0 + s1;
   }
   __syncthreads();
@@ -418,6 +455,7 @@ mlk_status mlk_build_basis(mlk_ctx ctx, mlk_tree tree, int32_t w, mlk_basis* out
       jb.qlo = B->Phi.p + B->phi_off[q];
       jb.qhi = B->W.p + B->w_off[q];
       jb.ldq = s;
+      jb.stacked = 0;
       qj.push_back(jb);
       k++;
     }
@@ -449,6 +487,7 @@ mlk_status mlk_build_basis(mlk_ctx ctx, mlk_tree tree, int32_t w, mlk_basis* out
       jb.qlo = Qt.p + i * 4 * (size_t)M * M;       // Q column-major == Q^T row-major
       jb.qhi = jb.qlo + (size_t)M * 2 * M;
       jb.ldq = 2 * M;
+      jb.stacked = 1;
       qj.push_back(jb);
     }
     DevBuf<StackJob> sjd(nc, st);

@@ -61,6 +61,8 @@ struct Ctx {
   // slow and erratic -- 0.3 to 14 ms per call on B200 while NVML is polled -- so it is queried
   // once per context, not per call)
   int64_t free_at_first_use = -1;
+  cudaStream_t copy_stream = nullptr;  // mlk_cw_export_async (created on first use)
+  cudaEvent_t copy_ready = nullptr;
   int64_t scratch_budget_bytes();
 
   cudaEvent_t get_event();

@@ -150,8 +150,21 @@ void mlk_ctx_destroy(mlk_ctx ctx) {
     cudaEventDestroy(p.b);
   }
   for (auto e : ctx->c.event_pool) cudaEventDestroy(e);
+  if (ctx->c.copy_stream) {
+    cudaStreamSynchronize(ctx->c.copy_stream);
+    cudaStreamDestroy(ctx->c.copy_stream);
+    cudaEventDestroy(ctx->c.copy_ready);
+  }
   if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
   delete ctx;
+}
+
+mlk_status mlk_ctx_wait_copies(mlk_ctx ctx) {
+  MLK_API_BEGIN
+  MLK_REQUIRE(ctx, "ctx is NULL");
+  CUDA_CHECK(cudaSetDevice(ctx->c.device));
+  if (ctx->c.copy_stream) CUDA_CHECK(cudaStreamSynchronize(ctx->c.copy_stream));
+  MLK_API_END
 }
 
 void* mlk_ctx_stream(mlk_ctx ctx) { return ctx ? (void*)ctx->c.stream : nullptr; }

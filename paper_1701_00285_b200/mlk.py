@@ -34,7 +34,7 @@ SYMBOLS = [
     "mlk_basis_info", "mlk_basis_export", "mlk_apply_wt", "mlk_apply_w", "mlk_assemble_cw",
     "mlk_cw_free", "mlk_cw_info", "mlk_cw_export", "mlk_cw_owner", "mlk_cw_shard_len", "mlk_cw_pack",
     "mlk_cw_unpack", "mlk_cw_values_device", "mlk_cov_matvec", "mlk_cw_matvec", "mlk_partition_lpt",
-    "mlk_shard_plan", "mlk_launch_count", "mlk_cw_flops",
+    "mlk_shard_plan", "mlk_launch_count", "mlk_cw_flops", "mlk_cw_export_async", "mlk_ctx_wait_copies",
 ]
 
 
@@ -98,6 +98,8 @@ _sig = {
     "mlk_shard_plan": (C.c_int, [P, P, C.c_int64, C.c_int32, P, P]),
     "mlk_launch_count": (C.c_int64, []),
     "mlk_cw_flops": (C.c_int, [P, P, P, P]),
+    "mlk_cw_export_async": (C.c_int, [P, P, P]),
+    "mlk_ctx_wait_copies": (C.c_int, [P]),
 }
 for _n, (_r, _a) in _sig.items():
     _f = getattr(_lib, _n)
@@ -178,6 +180,10 @@ class Ctx:
             _check(_lib.mlk_ctx_kernel_stats(self.h, i, None, buf, 128, C.byref(l), C.byref(ms)))
             out[buf.value.decode()] = dict(launches=l.value, ms=ms.value)
         return out
+
+    def wait_copies(self):
+        """Block until every mlk_cw_export_async copy of this context has landed."""
+        _check(_lib.mlk_ctx_wait_copies(self.h))
 
     def close(self):
         if getattr(self, "h", None):
@@ -315,6 +321,14 @@ class CW:
         vp, _ = _ptr(vals)
         _check(_lib.mlk_cw_export(self.h, None, None, None, vp))
         return dict(brow_ptr=brow_ptr, bcol=bcol, val_off=val_off, values=vals)
+
+    def export_async(self, ctx, out):
+        """Enqueue the copy of all BSR values into `out` (NumPy array or torch tensor, ideally
+        pinned) behind the work already on the context stream; ctx.wait_copies() completes it."""
+        vp, _ = _ptr(out)
+        _check(_lib.mlk_cw_export_async(ctx.h, self.h, vp))
+        self._async_keep = out
+        return out
 
     def stage_flops(self):
         g, a, b = C.c_double(), C.c_double(), C.c_double()

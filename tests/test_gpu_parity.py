@@ -280,6 +280,27 @@ def test_assembly_deterministic(mlk, ctx):
     assert np.array_equal(a, b)
 
 
+def test_export_async_matches_export(mlk, ctx):
+    """mlk_cw_export_async (copy stream, overlapping the next call) lands the same values."""
+    import torch
+    X, dirs = _setup(4096, 10, 128, 1)
+    g = mlk.build_tree(ctx, X, 128, 1, dirs)
+    gb = mlk.build_basis(ctx, g, 2)
+    k = dict(family=1, rho=1.0)
+    cw = mlk.assemble_cw(ctx, g, gb, k, dict(mode=1, tau=1e-3))
+    ref = cw.export()["values"]
+    pinned = torch.empty(cw.nnz, dtype=torch.float64).pin_memory()
+    cw.export_async(ctx, pinned.numpy())
+    v = wl.vectors(1, gb.dim, seed=4)
+    mlk.cw_matvec(ctx, g, gb, k, None, mlk.MATVEC_EXACT, v)   # runs while the copy is in flight
+    ctx.wait_copies()
+    assert np.array_equal(pinned.numpy(), ref)
+    dev = torch.empty(cw.nnz, dtype=torch.float64, device="cuda")
+    cw.export_async(ctx, dev)
+    ctx.wait_copies()
+    assert np.array_equal(dev.cpu().numpy(), ref)
+
+
 # --------------------------------------------------------------------------------- matvec
 @pytest.mark.parametrize("fam,rho", FAMS)
 def test_matvec_exact_and_bsr(mlk, ctx, fam, rho):
