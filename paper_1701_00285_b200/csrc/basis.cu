@@ -6,6 +6,8 @@
 // The QR kernel runs one CTA per matrix (batched over the cells of a level).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <memory>
 
 #include "api.cuh"
@@ -79,18 +81,23 @@ constexpr int kQrSmemLimit = 225 * 1024;
 // ||(alpha, x)||, tau = (beta - alpha)/beta, v = x/(alpha - beta), tau = 0 when x = 0), then
 // W1T = T^T V^T for the compact-WY form Q = H_0 ... H_{nc-1} = I - V T V^T, so that
 // Q^T = I - V W1T is formed by the DMMA GEMM (gemm.cu).
-//  * Column step k takes two barriers: (1) one warp per column j >= k forms x . a_j (rows
-//    i > k, lanes over rows, shuffle reduction); the warp of column k (j = k gives |x|^2)
-//    also forms beta, tau and the scale once and publishes them; (2) all threads apply H_k
-//    element-wise to the trailing columns, reading the unscaled x (column k's scaling and
-//    beta are stored at the start of the next step).
+//  * Column step k takes two barriers: (1) thread j forms x . a_j for its column j >= k
+//    (serial, four partial sums); the owner of column k (j = k gives |x|^2) forms beta, tau
+//    and the scale once; (2) thread j applies H_k to its column j > k, reading the unscaled
+//    x (column k's scaling and beta are stored at the start of the next step).
+//  * Stacked merges [R_L; R_R] touch only rows {k} and nc..nc+k in step k (the triangles'
+//    structure is preserved), a third of the dense work.
 //  * T is never formed: with G = V^T V, T^{-1} = triu(G, 1) + diag(1/tau) (the inverse of the
 //    dlarft recursion), so W1T solves T^{-T} W1T = V^T by forward substitution,
 //    W1T[l][i] = tau_l (V[i][l] - sum_{q<l} G[q][l] W1T[q][i]), one thread per row i, in place
 //    of A's row i (R and V are exported first).  A reflector with tau = 0 is the identity and
 //    gets a zero row.
 // SMEM: the matrix lives in shared memory (odd column stride); GS: G lives there too.
-constexpr int kQrThreads = 1024;
+constexpr int kQrThreads = 256;
+// phase timestamps of block 0 of the last k_qr_wy launch (diagnostics, MLK_QR_PROFILE)
+__device__ long long g_qr_prof[12];
+#define QR_STAMP(i) \
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_qr_prof[i] = clock64();
 
 template <bool SMEM, bool GS>
 __global__ void __launch_bounds__(kQrThreads) k_qr_wy(const QrJob* __restrict__ jobs, int* __restrict__ rank_flag) {
@@ -101,78 +108,75 @@ __global__ void __launch_bounds__(kQrThreads) k_qr_wy(const QrJob* __restrict__ 
   const int lda = SMEM ? (m | 1) : m;
   double* taus = sh;                                // nc
   double* dots = taus + nc;                         // nc: x . a_j of the current step (by column)
-  double* rowk = dots + nc;                         // nc: a_kj of the current step (by column)
-  double* A = SMEM ? rowk + nc + ((3 * nc) & 1) : jb.A;
+  double* A = SMEM ? dots + nc : jb.A;
   double* G = GS ? A + (int64_t)lda * nc : jb.T;    // G[q][l], q < l, row-major nc x nc
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  QR_STAMP(0);
   if (SMEM) {
-    for (int64_t e = tid; e < (int64_t)m * nc; e += nt) {
-      const int j = (int)(e / m), i = (int)(e - (int64_t)j * m);
-      A[(int64_t)j * lda + i] = jb.A[e];
+    // four independent global loads in flight per thread
+    const int64_t tot = (int64_t)m * nc;
+    for (int64_t e0 = tid; e0 < tot; e0 += 4 * (int64_t)nt) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) v[u] = e0 + u * nt < tot ? jb.A[e0 + u * nt] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int64_t e = e0 + u * nt;
+        if (e < tot) {
+          const int j = (int)(e / m), i = (int)(e - (int64_t)j * m);
+          A[(int64_t)j * lda + i] = v[u];
+        }
+      }
     }
     __syncthreads();
   }
+  QR_STAMP(1);
   // Rows a reflector touches: dense, x = rows k+1..m-1; stacked [R_L; R_R] (both upper
   // triangular), x has nonzeros only in rows nc..nc+k and the structure is preserved, so
   // rows nc..nc+k (exactly the entries LAPACK's dense sweep would change).
   const bool stk = jb.stacked != 0;
-  // warp w owns the columns j = w, w + nw, ... in both phases of every step; a warp's columns
-  // are processed CB at a time so their dot reductions share the shuffle rounds
-  constexpr int CB = 4;
+  // Thread j owns column j: its dot x . a_j is a serial sum (four partial sums, no shuffles)
+  // and its update touches only its column; the odd column stride keeps the column-strided
+  // accesses of a half-warp in distinct banks.  Two barriers per step.
   for (int k = 0; k < nc; k++) {
     const double* ak = A + (int64_t)k * lda;
     const int lo = stk ? nc : k + 1, hi = stk ? nc + k + 1 : m;
-    // (1) dots x . a_j (rows lo..hi-1) for the owned columns j >= k, a copy of a_kj; the owner
-    //     of column k forms the reflector; the owner of column k - 1 finishes it (beta on the
-    //     diagonal, x scaled into v) -- column k - 1 is not read in this step
-    if (k > 0 && warp == (k - 1) % nw) {
+    if (k > 0) {  // finish column k - 1 (not read in this step): x scaled into v, beta on the diagonal
       double* ap = A + (int64_t)(k - 1) * lda;
       const double* pv = s_piv + 3 * ((k - 1) & 1);
       const int plo = stk ? nc : k, phi = stk ? nc + k : m;
-      for (int i = plo + lane; i < phi; i += 32) ap[i] *= pv[1];
-      if (lane == 0) ap[k - 1] = pv[2];
+      for (int i = plo + tid; i < phi; i += nt) ap[i] *= pv[1];
+      if (tid == 0) ap[k - 1] = pv[2];
     }
-    const int jfirst = warp + ((k - warp + nw - 1) / nw) * nw;  // first owned column >= k
-    for (int j0 = jfirst; j0 < nc; j0 += CB * nw) {
-      double sum[CB];
-      const double* aj[CB];
-#pragma unroll
-      for (int c = 0; c < CB; c++) {
-        sum[c] = 0.0;
-        aj[c] = A + (int64_t)min(j0 + c * nw, nc - 1) * lda;
+    // (1) dots for the columns j >= k; the owner of column k forms the reflector
+    for (int j = k + tid; j < nc; j += nt) {
+      const double* aj = A + (int64_t)j * lda;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int i = lo;
+#pragma unroll 2
+      for (; i + 3 < hi; i += 4) {
+        s0 = fma(ak[i], aj[i], s0);
+        s1 = fma(ak[i + 1], aj[i + 1], s1);
+        s2 = fma(ak[i + 2], aj[i + 2], s2);
+        s3 = fma(ak[i + 3], aj[i + 3], s3);
       }
-      for (int i = lo + lane; i < hi; i += 32) {
-        const double x = ak[i];
-#pragma unroll
-        for (int c = 0; c < CB; c++) sum[c] = fma(x, aj[c][i], sum[c]);
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-        for (int c = 0; c < CB; c++) sum[c] += __shfl_xor_sync(0xffffffffu, sum[c], o);
-      if (lane == 0) {
-#pragma unroll
-        for (int c = 0; c < CB; c++) {
-          const int j = j0 + c * nw;
-          if (j >= nc) break;
-          if (j == k) {
-            const double alpha = ak[k], xn2 = sum[c];
-            double tau = 0.0, scal = 1.0, beta = alpha;
-            if (xn2 > 0.0) {
-              beta = -copysign(sqrt(fma(alpha, alpha, xn2)), alpha);
-              tau = (beta - alpha) / beta;
-              scal = 1.0 / (alpha - beta);
-            }
-            taus[k] = tau;
-            double* pv = s_piv + 3 * (k & 1);
-            pv[0] = tau;
-            pv[1] = scal;
-            pv[2] = beta;
-          } else {
-            dots[j] = sum[c];
-            rowk[j] = aj[c][k];
-          }
+      for (; i < hi; i++) s0 = fma(ak[i], aj[i], s0);
+      const double sum = (s0 + s1) + (s2 + s3);
+      if (j == k) {
+        const double alpha = ak[k];
+        double tau = 0.0, scal = 1.0, beta = alpha;
+        if (sum > 0.0) {
+          beta = -copysign(sqrt(fma(alpha, alpha, sum)), alpha);
+          tau = (beta - alpha) / beta;
+          scal = 1.0 / (alpha - beta);
         }
+        taus[k] = tau;
+        double* pv = s_piv + 3 * (k & 1);
+        pv[0] = tau;
+        pv[1] = scal;
+        pv[2] = beta;
+      } else {
+        dots[j] = sum;
       }
     }
     __syncthreads();
@@ -180,45 +184,47 @@ __global__ void __launch_bounds__(kQrThreads) k_qr_wy(const QrJob* __restrict__ 
     const double tau = s_piv[3 * (k & 1)];
     if (tau != 0.0) {
       const double scal = s_piv[3 * (k & 1) + 1];
-      const int jnext = warp + ((k + 1 - warp + nw - 1) / nw) * nw;  // first owned column > k
-      for (int j0 = jnext; j0 < nc; j0 += CB * nw) {
-        double g[CB];
-        double* aj[CB];
+      for (int j = k + 1 + tid; j < nc; j += nt) {
+        double* __restrict__ aj = A + (int64_t)j * lda;
+        const double* __restrict__ xk = ak;
+        const double f = tau * fma(scal, dots[j], aj[k]);
+        const double g = f * scal;
+        aj[k] -= f;
+        // columns j and k never alias: stage 8 loads before the 8 stores (the compiler cannot
+        // prove it and would serialise load - fma - store per element)
+        int i = lo;
+        for (; i + 7 < hi; i += 8) {
+          double x[8], y[8];
 #pragma unroll
-        for (int c = 0; c < CB; c++) {
-          const int j = min(j0 + c * nw, nc - 1);
-          aj[c] = A + (int64_t)j * lda;
-          const double akj = rowk[j];
-          const double f = j0 + c * nw < nc ? tau * fma(scal, dots[j], akj) : 0.0;
-          g[c] = f * scal;
-          if (lane == 0 && j0 + c * nw < nc) aj[c][k] = akj - f;
-        }
-        for (int i = lo + lane; i < hi; i += 32) {
-          const double x = ak[i];
+          for (int u = 0; u < 8; u++) {
+            x[u] = xk[i + u];
+            y[u] = aj[i + u];
+          }
 #pragma unroll
-          for (int c = 0; c < CB; c++)
-            if (j0 + c * nw < nc) aj[c][i] = fma(-g[c], x, aj[c][i]);
+          for (int u = 0; u < 8; u++) aj[i + u] = fma(-g, x[u], y[u]);
         }
+        for (; i < hi; i++) aj[i] = fma(-g, xk[i], aj[i]);
       }
     }
     __syncthreads();
   }
   // finish the last column
-  if (warp == (nc - 1) % nw) {
+  {
     double* ap = A + (int64_t)(nc - 1) * lda;
     const double* pv = s_piv + 3 * ((nc - 1) & 1);
-    const int plo = stk ? nc : nc, phi = stk ? 2 * nc : m;
-    for (int i = plo + lane; i < phi; i += 32) ap[i] *= pv[1];
-    if (lane == 0) ap[nc - 1] = pv[2];
+    const int plo = nc, phi = stk ? 2 * nc : m;
+    for (int i = plo + tid; i < phi; i += nt) ap[i] *= pv[1];
+    if (tid == 0) ap[nc - 1] = pv[2];
   }
   __syncthreads();
+  QR_STAMP(2);
   // R, rank test (reading R9), V row-major with the unit diagonal made explicit
   for (int e = tid; e < nc * nc; e += nt) {
     int i = e / nc, j = e - i * nc;
     jb.R[e] = j >= i ? A[(int64_t)j * lda + i] : 0.0;
   }
-  for (int64_t e = tid; e < (int64_t)m * nc; e += nt) {
-    int i = (int)(e / nc), l = (int)(e - (int64_t)i * nc);
+  for (int e = tid; e < m * nc; e += nt) {
+    const int i = e / nc, l = e - i * nc;
     jb.V[e] = i == l ? 1.0 : (i > l ? A[(int64_t)l * lda + i] : 0.0);
   }
   if (tid == 0) {
@@ -230,6 +236,7 @@ __global__ void __launch_bounds__(kQrThreads) k_qr_wy(const QrJob* __restrict__ 
     }
     if (!(mn > 1e-13 * mx)) atomicExch(rank_flag, 1);
   }
+  QR_STAMP(3);
   // G[q][l] = (V^T V)[q][l] for q < l: column q of V is (0.., 1 at q, A[q*lda + i] for i > q),
   // so G[q][l] = A[q*lda + l] + sum_{i > l} A[q*lda + i] A[l*lda + i].  One thread per pair.
   for (int e = tid; e < nc * nc; e += nt) {
@@ -248,6 +255,7 @@ __global__ void __launch_bounds__(kQrThreads) k_qr_wy(const QrJob* __restrict__ 
     G[(int64_t)q * nc + l] = s0 + s1;
   }
   __syncthreads();
+  QR_STAMP(4);
   // forward substitution, thread per row i (reads only its own row of A, then overwrites it)
   for (int i = tid; i < m; i += nt) {
     for (int l = 0; l < nc; l++) {
@@ -255,24 +263,28 @@ __global__ void __launch_bounds__(kQrThreads) k_qr_wy(const QrJob* __restrict__ 
       double w = 0.0;
       if (tl != 0.0) {
         const double vil = i == l ? 1.0 : (i > l ? A[(int64_t)l * lda + i] : 0.0);
-        double s0 = 0.0, s1 = 0.0;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
         int q = 0;
-        for (; q + 1 < l; q += 2) {
+        for (; q + 3 < l; q += 4) {
           s0 = fma(G[(int64_t)q * nc + l], A[(int64_t)q * lda + i], s0);
           s1 = fma(G[(int64_t)(q + 1) * nc + l], A[(int64_t)(q + 1) * lda + i], s1);
+          s2 = fma(G[(int64_t)(q + 2) * nc + l], A[(int64_t)(q + 2) * lda + i], s2);
+          s3 = fma(G[(int64_t)(q + 3) * nc + l], A[(int64_t)(q + 3) * lda + i], s3);
         }
-        if (q < l) s0 = fma(G[(int64_t)q * nc + l], A[(int64_t)q * lda + i], s0);
-        w = tl * (vil - (s0 + s1));
+        for (; q < l; q++) s0 = fma(G[(int64_t)q * nc + l], A[(int64_t)q * lda + i], s0);
+        w = tl * (vil - ((s0 + s1) + (s2 + s3)));
       }
       A[(int64_t)l * lda + i] = w;   // row i of W1T, in place (entries q < l already replaced)
       jb.W1T[(int64_t)l * m + i] = w;
     }
   }
+  __syncthreads();
+  QR_STAMP(5);
 }
 
-// dynamic shared memory of k_qr_wy: taus, dots, rowk (+ A) (+ G)
+// dynamic shared memory of k_qr_wy: taus, dots (+ A) (+ G)
 inline size_t qr_smem(int m, int nc, bool a_in, bool g_in) {
-  size_t d = 3 * (size_t)nc + 1;
+  size_t d = 2 * (size_t)nc;
   if (a_in) d += (size_t)(m | 1) * nc;
   if (g_in) d += (size_t)nc * nc;
   return d * sizeof(double);
@@ -328,6 +340,14 @@ void run_qr(Ctx& c, std::vector<QrJob>& jobs, int nc, int* flag, const char* nam
       k_qr_wy<false, false><<<(unsigned)jobs.size(), kQrThreads, s0, c.stream>>>(dj.p, flag);
     }
     check_launch("k_qr_wy");
+    if (std::getenv("MLK_QR_PROFILE")) {
+      long long h[12];
+      CUDA_CHECK(cudaStreamSynchronize(c.stream));
+      CUDA_CHECK(cudaMemcpyFromSymbol(h, g_qr_prof, sizeof(h)));
+      std::fprintf(stderr,
+                   "[mlk] qr %s m=%d nc=%d jobs=%zu: copy %lld fact %lld export %lld G %lld fs %lld cycles\n", name,
+                   m_max, nc, jobs.size(), h[1] - h[0], h[2] - h[1], h[3] - h[2], h[4] - h[3], h[5] - h[4]);
+    }
   }
   std::vector<GemmDesc> gd;
   for (auto& j : jobs) {
