@@ -78,30 +78,29 @@ void make_tile_units(std::vector<TileUnit>& out, int64_t a_begin, int32_t s_a, i
     int qc = std::min(width, p_b - c0);
     int rq, nr;
     tile_split(qc, rq, nr);
-    for (int32_t r0 = 0; r0 < s_a; r0 += 32) {
-      TileUnit u;
-      u.a_begin = a_begin;
-      u.b_begin = b_begin;
-      u.s_a = s_a;
-      u.s_b = s_b;
-      u.row0 = r0;
-      u.c0 = c0;
-      u.qc = qc;
-      u.p_b = p_b;
-      u.trans = trans;
-      u.rq = rq;
-      u.nr = nr;
-      u.Wb = Wb;
-      u.ldw = ldw;
-      u.U = U;
-      u.ldu = ldu;
-      // a tensor map needs a 16-byte aligned base and a row stride that is a multiple of 16 bytes
-      u.bulk = (ldw % 2 == 0) && ((reinterpret_cast<uintptr_t>(Wb) & 15) == 0);
-      u.xmap = u.wmap = -1;
-      // FP64-slot estimate: Gram dp + kernel ~50 + contraction 8 rq per entry
-      u.cost = 32.0 * s_b * (dp + 50 + 8.0 * rq + nr);
-      out.push_back(u);
-    }
+    TileUnit u;
+    u.a_begin = a_begin;
+    u.b_begin = b_begin;
+    u.s_a = s_a;
+    u.s_b = s_b;
+    u.row0 = 0;
+    u.n_tasks = (int32_t)ceil_div(s_a, 32);
+    u.c0 = c0;
+    u.qc = qc;
+    u.p_b = p_b;
+    u.trans = trans;
+    u.rq = rq;
+    u.nr = nr;
+    u.Wb = Wb;
+    u.ldw = ldw;
+    u.U = U;
+    u.ldu = ldu;
+    // a tensor map needs a 16-byte aligned base and a row stride that is a multiple of 16 bytes
+    u.bulk = (ldw % 2 == 0) && ((reinterpret_cast<uintptr_t>(Wb) & 15) == 0);
+    u.xmap = u.wmap = -1;
+    // FP64-slot estimate per 32-row task: Gram dp + evaluation ~20 + contraction per entry
+    u.cost = 32.0 * s_b * (dp + 20 + 8.0 * rq + nr);
+    out.push_back(u);
   }
 }
 
@@ -173,7 +172,8 @@ __global__ void k_tile_aug(const double* __restrict__ Xt, int dpt, int d, int64_
 // wait on a CTA barrier inside a unit.
 template <int RQ, int FAM, int NV>
 __global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4)
-    k_tile_contract(const TileUnit* __restrict__ units, int n_units, int* __restrict__ counter,
+    k_tile_contract(const TileUnit* __restrict__ units, const int32_t* __restrict__ task_range,
+                    const int32_t* __restrict__ task_first, int n_units, int* __restrict__ counter,
                     const double* __restrict__ Pa, const double* __restrict__ Pb, int dpa, int sdp,
                     KernelParams kp, const CUtensorMap* __restrict__ maps) {
   constexpr int BN = TileCfg<RQ>::BN;
@@ -209,7 +209,9 @@ __global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4)
     __syncthreads();
     const int ui = s_unit;
     if (ui >= n_units) break;
-    const TileUnit u = units[ui];
+    const int ri = task_range[ui];
+    TileUnit u = units[ri];
+    u.row0 += 32 * (ui - task_first[ri]);
     const int64_t a0 = u.a_begin + u.row0;
     const int rows = min(32, u.s_a - u.row0);
     // a tile (rows x dpa); rows past the range are zero (their outputs are discarded)
@@ -421,7 +423,17 @@ struct AugArgs {
   const double* Pb;
   int dpa, sdp;
   const CUtensorMap* maps;
+  const int32_t* task_range;  // task -> range (relative to the class), per class
+  const int32_t* task_first;  // range -> first task (relative to the class)
 };
+
+// task -> range map of one class: ranges r own tasks first[r] .. first[r] + n_tasks[r] - 1
+__global__ void k_expand_tasks(const int32_t* __restrict__ first, const int32_t* __restrict__ ntask, int n_ranges,
+                               int32_t* __restrict__ task_range) {
+  const int r = blockIdx.x;
+  if (r >= n_ranges) return;
+  for (int t = threadIdx.x; t < ntask[r]; t += blockDim.x) task_range[first[r] + t] = r;
+}
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
@@ -460,6 +472,7 @@ int class_bn(int rq) {
 
 template <int RQ, int FAM, int NV = 0>
 void launch_class(Ctx& c, const AugArgs& ag, const KernelParams& kp, const TileUnit* units, int n, int* counter) {
+  // units = this class's ranges; n = its tasks (ag.task_range / ag.task_first are class-relative)
   constexpr int BN = TileCfg<RQ>::BN;
   size_t smem = sizeof(double) * (size_t)(32 * ag.sdp + TileCfg<RQ>::NST * stage_doubles(RQ, BN, ag.sdp));
   auto fn = k_tile_contract<RQ, FAM, NV>;
@@ -473,7 +486,8 @@ void launch_class(Ctx& c, const AugArgs& ag, const KernelParams& kp, const TileU
     smem_set = smem;
   }
   int grid = std::min<int64_t>(n, (int64_t)num_sms(c.device) * occ);
-  fn<<<grid, 128, smem, c.stream>>>(units, n, counter, ag.Pa, ag.Pb, ag.dpa, ag.sdp, kp, ag.maps);
+  fn<<<grid, 128, smem, c.stream>>>(units, ag.task_range, ag.task_first, n, counter, ag.Pa, ag.Pb, ag.dpa, ag.sdp, kp,
+                                    ag.maps);
   check_launch("k_tile_contract");
 }
 
@@ -505,15 +519,36 @@ void launch_fam(Ctx& c, const AugArgs& ag, const KernelParams& kp, int rq, const
 void run_tile_contract(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, std::vector<TileUnit>& units,
                        const char* name) {
   if (units.empty()) return;
-  // group by class, largest cost first inside a class
-  std::stable_sort(units.begin(), units.end(), [](const TileUnit& a, const TileUnit& b) {
+  // ranges grouped by class, largest per-task cost first inside a class
+  std::vector<int32_t> order(units.size());
+  for (size_t i = 0; i < units.size(); i++) order[i] = (int32_t)i;
+  std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
+    const TileUnit& a = units[x];
+    const TileUnit& b = units[y];
     if (a.rq != b.rq) return a.rq > b.rq;
     return a.cost > b.cost;
   });
+  std::vector<TileUnit> ranges(units.size());
+  for (size_t i = 0; i < order.size(); i++) ranges[i] = units[order[i]];
+  // classes, task prefixes (class-relative)
   std::vector<int> starts;
-  for (size_t i = 0; i < units.size(); i++)
-    if (i == 0 || units[i].rq != units[i - 1].rq) starts.push_back((int)i);
-  starts.push_back((int)units.size());
+  for (size_t i = 0; i < ranges.size(); i++)
+    if (i == 0 || ranges[i].rq != ranges[i - 1].rq) starts.push_back((int)i);
+  starts.push_back((int)ranges.size());
+  std::vector<int32_t> first(ranges.size()), ntask(ranges.size());
+  std::vector<int64_t> class_task0(starts.size(), 0);
+  int64_t tasks_total = 0;
+  for (size_t g = 0; g + 1 < starts.size(); g++) {
+    class_task0[g] = tasks_total;
+    int32_t acc = 0;
+    for (int i = starts[g]; i < starts[g + 1]; i++) {
+      first[i] = acc;
+      ntask[i] = ranges[i].n_tasks;
+      acc += ranges[i].n_tasks;
+    }
+    tasks_total += acc;
+  }
+  class_task0.back() = tasks_total;
   DevBuf<int> counters(starts.size(), c.stream);
   counters.zero();
   // augmented, pre-scaled coordinates (k_tile_aug); the smem row stride avoids 2-way bank
@@ -537,10 +572,10 @@ void run_tile_contract(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, s
       idx[key] = k;
       return k;
     };
-    const TileUnit* prev = nullptr;  // consecutive units mostly share W_b: skip the lookup
-    for (auto& u : units) {
-      if (!u.bulk) continue;
+    const TileUnit* prev = nullptr;  // consecutive ranges mostly share W_b: skip the lookup
+    for (auto& u : ranges) {
       u.wrows = u.rq > 0 ? 8 * u.rq + u.nr : 8;
+      if (!u.bulk) continue;
       if (prev && prev->Wb == u.Wb && prev->rq == u.rq && prev->nr == u.nr && prev->p_b == u.p_b &&
           prev->s_b == u.s_b && prev->ldw == u.ldw) {
         u.xmap = prev->xmap;
@@ -556,16 +591,29 @@ void run_tile_contract(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, s
   DevBuf<CUtensorMap> maps_d(std::max<size_t>(maps.size(), 1), c.stream);
   maps_d.upload(maps);
   ag.maps = maps_d.p;
-  DevBuf<TileUnit> du(units.size(), c.stream);
-  du.upload(units);
+  DevBuf<TileUnit> du(ranges.size(), c.stream);
+  du.upload(ranges);
+  DevBuf<int32_t> first_d(ranges.size(), c.stream), ntask_d(ranges.size(), c.stream);
+  first_d.upload(first);
+  ntask_d.upload(ntask);
+  DevBuf<int32_t> task_range((size_t)std::max<int64_t>(tasks_total, 1), c.stream);
   TimedLaunch tl(c, name);
   k_tile_aug<<<(unsigned)ceil_div(tree->n, 256), 256, 0, c.stream>>>(tree->Xt.p, tree->d_pad, tree->d, tree->n,
                                                                      kp.scale, aug.p, aug.p + (size_t)tree->n * ag.dpa,
                                                                      ag.dpa);
   check_launch("k_tile_aug");
   for (size_t g = 0; g + 1 < starts.size(); g++) {
-    int s0 = starts[g], n = starts[g + 1] - starts[g];
-    int rq = units[s0].rq;
+    const int s0 = starts[g], nr_ = starts[g + 1] - starts[g];
+    k_expand_tasks<<<(unsigned)nr_, 128, 0, c.stream>>>(first_d.p + s0, ntask_d.p + s0, nr_,
+                                                        task_range.p + class_task0[g]);
+    check_launch("k_expand_tasks");
+  }
+  for (size_t g = 0; g + 1 < starts.size(); g++) {
+    const int s0 = starts[g];
+    const int n = (int)(class_task0[g + 1] - class_task0[g]);
+    const int rq = ranges[s0].rq;
+    ag.task_range = task_range.p + class_task0[g];
+    ag.task_first = first_d.p + s0;
     switch (kp.family) {
       case MLK_MATERN_12: launch_fam<MLK_MATERN_12>(c, ag, kp, rq, du.p + s0, n, counters.p + g); break;
       case MLK_MATERN_32: launch_fam<MLK_MATERN_32>(c, ag, kp, rq, du.p + s0, n, counters.p + g); break;

@@ -13,7 +13,8 @@ namespace mlk {
 struct TileUnit {
   int64_t a_begin, b_begin;  // first tree position of the a / b point ranges
   int32_t s_a, s_b;          // points in the ranges
-  int32_t row0;              // first a row handled by this unit (multiple of 32)
+  int32_t row0;              // first a row of the range (tasks cover row0 + 32 i)
+  int32_t n_tasks;           // 32-row CTA tasks of the range: ceil((s_a - row0) / 32)
   int32_t c0, qc;            // first column of W_b rows handled, and how many (<= 8 RQ)
   int32_t p_b;               // rows of W_b
   int32_t trans;             // 0: U[r * ldu + c0 + l]; 1: U[(c0 + l) * ldu + r]
