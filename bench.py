@@ -251,6 +251,9 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         step(X_d, dirs_d)
+        # N > 1: the all-gather / allreduce run on NCCL's stream behind torch's current stream;
+        # the end event must follow them
+        stream.wait_stream(torch.cuda.current_stream(dev))
         e1.record(stream)
         e1.synchronize()
         step_ms.append(e0.elapsed_time(e1))

@@ -270,6 +270,40 @@ def test_cfg2_full_size_sampled_blocks(mlk, ctx):
         assert e <= TOL_BLOCK, (k, a, b, e)
 
 
+@pytest.mark.parametrize("name,max_entries", [("cfg3", 2 ** 22), ("cfg4", 2 ** 20)])
+def test_full_size_sampled_blocks(mlk, ctx, name, max_entries):
+    """cfg3 / cfg4 at BASELINE size in the bench's launch configuration: tree bit-exact, the
+    BSR structure bit-exact against the oracle's pair list (tests/golden/pairs_<cfg>.npz,
+    written by tools/make_golden_pairs.py from oracle/ only), and seeded sampled blocks
+    (leaf self blocks, random admitted pairs) recomputed one by one by the oracle."""
+    import os
+    inp = wl.make(name)
+    c = inp["cfg"]
+    X = inp["X"]
+    g, o = _tree_both(mlk, ctx, X, c["leaf"], c["tree"], inp["dirs"])
+    _check_tree(g, o)
+    gb = mlk.build_basis(ctx, g, c["w"])
+    ob = OB.build_basis(X, o, c["w"])
+    gold = np.load(os.path.join(os.path.dirname(__file__), "golden", "pairs_%s.npz" % name))
+    pairs = [tuple(int(v) for v in p) for p in gold["pairs"]]
+    kern = wl.kernel_dict(c)
+    cw = mlk.assemble_cw(ctx, g, gb, kern, dict(mode=c["pairs"], tau=c["tau"]))
+    got = cw.export()
+    _, _, brow_ptr, bcol, val_off = OAs.bsr_structure(ob, pairs)
+    assert np.array_equal(got["brow_ptr"], brow_ptr) and np.array_equal(got["bcol"], bcol)
+    assert np.array_equal(got["val_off"], val_off)
+    size = lambda q: int(o.end[q] - o.begin[q])
+    rng = np.random.default_rng([0, 3])
+    selfs = [k for k, (a, b) in enumerate(pairs) if a == b and o.is_leaf[a]]
+    small = [k for k, (a, b) in enumerate(pairs) if a != b and size(a) * size(b) <= max_entries]
+    idx = sorted(set(rng.choice(selfs, 6, replace=False).tolist()) | set(rng.choice(small, 14, replace=False).tolist()))
+    for k in idx:
+        a, b = pairs[k]
+        ref = OAs.block(X, o, ob, kern, a, b).ravel()
+        e = np.linalg.norm(got["values"][val_off[k]:val_off[k + 1]] - ref) / np.linalg.norm(ref)
+        assert e <= TOL_BLOCK, (name, k, a, b, e)
+
+
 def test_assembly_deterministic(mlk, ctx):
     X, dirs = _setup(4096, 10, 128, 1)
     g = mlk.build_tree(ctx, X, 128, 1, dirs)
