@@ -86,65 +86,81 @@ def dist_env():
 
 
 # --------------------------------------------------------------------------- reference arm
-def oracle_sample(cfg_name, budget_s, seed_tag=0):
-    """The oracle (as it stands) on a bounded, seeded sample of the workload's admitted blocks.
-    Returns (pairs/s, description, cores)."""
-    from oracle import admission as OA
-    from oracle import assemble as OAs
-    from oracle import basis as OB
-    from oracle import tree as OT
+METRIC = "C_W assembly covariance pairs/s (FP64 TFLOP/s and % of FP64 peak in 'fp64')"
 
-    inp = wl.make(cfg_name)
-    c = inp["cfg"]
-    X = inp["X"]
-    tr = OT.build_tree(X, c["leaf"], c["tree"], inp["dirs"])
-    B = OB.build_basis(X, tr, c["w"])
-    pairs = OA.admitted_pairs(X, tr, B, c["pairs"], c["tau"])
-    kern = wl.kernel_dict(c)
-    rng = np.random.default_rng([0, 3, seed_tag])
-    order = rng.permutation(len(pairs))
-    ent = 0.0
-    nb = 0
-    t0 = time.perf_counter()
-    for k in order:
-        a, b = pairs[k]
-        OAs.block(X, tr, B, kern, a, b)
-        ent += float(tr.end[a] - tr.begin[a]) * float(tr.end[b] - tr.begin[b])
-        nb += 1
-        if time.perf_counter() - t0 >= budget_s:
-            break
-    dt = time.perf_counter() - t0
-    cores = len(os.sched_getaffinity(0))
-    try:
-        from threadpoolctl import threadpool_info
-        blas = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
-    except Exception:
-        blas = None
-    desc = ("oracle blocks W_a C W_b^T (direct differences + NumPy matmul) for %d of %d admitted %s "
-            "blocks in seeded random order, %.1f s budget; tree/basis/admission untimed; BLAS threads %s"
-            % (nb, len(pairs), cfg_name, budget_s, blas))
-    return ent / dt, desc, cores, blas
+
+def config_dict(name, ws):
+    c = wl.CONFIGS[name]
+    return {"workload": name, "n": c["n"], "d": c["d"], "w": c["w"], "leaf": c["leaf"], "family": c["family"],
+            "rho": c["rho"], "tau": c["tau"], "pairs_mode": c["pairs"], "parallelism": "pairs%d" % ws,
+            "l2": "flushed (512 MB write) between timed steps",
+            "step": "build_tree + build_basis + assemble_cw(+all-gather) + cw_matvec EXACT nvec=1"}
+
+
+class OracleSampler:
+    """The oracle (as it stands) on bounded, seeded samples of a workload's admitted blocks.
+    Tree, basis and admission are built once (untimed); each sample times oracle blocks
+    W_a C(X_a, X_b) W_b^T in seeded random order until the time budget is spent."""
+
+    def __init__(self, cfg_name):
+        from oracle import admission as OA
+        from oracle import basis as OB
+        from oracle import tree as OT
+
+        inp = wl.make(cfg_name)
+        c = inp["cfg"]
+        self.name = cfg_name
+        self.X = inp["X"]
+        self.tr = OT.build_tree(self.X, c["leaf"], c["tree"], inp["dirs"])
+        self.B = OB.build_basis(self.X, self.tr, c["w"])
+        self.pairs = OA.admitted_pairs(self.X, self.tr, self.B, c["pairs"], c["tau"])
+        self.kern = wl.kernel_dict(c)
+
+    def sample(self, budget_s, seed_tag=0):
+        from oracle import assemble as OAs
+
+        tr = self.tr
+        order = np.random.default_rng([0, 3, seed_tag]).permutation(len(self.pairs))
+        ent = 0.0
+        nb = 0
+        t0 = time.perf_counter()
+        for k in order:
+            a, b = self.pairs[k]
+            OAs.block(self.X, tr, self.B, self.kern, a, b)
+            ent += float(tr.end[a] - tr.begin[a]) * float(tr.end[b] - tr.begin[b])
+            nb += 1
+            if time.perf_counter() - t0 >= budget_s:
+                break
+        dt = time.perf_counter() - t0
+        cores = len(os.sched_getaffinity(0))
+        try:
+            from threadpoolctl import threadpool_info
+            blas = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+        except Exception:
+            blas = None
+        desc = ("oracle blocks W_a C W_b^T (direct differences + NumPy matmul) for %d of %d admitted %s "
+                "blocks in seeded random order, %.1f s budget; tree/basis/admission built once, untimed; "
+                "BLAS threads %s" % (nb, len(self.pairs), self.name, budget_s, blas))
+        return ent / dt, desc, cores
 
 
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
+    sampler = OracleSampler(args.config)
+    for w in range(args.warmup):
+        sampler.sample(min(3.0, args.ref_budget), seed_tag=100 + w)
     vals = []
-    for _ in range(args.warmup):
-        oracle_sample(args.config, min(5.0, args.ref_budget))
     desc = cores = None
     for s in range(args.steps):
-        v, desc, cores, blas = oracle_sample(args.config, args.ref_budget, seed_tag=s + 1)
+        v, desc, cores = sampler.sample(args.ref_budget, seed_tag=s + 1)
         vals.append(v)
     value = float(np.mean(vals))
-    c = wl.CONFIGS[args.config]
     line = {
-        "impl": "reference", "metric": "C_W assembly covariance pairs/s", "value": value,
+        "impl": "reference", "metric": METRIC, "value": value,
         "unit": "covariance pairs/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "higher_is_better": True, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "n": c["n"], "d": c["d"], "w": c["w"], "leaf": c["leaf"],
-                   "tau": c["tau"]},
+        "higher_is_better": True, "dtype": "f64", "data": "synthetic", "config": config_dict(args.config, ws),
         "cpu_baseline": {"value": value, "unit": "covariance pairs/s", "cores": cores, "kind": "oracle",
                          "sample": desc},
         "e2e": {"value": value, "unit": "covariance pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -162,7 +178,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--impl", default="ours")
-    ap.add_argument("--ref-budget", type=float, default=15.0)
+    ap.add_argument("--ref-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     args = ap.parse_args()
@@ -309,17 +325,13 @@ def main():
                      ("search", "assemble_tile_contract", "assemble_wa_gemm")) / args.steps
         cpu = None
         if not args.no_cpu_baseline and ws == 1:
-            v, desc, cores, blas = oracle_sample(args.config, args.ref_budget)
+            v, desc, cores = OracleSampler(args.config).sample(args.ref_budget)
             cpu = {"value": v, "unit": "covariance pairs/s", "cores": cores, "kind": "oracle", "sample": desc}
         line = {
-            "metric": "C_W assembly covariance pairs/s (FP64 TFLOP/s and % of FP64 peak in 'fp64')",
+            "metric": METRIC,
             "value": value, "unit": "covariance pairs/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.config, "n": c["n"], "d": c["d"], "w": c["w"], "leaf": c["leaf"],
-                       "family": c["family"], "rho": c["rho"], "tau": c["tau"], "pairs_mode": c["pairs"],
-                       "parallelism": "pairs%d" % ws, "l2": "flushed (512 MB write) between timed steps",
-                       "step": "build_tree + build_basis + assemble_cw(+all-gather) + cw_matvec EXACT nvec=1"},
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_dict(args.config, ws),
             "fp64": {"assembly_flops_per_step": flops, "tflops_step": flops / (ms_per_step * 1e-3) / 1e12,
                      "tflops_assembly": flops / (asm_ms * 1e-3) / 1e12 if asm_ms > 0 else None,
                      "pct_of_peak_step": 100.0 * flops / (ms_per_step * 1e-3) / 1e12 / peak,

@@ -117,6 +117,13 @@ mlk_status mlk_tree_export(mlk_tree tree, int64_t* perm, int64_t* begin, int64_t
  * internal: [R_L; R_R] = Q R (2M x M), Phi = Q_1^T (Phi_L (+) Phi_R), W = Q_2^T (...).
  * M = C(d + w, w).  L = Phi_root (R10).  MLK_ERR_RANK_DEFICIENT if a leaf has fewer than M
  * points or |R_kk| <= 1e-13 max_i |R_ii| in any cell (R9).
+ * Asynchrony: the leaf level is factored before the call returns (its rank test is the one
+ * that can fail: [R_L; R_R] has full column rank whenever R_L does); the merge levels -- a
+ * latency-bound chain of small QRs -- are left running on the context's auxiliary stream so
+ * they overlap the caller's next host work (e.g. the admission search and planning of
+ * mlk_assemble_cw).  Every call that reads the blocks (mlk_basis_export of W / Phi / L,
+ * mlk_apply_wt, mlk_apply_w, mlk_assemble_cw, mlk_cw_matvec EXACT) waits for them first and
+ * reports a numerically rank-deficient merge there (MLK_ERR_RANK_DEFICIENT).
  */
 mlk_status mlk_build_basis(mlk_ctx ctx, mlk_tree tree, int32_t w, mlk_basis* out);
 void mlk_basis_free(mlk_basis basis); /* NULL-safe */

@@ -21,10 +21,16 @@
   }                                                                        \
   return MLK_OK;
 
+struct mlk_basis_s;
 namespace mlk {
 void partition_lpt(const double* cost, int64_t n, int nranks, int32_t* owner);
 void shard_plan(const int64_t* val_off, const int32_t* owner, int64_t n, int nranks, int64_t* shard_off,
                 int64_t* shard_len);
+
+// make the context stream wait until the basis's asynchronous merge levels have completed;
+// the first call also synchronises and reports a rank-deficient merge (MLK_ERR_RANK_DEFICIENT)
+void basis_wait(Ctx& c, const mlk_basis_s* B);
+void basis_sync(const mlk_basis_s* B);
 
 // padded coordinate count for the DMMA k = 4 Gram steps
 inline int pad4(int d) { return (d + 3) / 4 * 4; }
@@ -64,6 +70,11 @@ struct mlk_basis_s {
   std::vector<int64_t> phi_off;    // node -> offset of Phi block in Phi
   mlk::DevBuf<double> W;           // all W blocks, C_W order, each p x |node| row-major
   mlk::DevBuf<double> Phi;         // all Phi blocks, M x |node| row-major
+  // the merge levels run asynchronously on the context's auxiliary stream; `ready` marks
+  // their completion and consumers wait on it (mlk::basis_wait), checking merge_flag once
+  cudaEvent_t ready = nullptr;
+  mlk::DevBuf<int> merge_flag;
+  mutable bool ready_checked = false;
 };
 
 struct mlk_cw_s {

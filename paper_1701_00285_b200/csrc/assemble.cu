@@ -171,7 +171,7 @@ std::vector<std::pair<int, int>> admitted_pairs(Ctx& c, const mlk_tree_s* tree, 
       std::vector<int64_t> off(t + 2, 0);
       for (int L = 0; L <= t; L++) off[L + 1] = off[L] + (int64_t)init.size() * ((int64_t)1 << L);
       DevBuf<SearchItem> items(off[t + 1], st);
-      CUDA_CHECK(cudaMemcpyAsync(items.p, init.data(), init.size() * sizeof(SearchItem), cudaMemcpyHostToDevice, st));
+      upload_async(items.p, init.data(), init.size() * sizeof(SearchItem), st);
       DevBuf<int2> pr(off[t + 1], st);
       std::vector<int> cnt0(t + 3, 0);
       cnt0[0] = (int)init.size();
@@ -476,6 +476,8 @@ mlk_status mlk_assemble_cw(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const ml
   };
 
   trace.mark("plan");
+  basis_wait(c, B);  // the basis merge levels ran on the auxiliary stream during the search and planning
+  trace.mark("basis_wait");
   if (dd) {
     std::vector<std::array<int64_t, 8>> jobs;
     for (int64_t i = 0; i < npc; i++) {

@@ -367,6 +367,22 @@ void run_qr(Ctx& c, std::vector<QrJob>& jobs, int nc, int* flag, const char* nam
 }  // namespace
 }  // namespace mlk
 
+namespace mlk {
+void basis_sync(const mlk_basis_s* B) {
+  if (!B->ready || B->ready_checked) return;
+  CUDA_CHECK(cudaEventSynchronize(B->ready));
+  int f = 0;
+  CUDA_CHECK(cudaMemcpy(&f, B->merge_flag.p, sizeof(int), cudaMemcpyDeviceToHost));
+  B->ready_checked = true;
+  if (f) throw Error(MLK_ERR_RANK_DEFICIENT, "merged moment matrix is rank deficient (|R_kk| <= 1e-13 max|R_ii|)");
+}
+
+void basis_wait(Ctx& c, const mlk_basis_s* B) {
+  basis_sync(B);
+  if (B->ready) CUDA_CHECK(cudaStreamWaitEvent(c.stream, B->ready, 0));
+}
+}  // namespace mlk
+
 using namespace mlk;
 
 extern "C" {
@@ -482,9 +498,31 @@ mlk_status mlk_build_basis(mlk_ctx ctx, mlk_tree tree, int32_t w, mlk_basis* out
     run_qr(c, qj, M, flag.p, "basis_leaf_qr");
   }
   trace.mark("leaves");
-  // ---- internal levels, bottom-up
-  DevBuf<double> Qt;
-  DevBuf<double> Ast;
+  {
+    auto fl = flag.download(1);
+    if (fl[0]) throw Error(MLK_ERR_RANK_DEFICIENT, "moment matrix is rank deficient (|R_kk| <= 1e-13 max|R_ii|)");
+  }
+  trace.mark("leaf_check");
+  // ---- internal levels, bottom-up, on the auxiliary stream: the call returns while they run
+  // ([R_L; R_R] has full column rank whenever R_L does, so the synchronous leaf check above is
+  // the one that can fail; merge_flag re-checks numerically when the basis is first used)
+  if (!c.aux_stream) CUDA_CHECK(cudaStreamCreateWithFlags(&c.aux_stream, cudaStreamNonBlocking));
+  CUDA_CHECK(cudaEventCreateWithFlags(&B->ready, cudaEventDisableTiming));
+  CUDA_CHECK(cudaEventRecord(B->ready, st));
+  CUDA_CHECK(cudaStreamWaitEvent(c.aux_stream, B->ready, 0));
+  const cudaStream_t main_stream = st;
+  st = c.aux_stream;
+  c.stream = st;  // run_qr / gemm_batched / TimedLaunch use the context stream
+  struct RestoreStream {
+    Ctx& c;
+    cudaStream_t s;
+    ~RestoreStream() { c.stream = s; }
+  } restore{c, main_stream};
+  B->merge_flag.alloc(1, st);
+  B->merge_flag.zero();
+  Rbuf.s = st;  // freed behind the merges
+  DevBuf<double> Qt(0, st);
+  DevBuf<double> Ast(0, st);
   for (int dep = tree->t - 1; dep >= 0; dep--) {
     std::vector<int> cellsq;
     for (int q = (1 << dep) - 1; q < (2 << dep) - 1; q++)
@@ -517,7 +555,9 @@ mlk_status mlk_build_basis(mlk_ctx ctx, mlk_tree tree, int32_t w, mlk_basis* out
       k_stack_r<<<(unsigned)nc, 256, 0, st>>>(sjd.p, M);
       check_launch("k_stack_r");
     }
-    run_qr(c, qj, M, flag.p, "basis_merge_qr");
+    trace.mark("lvl_stack");
+    run_qr(c, qj, M, B->merge_flag.p, "basis_merge_qr");
+    trace.mark("lvl_qr");
     // Phi_q / W_q = (Q^T)[rows, cols of child] x Phi_child
     std::vector<GemmDesc> gd;
     for (size_t i = 0; i < nc; i++) {
@@ -538,15 +578,14 @@ mlk_status mlk_build_basis(mlk_ctx ctx, mlk_tree tree, int32_t w, mlk_basis* out
       }
     }
     gemm_batched(c, gd, "basis_transfer_gemm");
+    trace.mark("lvl_gemm");
   }
   trace.mark("levels");
-  auto fl = flag.download(1);
-  trace.mark("sync");
-  if (fl[0]) throw Error(MLK_ERR_RANK_DEFICIENT, "moment matrix is rank deficient (|R_kk| <= 1e-13 max|R_ii|)");
-  CUDA_CHECK(cudaStreamSynchronize(st));
+  CUDA_CHECK(cudaEventRecord(B->ready, st));
   *out = B.release();
   MLK_API_END
 }
+
 
 void mlk_basis_free(mlk_basis basis) {
   if (!basis) return;
@@ -555,6 +594,8 @@ void mlk_basis_free(mlk_basis basis) {
   cudaDeviceSynchronize();
   basis->W.s = nullptr;
   basis->Phi.s = nullptr;
+  basis->merge_flag.s = nullptr;
+  if (basis->ready) cudaEventDestroy(basis->ready);
   delete basis;
 }
 
@@ -572,6 +613,8 @@ mlk_status mlk_basis_export(mlk_basis basis, int32_t* cells, int64_t* cell_row_o
   MLK_API_BEGIN
   MLK_REQUIRE(basis, "basis is NULL");
   CUDA_CHECK(cudaSetDevice(basis->device));
+  // cells / row offsets are host-side; only the device blocks wait for the merge levels
+  if (node >= 0 || L) basis_sync(basis);
   const mlk_tree_s* tree = basis->tree;
   if (cells) std::copy(basis->cells.begin(), basis->cells.end(), cells);
   if (cell_row_off) std::copy(basis->row_off.begin(), basis->row_off.end(), cell_row_off);

@@ -8,7 +8,9 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <deque>
 #include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -62,6 +64,7 @@ struct Ctx {
   // once per context, not per call)
   int64_t free_at_first_use = -1;
   cudaStream_t copy_stream = nullptr;  // mlk_cw_export_async (created on first use)
+  cudaStream_t aux_stream = nullptr;   // asynchronous basis merge levels (created on first use)
   cudaEvent_t copy_ready = nullptr;
   int64_t scratch_budget_bytes();
 
@@ -97,6 +100,13 @@ inline void check_launch(const char* name) {
   if (e != cudaSuccess) throw Error(MLK_ERR_CUDA, std::string("launch ") + name + ": " + cudaGetErrorString(e));
 }
 
+// Host -> device copy that returns immediately: small transfers are staged through a
+// process-wide pinned ring buffer (a chunk is reused only after the event recorded behind its
+// copy has completed), large ones go straight to cudaMemcpyAsync.  Pageable cudaMemcpyAsync
+// would block the host until the stream reaches the copy.  dst: device memory of the current
+// device; src: host memory.
+void upload_async(void* dst, const void* src, size_t bytes, cudaStream_t s);
+
 // Stream-ordered device buffer.
 template <typename T>
 struct DevBuf {
@@ -115,7 +125,7 @@ struct DevBuf {
     if (n) CUDA_CHECK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
   }
   void upload(const T* host, size_t count) {
-    if (count) CUDA_CHECK(cudaMemcpyAsync(p, host, count * sizeof(T), cudaMemcpyHostToDevice, s));
+    if (count) upload_async(p, host, count * sizeof(T), s);
   }
   void upload(const std::vector<T>& v) {
     if (v.size() > n) alloc(v.size(), s);

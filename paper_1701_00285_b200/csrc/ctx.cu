@@ -33,6 +33,69 @@ int num_sms(int device) {
   return v;
 }
 
+namespace {
+struct PinnedRing {
+  static constexpr size_t kCap = (size_t)64 << 20;
+  char* base = nullptr;
+  size_t head = 0;
+  int device = -1;
+  struct Chunk {
+    size_t off, len;
+    cudaEvent_t ev;
+  };
+  std::deque<Chunk> live;
+  std::vector<cudaEvent_t> pool;
+  std::mutex mu;
+};
+PinnedRing g_ring[64];
+}  // namespace
+
+void upload_async(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  int dev = 0;
+  CUDA_CHECK(cudaGetDevice(&dev));
+  if (bytes == 0) return;
+  if (bytes > PinnedRing::kCap / 4 || dev < 0 || dev >= 64) {
+    CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
+    return;
+  }
+  PinnedRing& r = g_ring[dev];
+  std::lock_guard<std::mutex> lock(r.mu);
+  if (!r.base) {
+    CUDA_CHECK(cudaHostAlloc((void**)&r.base, PinnedRing::kCap, cudaHostAllocPortable));
+    r.device = dev;
+  }
+  const size_t len = (bytes + 255) & ~(size_t)255;
+  if (r.head + len > PinnedRing::kCap) r.head = 0;
+  // the chunks overlapping [head, head + len) are the oldest live ones: wait for their copies
+  while (!r.live.empty()) {
+    const auto& ch = r.live.front();
+    const bool overlap = ch.off < r.head + len && r.head < ch.off + ch.len;
+    if (!overlap) break;
+    CUDA_CHECK(cudaEventSynchronize(ch.ev));
+    r.pool.push_back(ch.ev);
+    r.live.pop_front();
+  }
+  // retire completed chunks at the front so the deque stays short
+  while (!r.live.empty() && cudaEventQuery(r.live.front().ev) == cudaSuccess) {
+    r.pool.push_back(r.live.front().ev);
+    r.live.pop_front();
+  }
+  cudaGetLastError();  // cudaEventQuery's cudaErrorNotReady is not an error here
+  char* stage = r.base + r.head;
+  std::memcpy(stage, src, bytes);
+  CUDA_CHECK(cudaMemcpyAsync(dst, stage, bytes, cudaMemcpyHostToDevice, s));
+  cudaEvent_t ev;
+  if (!r.pool.empty()) {
+    ev = r.pool.back();
+    r.pool.pop_back();
+  } else {
+    CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  }
+  CUDA_CHECK(cudaEventRecord(ev, s));
+  r.live.push_back({r.head, len, ev});
+  r.head += len;
+}
+
 int64_t Ctx::scratch_budget_bytes() {
   if (free_at_first_use < 0) {
     size_t freeb = 0, totalb = 0;
@@ -150,6 +213,10 @@ void mlk_ctx_destroy(mlk_ctx ctx) {
     cudaEventDestroy(p.b);
   }
   for (auto e : ctx->c.event_pool) cudaEventDestroy(e);
+  if (ctx->c.aux_stream) {
+    cudaStreamSynchronize(ctx->c.aux_stream);
+    cudaStreamDestroy(ctx->c.aux_stream);
+  }
   if (ctx->c.copy_stream) {
     cudaStreamSynchronize(ctx->c.copy_stream);
     cudaStreamDestroy(ctx->c.copy_stream);

@@ -184,6 +184,7 @@ mlk_status mlk_apply_wt(mlk_ctx ctx, mlk_basis basis, const double* v, double* a
   const mlk_tree_s* tree = basis->tree;
   DevIn<double> vin(v, (size_t)nvec * basis->dim, c.stream);
   DevOut<double> aout(a, (size_t)nvec * tree->n, c.stream);
+  basis_wait(c, basis);
   apply_wt_dev(c, tree, basis, vin.p, aout.p, nvec);
   aout.finish();
   MLK_API_END
@@ -198,6 +199,7 @@ mlk_status mlk_apply_w(mlk_ctx ctx, mlk_basis basis, const double* b, double* y,
   const mlk_tree_s* tree = basis->tree;
   DevIn<double> bin(b, (size_t)nvec * tree->n, c.stream);
   DevOut<double> yout(y, (size_t)nvec * basis->dim, c.stream);
+  basis_wait(c, basis);
   apply_w_dev(c, tree, basis, bin.p, yout.p, nvec);
   yout.finish();
   MLK_API_END
@@ -233,6 +235,7 @@ mlk_status mlk_cw_matvec(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const mlk_
   if (mode == MLK_MATVEC_EXACT) {
     check_kernel(kernel);
     DevBuf<double> a((size_t)nvec * tree->n, c.stream), b((size_t)nvec * tree->n, c.stream);
+    basis_wait(c, basis);
     apply_wt_dev(c, tree, basis, vin.p, a.p, nvec);
     cov_matvec_dev(c, tree, *kernel, a.p, b.p, nvec);
     apply_w_dev(c, tree, basis, b.p, yout.p, nvec);
