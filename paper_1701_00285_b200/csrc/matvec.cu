@@ -3,6 +3,7 @@
 // in place of a wavelet block; steps (1), (3) and the BSR product are HBM-bound passes over
 // the stored W blocks / BSR values with a fixed summation order (deterministic).
 #include <algorithm>
+#include <cstdlib>
 
 #include "api.cuh"
 #include "tile.cuh"
@@ -144,21 +145,99 @@ void apply_w_dev(Ctx& c, const mlk_tree_s* tree, const mlk_basis_s* B, const dou
   check_launch("k_apply_w");
 }
 
-// b = C a for this rank's rows (others zero); a, b device, nvec x n
+// Symmetric C a column partials: tile I (of this rank's t0..t1-1) holds 4 (warp) x nvec rows
+// of n - 32 I columns starting at column 32 I, at offset 4 nvec sum_{I' < I} (n - 32 I').
+// Two fixed-order levels: tmp[l][c][j] = sum over the tiles of chunk c (kColChunk tiles) and
+// the 4 warps, then b[l][j] += sum over chunks c in order.  Deterministic.
+constexpr int kColChunk = 64;
+__device__ __forceinline__ int64_t colpart_off(int64_t I, int64_t t0, int64_t n, int nvec) {
+  return 4 * (int64_t)nvec * ((I - t0) * n - 16 * (I * (I - 1) - t0 * (t0 - 1)));
+}
+
+__global__ void k_colpart_chunks(const double* __restrict__ colpart, int64_t t0, int64_t t1, int64_t n, int nvec,
+                                 int nchunks, double* __restrict__ tmp) {
+  const int64_t j = 32 * t0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int c = blockIdx.y, l = blockIdx.z;
+  if (j >= n) return;
+  const int64_t i0 = t0 + (int64_t)c * kColChunk;
+  const int64_t i1 = std::min<int64_t>({t1, i0 + kColChunk, j / 32 + 1});
+  double s = 0.0;
+  for (int64_t I = i0; I < i1; I++) {
+    const int64_t w = n - 32 * I, base = colpart_off(I, t0, n, nvec) + (j - 32 * I);
+#pragma unroll
+    for (int wp = 0; wp < 4; wp++) s += colpart[base + ((int64_t)wp * nvec + l) * w];
+  }
+  tmp[((int64_t)l * nchunks + c) * n + j] = s;
+}
+
+__global__ void k_colpart_final(const double* __restrict__ tmp, int64_t j0, int64_t n, int nchunks,
+                                double* __restrict__ b) {
+  const int64_t j = j0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int l = blockIdx.y;
+  if (j >= n) return;
+  double s = 0.0;
+  for (int c = 0; c < nchunks; c++) s += tmp[((int64_t)l * nchunks + c) * n + j];
+  b[(int64_t)l * n + j] += s;
+}
+
+// b = C a for this rank's rows (others zero); a, b device, nvec x n.  Up to 4 vectors use the
+// symmetric kernel (each covariance entry evaluated once for the pair (i, j), i <= j) when its
+// column partials (4 warps x nvec x n^2 / 64 doubles over all ranks) fit the scratch budget.
 void cov_matvec_dev(Ctx& c, const mlk_tree_s* tree, const mlk_kernel& k, const double* a, double* b, int nvec) {
   const int64_t n = tree->n;
   CUDA_CHECK(cudaMemsetAsync(b, 0, sizeof(double) * nvec * n, c.stream));
-  // rows of this rank: contiguous 32-row tiles
-  int64_t tiles = ceil_div(n, 32);
+  // rows of this rank: a contiguous range of 32-row tiles (for the symmetric kernel balanced by
+  // the triangular task costs n - 32 I)
+  const int64_t tiles = ceil_div(n, 32);
   int64_t t0 = tiles * c.rank / c.nranks, t1 = tiles * (c.rank + 1) / c.nranks;
+  const bool sym_ok = nvec <= 4 && std::getenv("MLK_NO_SYM_MATVEC") == nullptr;
+  int64_t cp = 0;
+  if (sym_ok) {
+    // balance the triangular costs (n - 32 I) over ranks
+    auto cost_before = [&](int64_t I) { return (double)I * n - 16.0 * I * (I - 1); };
+    const double total = cost_before(tiles);
+    t0 = 0;
+    while (t0 < tiles && cost_before(t0 + 1) <= total * c.rank / c.nranks) t0++;
+    t1 = t0;
+    while (t1 < tiles && cost_before(t1 + 1) <= total * (c.rank + 1) / c.nranks) t1++;
+    if (c.rank == c.nranks - 1) t1 = tiles;
+    for (int64_t I = t0; I < t1; I++) cp += 4 * (int64_t)nvec * (n - 32 * I);
+  }
   if (t1 <= t0) return;
-  int64_t r0 = t0 * 32, r1 = std::min<int64_t>(n, t1 * 32);
+  const int nv = nvec == 1 ? 1 : nvec == 2 ? 2 : 4;
   std::vector<TileUnit> units;
+  if (sym_ok && cp * (int64_t)sizeof(double) <= c.scratch_budget_bytes()) {
+    int64_t off = 0;
+    for (int64_t I = t0; I < t1; I++) {
+      const int64_t r = 32 * I;
+      make_tile_units(units, r, (int32_t)std::min<int64_t>(32, n - r), r, (int32_t)(n - r), a, n, nvec, b + r, n, 1,
+                      tree->d_pad);
+      TileUnit& u = units.back();
+      u.rq = -nv;
+      u.w_col0 = r;
+      u.w_cols = n;
+      u.cp_off = off;
+      off += 4 * (int64_t)nvec * (n - r);
+    }
+    DevBuf<double> colpart(std::max<int64_t>(cp, 1), c.stream);
+    run_tile_contract(c, tree, make_kernel_params(k), units, "cov_matvec_tile", colpart.p);
+    TimedLaunch tl(c, "cov_matvec_colsum");
+    const int nchunks = (int)ceil_div(t1 - t0, kColChunk);
+    DevBuf<double> tmp((size_t)nvec * nchunks * n, c.stream);
+    dim3 g1((unsigned)ceil_div(n - 32 * t0, 256), (unsigned)nchunks, (unsigned)nvec);
+    k_colpart_chunks<<<g1, 256, 0, c.stream>>>(colpart.p, t0, t1, n, nvec, nchunks, tmp.p);
+    check_launch("k_colpart_chunks");
+    dim3 g2((unsigned)ceil_div(n - 32 * t0, 256), (unsigned)nvec);
+    k_colpart_final<<<g2, 256, 0, c.stream>>>(tmp.p, 32 * t0, n, nchunks, b);
+    check_launch("k_colpart_final");
+    return;
+  }
+  const int64_t r0 = t0 * 32, r1 = std::min<int64_t>(n, t1 * 32);
   // rows r0..r1 as an a range; b range = all points; W_b = the vectors a (nvec x n)
   make_tile_units(units, r0, (int32_t)(r1 - r0), 0, (int32_t)n, a, n, nvec, b + r0, n, 1, tree->d_pad);
   // up to 4 vectors: lane-local DFMA contraction instead of 8-column DMMAs (tile.cu, NV)
   if (nvec <= 4)
-    for (auto& u : units) u.rq = nvec == 1 ? -1 : nvec == 2 ? -2 : -4;
+    for (auto& u : units) u.rq = -nv;
   run_tile_contract(c, tree, make_kernel_params(k), units, "cov_matvec_tile");
 }
 

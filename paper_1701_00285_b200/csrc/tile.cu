@@ -98,6 +98,9 @@ void make_tile_units(std::vector<TileUnit>& out, int64_t a_begin, int32_t s_a, i
     // a tensor map needs a 16-byte aligned base and a row stride that is a multiple of 16 bytes
     u.bulk = (ldw % 2 == 0) && ((reinterpret_cast<uintptr_t>(Wb) & 15) == 0);
     u.xmap = u.wmap = -1;
+    u.w_col0 = 0;
+    u.w_cols = s_b;
+    u.cp_off = 0;
     // FP64-slot estimate per 32-row task: Gram dp + evaluation ~20 + contraction per entry
     u.cost = 32.0 * s_b * (dp + 20 + 8.0 * rq + nr);
     out.push_back(u);
@@ -125,7 +128,9 @@ struct TileCfg {
   // the 16-byte B-fragment loads of a quarter-warp (2 rows x 4 chunks) hit distinct banks
   // without any swizzle -- which a 1-D bulk copy could not apply
   static constexpr int BN = RQ >= 6 ? 24 : 40;
-  static constexpr int NST = RQ >= 16 ? 2 : 3;   // stages in the smem ring
+  // stages in the smem ring: the one-group class (C a, tiny cells) has short stages, so it
+  // needs a deeper ring to cover the TMA latency
+  static constexpr int NST = RQ == 1 ? 6 : (RQ >= 16 ? 2 : 3);
   static constexpr int G = RQ <= 12 ? RQ : 8;    // W_b fragments held per DMMA group
   static constexpr int NACC = 1;                 // accumulator sets (2 measured no faster)
 };
@@ -170,12 +175,17 @@ __global__ void k_tile_aug(const double* __restrict__ Xt, int dpt, int d, int64_
 // by a tensor map (odd row stride or unaligned base) use 8-byte cp.async instead.  The last
 // warp to finish a stage (a shared counter) refills it with the stage NST ahead, so warps never
 // wait on a CTA barrier inside a unit.
-template <int RQ, int FAM, int NV>
+// SYM (with NV > 0): symmetric C a.  A task (32-row tile I) covers the points j >= its first
+// row; the row part b_i += C_ij a_j keeps j >= i, the column part b_j += C_ij a_i (j > i) is
+// reduced over each warp's 8 rows by shuffles and written to colpart (one row per warp and
+// vector); k_colpart_sum adds them in (tile, warp) order.  Half the covariance evaluations,
+// deterministic.
+template <int RQ, int FAM, int NV, bool SYM = false>
 __global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4)
     k_tile_contract(const TileUnit* __restrict__ units, const int32_t* __restrict__ task_range,
                     const int32_t* __restrict__ task_first, int n_units, int* __restrict__ counter,
                     const double* __restrict__ Pa, const double* __restrict__ Pb, int dpa, int sdp,
-                    KernelParams kp, const CUtensorMap* __restrict__ maps) {
+                    KernelParams kp, const CUtensorMap* __restrict__ maps, double* __restrict__ colpart) {
   constexpr int BN = TileCfg<RQ>::BN;
   constexpr int G = TileCfg<RQ>::G;
   constexpr int NST = TileCfg<RQ>::NST;
@@ -237,7 +247,7 @@ __global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4)
         if (lane == 0) {
           mbar_arrive_expect_tx(&full[slot], 8u * BN * (sdp + u.wrows));
           tma_2d_g2s(Xs, maps + u.xmap, 0, (int)(u.b_begin + b0), &full[slot]);
-          tma_2d_g2s(Ws, maps + u.wmap, b0, u.c0, &full[slot]);
+          tma_2d_g2s(Ws, maps + u.wmap, (int)(u.w_col0 + b0), u.c0, &full[slot]);
         }
       } else {
         const int cpr = dpa >> 1;
@@ -247,7 +257,7 @@ __global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4)
         }
         for (int e = lane; e < u.qc * nb; e += 32) {
           const int rho = e / nb, y = e - rho * nb;
-          cp_async8(Ws + rho * BN + y, u.Wb + (int64_t)(u.c0 + rho) * u.ldw + b0 + y, true);
+          cp_async8(Ws + rho * BN + y, u.Wb + (int64_t)(u.c0 + rho) * u.ldw + u.w_col0 + b0 + y, true);
         }
         cp_async_commit();
         cp_async_wait<0>();
@@ -280,6 +290,12 @@ __global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4)
 
     const int ar = warp * 8 + (lane >> 2);
     const int64_t ga = a0 + ar;
+    double arow[SYM ? NV : 1];  // a_i of the lane's row (column part of the symmetric product)
+    if constexpr (SYM) {
+#pragma unroll
+      for (int l = 0; l < NV; l++)  // sigma2 folded in here (the row part gets it in the epilogue)
+        arow[l] = (ar < rows && l < u.qc) ? kp.sigma2 * u.Wb[(int64_t)l * u.ldw + ga] : 0.0;
+    }
     for (int s = 0; s < nst; s++) {
       const int g = gs + s, slot = g % NST;
       mbar_wait(&full[slot], (unsigned)((g / NST) & 1));
@@ -311,6 +327,18 @@ __global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4)
           if (y + e >= u.s_b) cv[t][e] = 0.0;
         }
       }
+      double cvc[SYM ? T : 1][2];  // column-part weights: j > i only
+      if constexpr (SYM) {
+#pragma unroll
+        for (int t = 0; t < T; t++) {
+#pragma unroll
+          for (int e = 0; e < 2; e++) {
+            const int64_t j = u.b_begin + yb + 8 * t + 2 * (lane & 3) + e;
+            cvc[t][e] = (j > ga && ar < rows) ? cv[t][e] : 0.0;
+            if (j < ga) cv[t][e] = 0.0;  // row part: j >= i only
+          }
+        }
+      }
       if constexpr (NV > 0) {
         // 3'. C a for NV vectors: lane-local DFMAs over the lane's two columns per sub-tile
 #pragma unroll
@@ -321,6 +349,26 @@ __global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4)
             const double2 wv = *reinterpret_cast<const double2*>(Ws + l * BN + 2 * ch);
             accv[l] = fma(cv[t][0], wv.x, accv[l]);
             accv[l] = fma(cv[t][1], wv.y, accv[l]);
+          }
+        }
+        if constexpr (SYM) {
+          // column part: sum over the warp's 8 rows (lanes with equal lane & 3), lanes 0..3
+          // keep the sums of their columns
+#pragma unroll
+          for (int t = 0; t < T; t++) {
+#pragma unroll
+            for (int e = 0; e < 2; e++) {
+#pragma unroll
+              for (int l = 0; l < NV; l++) {
+                double v = cvc[t][e] * arow[l];
+                v += __shfl_xor_sync(0xffffffffu, v, 4);
+                v += __shfl_xor_sync(0xffffffffu, v, 8);
+                v += __shfl_xor_sync(0xffffffffu, v, 16);
+                const int y = yb + 8 * t + 2 * lane + e;
+                if (lane < 4 && y < u.s_b && l < u.qc)
+                  colpart[u.cp_off + ((int64_t)warp * u.qc + l) * u.s_b + y] = v;
+              }
+            }
           }
         }
       } else {
@@ -425,6 +473,7 @@ struct AugArgs {
   const CUtensorMap* maps;
   const int32_t* task_range;  // task -> range (relative to the class), per class
   const int32_t* task_first;  // range -> first task (relative to the class)
+  double* colpart = nullptr;  // symmetric C a column partials (nullptr: ordinary product)
 };
 
 // task -> range map of one class: ranges r own tasks first[r] .. first[r] + n_tasks[r] - 1
@@ -470,12 +519,12 @@ int class_bn(int rq) {
   }
 }
 
-template <int RQ, int FAM, int NV = 0>
+template <int RQ, int FAM, int NV = 0, bool SYM = false>
 void launch_class(Ctx& c, const AugArgs& ag, const KernelParams& kp, const TileUnit* units, int n, int* counter) {
   // units = this class's ranges; n = its tasks (ag.task_range / ag.task_first are class-relative)
   constexpr int BN = TileCfg<RQ>::BN;
   size_t smem = sizeof(double) * (size_t)(32 * ag.sdp + TileCfg<RQ>::NST * stage_doubles(RQ, BN, ag.sdp));
-  auto fn = k_tile_contract<RQ, FAM, NV>;
+  auto fn = k_tile_contract<RQ, FAM, NV, SYM>;
   // attribute / occupancy queries are driver round trips: once per instantiation and size
   static size_t smem_set = 0;
   static int occ = 0;
@@ -487,7 +536,7 @@ void launch_class(Ctx& c, const AugArgs& ag, const KernelParams& kp, const TileU
   }
   int grid = std::min<int64_t>(n, (int64_t)num_sms(c.device) * occ);
   fn<<<grid, 128, smem, c.stream>>>(units, ag.task_range, ag.task_first, n, counter, ag.Pa, ag.Pb, ag.dpa, ag.sdp, kp,
-                                    ag.maps);
+                                    ag.maps, ag.colpart);
   check_launch("k_tile_contract");
 }
 
@@ -495,9 +544,18 @@ template <int FAM>
 void launch_fam(Ctx& c, const AugArgs& ag, const KernelParams& kp, int rq, const TileUnit* units, int n,
                 int* counter) {
   switch (rq) {
-    case -1: launch_class<1, FAM, 1>(c, ag, kp, units, n, counter); break;
-    case -2: launch_class<1, FAM, 2>(c, ag, kp, units, n, counter); break;
-    case -4: launch_class<1, FAM, 4>(c, ag, kp, units, n, counter); break;
+    case -1:
+      if (ag.colpart) launch_class<1, FAM, 1, true>(c, ag, kp, units, n, counter);
+      else launch_class<1, FAM, 1>(c, ag, kp, units, n, counter);
+      break;
+    case -2:
+      if (ag.colpart) launch_class<1, FAM, 2, true>(c, ag, kp, units, n, counter);
+      else launch_class<1, FAM, 2>(c, ag, kp, units, n, counter);
+      break;
+    case -4:
+      if (ag.colpart) launch_class<1, FAM, 4, true>(c, ag, kp, units, n, counter);
+      else launch_class<1, FAM, 4>(c, ag, kp, units, n, counter);
+      break;
     case 1: launch_class<1, FAM>(c, ag, kp, units, n, counter); break;
     case 2: launch_class<2, FAM>(c, ag, kp, units, n, counter); break;
     case 3: launch_class<3, FAM>(c, ag, kp, units, n, counter); break;
@@ -517,7 +575,7 @@ void launch_fam(Ctx& c, const AugArgs& ag, const KernelParams& kp, int rq, const
 }  // namespace
 
 void run_tile_contract(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, std::vector<TileUnit>& units,
-                       const char* name) {
+                       const char* name, double* colpart) {
   if (units.empty()) return;
   // ranges grouped by class, largest per-task cost first inside a class
   std::vector<int32_t> order(units.size());
@@ -554,6 +612,7 @@ void run_tile_contract(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, s
   // augmented, pre-scaled coordinates (k_tile_aug); the smem row stride avoids 2-way bank
   // conflicts of the fragment loads when dpa/4 is even
   AugArgs ag;
+  ag.colpart = colpart;
   ag.dpa = pad4(tree->d + 2);
   ag.sdp = ((ag.dpa >> 2) & 1) ? ag.dpa : ag.dpa + 4;
   DevBuf<double> aug((size_t)2 * tree->n * ag.dpa, c.stream);
@@ -574,16 +633,17 @@ void run_tile_contract(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, s
     };
     const TileUnit* prev = nullptr;  // consecutive ranges mostly share W_b: skip the lookup
     for (auto& u : ranges) {
-      u.wrows = u.rq > 0 ? 8 * u.rq + u.nr : 8;
+      // C a (rq < 0): stage only the qc real vector rows (the kernel never reads rows >= qc)
+      u.wrows = u.rq > 0 ? 8 * u.rq + u.nr : u.qc;
       if (!u.bulk) continue;
       if (prev && prev->Wb == u.Wb && prev->rq == u.rq && prev->nr == u.nr && prev->p_b == u.p_b &&
-          prev->s_b == u.s_b && prev->ldw == u.ldw) {
+          prev->w_cols == u.w_cols && prev->ldw == u.ldw) {
         u.xmap = prev->xmap;
         u.wmap = prev->wmap;
       } else {
         const int bn = class_bn(u.rq);
         u.xmap = get(ag.Pb, tree->n, ag.dpa, ag.dpa, bn, ag.sdp);
-        u.wmap = get(u.Wb, u.p_b, u.s_b, u.ldw, u.wrows, bn);
+        u.wmap = get(u.Wb, u.p_b, u.w_cols, u.ldw, u.wrows, bn);
       }
       prev = &u;
     }

@@ -28,6 +28,9 @@ struct TileUnit {
   int32_t xmap, wmap;        // tensor maps of the b rows and of W_b (run_tile_contract)
   int32_t nr;                // columns 8 rq .. 8 rq + nr - 1 of the chunk are done with DFMAs
   int32_t wrows;             // W_b rows staged per stage (8 rq + nr)
+  int64_t w_col0;            // W_b column of point b_begin (0, except the symmetric C a tasks)
+  int64_t w_cols;            // columns of W_b addressable by the tensor map (s_b by default)
+  int64_t cp_off;            // symmetric C a: offset of this task's column partials (NV x s_b)
 };
 
 struct KernelParams {
@@ -44,9 +47,10 @@ KernelParams make_kernel_params(const mlk_kernel& k);
 int tile_rq_class(int qc);  // smallest available rq with 8 rq >= qc
 constexpr int kTileMaxRQ = 24;
 constexpr int kTileMaxNR = 3;  // at most this many remainder columns go to DFMA instead of padding
-// Run all units (any mix of rq classes) on the context stream.
+// Run all units (any mix of rq classes) on the context stream.  colpart != nullptr selects the
+// symmetric C a kernel (units with rq = -NV; see tile.cu).
 void run_tile_contract(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, std::vector<TileUnit>& units,
-                       const char* name);
+                       const char* name, double* colpart = nullptr);
 // Split a (pair, output) into units: rows in blocks of 32, W_b rows in balanced chunks.
 void make_tile_units(std::vector<TileUnit>& out, int64_t a_begin, int32_t s_a, int64_t b_begin, int32_t s_b,
                      const double* Wb, int64_t ldw, int32_t p_b, double* U, int64_t ldu, int32_t trans, int dp);

@@ -364,6 +364,24 @@ def test_matvec_exact_and_bsr(mlk, ctx, fam, rho):
     assert np.linalg.norm(ya - yr) <= 1e-11 * np.linalg.norm(yr)
 
 
+@pytest.mark.parametrize("nvec", [1, 2, 3, 5])
+def test_cov_matvec_symmetric_and_full_agree(mlk, ctx, nvec, monkeypatch):
+    """b = C a by the symmetric kernel (each pair (i, j) evaluated once, fixed-order column
+    reduction) equals the full n^2 kernel and the oracle; ragged n so the last tile is partial."""
+    X, dirs = _setup(3001, 3, 64, 0, "normal")
+    g, o = _tree_both(mlk, ctx, X, 64, 0, dirs)
+    kern = dict(family=OC.MATERN_52, rho=0.8, nugget=1e-3, sigma2=1.7)
+    a = np.random.default_rng([0, 5]).standard_normal((nvec, 3001))
+    b_sym = mlk.cov_matvec(ctx, g, kern, a)
+    b_sym2 = mlk.cov_matvec(ctx, g, kern, a)
+    assert np.array_equal(b_sym, b_sym2)                 # deterministic
+    monkeypatch.setenv("MLK_NO_SYM_MATVEC", "1")
+    b_full = mlk.cov_matvec(ctx, g, kern, a)
+    br = OM.cov_matvec(X, o, kern, a)
+    assert np.linalg.norm(b_sym - br) <= 1e-12 * np.linalg.norm(br)
+    assert np.linalg.norm(b_full - br) <= 1e-12 * np.linalg.norm(br)
+
+
 def test_matvec_cfg3_sampled_rows(mlk, ctx):
     """cfg3 at full size with its 10 N(0,1) vectors: apply_wt / apply_w in full, C a on 512
     seeded rows (the host cannot do the 1.7e10-entry product in test time)."""
