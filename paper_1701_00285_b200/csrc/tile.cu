@@ -127,7 +127,7 @@ struct TileCfg {
   // b points per stage.  BN = 8 (mod 16) makes a W row 8 BN doubles = 64 (mod 128) bytes, so
   // the 16-byte B-fragment loads of a quarter-warp (2 rows x 4 chunks) hit distinct banks
   // without any swizzle -- which a 1-D bulk copy could not apply
-  static constexpr int BN = RQ >= 6 ? 24 : 40;
+  static constexpr int BN = RQ >= 6 ? 24 : 56;
   // stages in the smem ring: the one-group class (C a, tiny cells) has short stages, so it
   // needs a deeper ring to cover the TMA latency
   static constexpr int NST = RQ == 1 ? 6 : (RQ >= 16 ? 2 : 3);
