@@ -304,6 +304,34 @@ def test_full_size_sampled_blocks(mlk, ctx, name, max_entries):
         assert e <= TOL_BLOCK, (name, k, a, b, e)
 
 
+def test_cfg5_shape_mini(mlk, ctx):
+    """cfg5's shape at reduced n (d = 50, w = 2 -> M = 1326 > every shared-memory path, leaf
+    2048, Gaussian rho = 4 + nugget 1e-6, tau = 1e-7): basis, every admitted block and C_W v
+    against the oracle.  cfg5 itself needs 8 GPUs (106 GB of W, 184 GB of BSR)."""
+    c = dict(wl.CONFIGS["cfg5"])
+    inp = wl.make(c, n=8192)
+    c = inp["cfg"]
+    X = inp["X"]
+    g, o = _tree_both(mlk, ctx, X, c["leaf"], c["tree"], inp["dirs"])
+    _check_tree(g, o)
+    gb = mlk.build_basis(ctx, g, c["w"])
+    ob = OB.build_basis(X, o, c["w"])
+    assert gb.M == 1326
+    for q in ob.cells:
+        Wg, _ = gb.block(q, int(o.end[q] - o.begin[q]))
+        assert np.linalg.norm(Wg - ob.W[q]) <= TOL_BLOCK * np.linalg.norm(ob.W[q])
+    kern = wl.kernel_dict(c)
+    pairs = OA.admitted_pairs(X, o, ob, c["pairs"], c["tau"])
+    ref = OAs.assemble(X, o, ob, kern, pairs)
+    got = mlk.assemble_cw(ctx, g, gb, kern, dict(mode=c["pairs"], tau=c["tau"])).export()
+    assert np.array_equal(got["val_off"], ref.val_off) and np.array_equal(got["bcol"], ref.bcol)
+    assert _block_errs(got["values"], ref).max() <= TOL_BLOCK
+    v = wl.vectors(1, gb.dim)
+    y = mlk.cw_matvec(ctx, g, gb, kern, None, mlk.MATVEC_EXACT, v)
+    yr = OM.cw_matvec_exact(X, o, ob, kern, v)
+    assert np.linalg.norm(y - yr) <= 1e-11 * np.linalg.norm(yr)
+
+
 def test_assembly_deterministic(mlk, ctx):
     X, dirs = _setup(4096, 10, 128, 1)
     g = mlk.build_tree(ctx, X, 128, 1, dirs)
