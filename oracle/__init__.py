@@ -16,6 +16,7 @@ Modules
                  Alg 6 pair admission with tau_{i,j}
   assemble    -- blocks W_i C W_j^T (Alg 6), dense C_W
   matvec      -- C_W v by the three-step product and on the BSR
+  pcg         -- PCG for C_W gamma_W = Z_W with the block-diagonal P_W, NEXT-1
 
 Parity status of every function is listed in DESIGN.md section "Oracle pins".
 """

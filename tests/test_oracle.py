@@ -445,3 +445,47 @@ def test_matvec_exact_bsr_and_round_trip():
     rows = np.array([0, 17, 255])
     a = Mv.apply_wt(tr, B, v)
     assert np.allclose(Mv.cov_matvec(X, tr, kern, a, rows=rows), Mv.cov_matvec(X, tr, kern, a)[:, rows])
+
+
+# ----------------------------------------------------------------------------- PCG (NEXT-1)
+from oracle import pcg as Pc  # noqa: E402
+
+
+def test_pcg_finite_termination_and_dense_solve():
+    """CG on an SPD matrix with 3 distinct eigenvalues stops in 3 iterations (Krylov space of
+    the minimal polynomial); the result equals numpy.linalg.solve."""
+    rng = np.random.default_rng(7)
+    Q, _ = np.linalg.qr(rng.standard_normal((40, 40)))
+    A = Q @ np.diag(np.repeat([1.0, 2.5, 7.0], [14, 13, 13])) @ Q.T
+    z = rng.standard_normal(40)
+    x, it, res = Pc.pcg(lambda v: A @ v, z, 1e-12, 100)
+    assert it == 3 and res <= 1e-12
+    assert np.linalg.norm(x - np.linalg.solve(A, z)) <= 1e-11 * np.linalg.norm(x)
+    # an exact preconditioner (M = A) converges in one step
+    x1, it1, _ = Pc.pcg(lambda v: A @ v, z, 1e-12, 100, precond=lambda r: np.linalg.solve(A, r))
+    assert it1 == 1 and np.linalg.norm(x1 - x) <= 1e-11 * np.linalg.norm(x)
+
+
+def test_pcg_cw_against_dense_system():
+    """gamma_W of the PCG (with and without P_W) solves the dense C_W = W C W^T system: the true
+    residual, not the recursive one, is below the tolerance, and both agree with a dense solve.
+    P_W's blocks are the diagonal blocks of the dense C_W and are SPD (Theorem)."""
+    X, tr, B, pairs = small_setup(n=512, d=2, w=2, leaf=32)
+    kern = dict(family=cv.MATERN_12, rho=0.2)   # cond(C_W) ~ 7e2
+    CW, _, _ = As.dense_cw(X, tr, B, kern)
+    z = np.random.default_rng(3).standard_normal(B.dim)
+    blocks = Pc.preconditioner_blocks(X, tr, B, kern)
+    row_off = np.array([B.row_off[q] for q in B.cells] + [B.dim])
+    for k, P in enumerate(blocks):
+        a, b = row_off[k], row_off[k + 1]
+        assert np.allclose(P, CW[a:b, a:b], rtol=0, atol=1e-12 * np.abs(CW).max())
+        assert np.linalg.eigvalsh(P).min() > 0
+    xd = np.linalg.solve(CW, z)
+    its = []
+    for use in (True, False):
+        x, it, res = Pc.solve_cw(X, tr, B, kern, z, tol=1e-10, max_iter=2000, use_precond=use)
+        its.append(it)
+        assert res <= 1e-10
+        assert np.linalg.norm(z - CW @ x) <= 2e-10 * np.linalg.norm(z)
+        assert np.linalg.norm(x - xd) <= 1e-7 * np.linalg.norm(xd)
+    assert its[0] < its[1]   # P_W pays off on this instance (63 vs 198 iterations)
