@@ -236,6 +236,23 @@ mlk_status mlk_cw_matvec(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const mlk_
                          mlk_cw cw, int32_t mode, const double* v, double* y, int32_t nvec);
 
 /* ------------------------------------------------------------------------------------------
+ * mlk_pcg_solve -- gamma_W = C_W^-1 z_W by preconditioned conjugate gradient (the
+ * survey's NEXT-1).  Products C_W p by the EXACT three-step product.
+ *  precond 1: P_W = diag of the self blocks W_k C W_k^T of every cell, taken from
+ *             the assembled `cw` (which must contain every self block -- always the case for
+ *             mlk_assemble_cw -- and be complete), Cholesky-factored once; MLK_ERR_RANK_DEFICIENT
+ *             if a block is not positive definite.  precond 0: P_W = I (cw may be NULL).
+ *  z_w, gamma_w: dim doubles (host or device).  Iterates from gamma = 0 until the recursive
+ *  residual satisfies ||r|| <= tol ||z_W|| or max_iter iterations; *iters receives the count and
+ *  *rel_residual the TRUE unpreconditioned residual ||z_W - C_W gamma|| / ||z_W||,
+ *  recomputed with one extra product.  Deterministic (fixed-order reductions).  nranks == 1 only
+ *  (MLK_ERR_UNSUPPORTED otherwise).
+ */
+mlk_status mlk_pcg_solve(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const mlk_kernel* kernel, mlk_cw cw,
+                         int32_t precond, const double* z_w, double* gamma_w, double tol, int32_t max_iter,
+                         int32_t* iters, double* rel_residual);
+
+/* ------------------------------------------------------------------------------------------
  * Host-only helpers (no device needed).
  * mlk_partition_lpt: longest-processing-time assignment of n units with the given costs to
  * nranks ranks (largest first to the least-loaded rank; ties to the lower rank), the

@@ -22,6 +22,7 @@
   return MLK_OK;
 
 struct mlk_basis_s;
+struct mlk_tree_s;
 namespace mlk {
 void partition_lpt(const double* cost, int64_t n, int nranks, int32_t* owner);
 void shard_plan(const int64_t* val_off, const int32_t* owner, int64_t n, int nranks, int64_t* shard_off,
@@ -31,6 +32,13 @@ void shard_plan(const int64_t* val_off, const int32_t* owner, int64_t n, int nra
 // the first call also synchronises and reports a rank-deficient merge (MLK_ERR_RANK_DEFICIENT)
 void basis_wait(Ctx& c, const mlk_basis_s* B);
 void basis_sync(const mlk_basis_s* B);
+
+// The three steps of C_W v (matvec.cu), device vectors, nvec x n (point space, tree order) or
+// nvec x dim (C_W space): a = W^T v, b = C a (this rank's rows), y = W b.
+void apply_wt_dev(Ctx& c, const mlk_tree_s* tree, const mlk_basis_s* B, const double* v, double* a, int nvec);
+void cov_matvec_dev(Ctx& c, const mlk_tree_s* tree, const mlk_kernel& k, const double* a, double* b, int nvec);
+void apply_w_dev(Ctx& c, const mlk_tree_s* tree, const mlk_basis_s* B, const double* b, double* y, int nvec);
+void check_kernel(const mlk_kernel* k);
 
 // padded coordinate count for the DMMA k = 4 Gram steps
 inline int pad4(int d) { return (d + 3) / 4 * 4; }

@@ -102,6 +102,8 @@ __global__ void k_bsr_matvec(const int32_t* __restrict__ brow_ptr, const int32_t
   }
 }
 
+}  // namespace
+
 std::vector<std::vector<CellJob>> level_jobs(const mlk_tree_s* tree, const mlk_basis_s* B) {
   std::vector<std::vector<CellJob>> lv(tree->t + 1);
   for (size_t i = 0; i < B->cells.size(); i++) {
@@ -247,7 +249,6 @@ void check_kernel(const mlk_kernel* k) {
   MLK_REQUIRE(k->rho > 0 && k->sigma2 > 0 && k->nugget >= 0, "need rho > 0, sigma2 > 0, nugget >= 0");
 }
 
-}  // namespace
 }  // namespace mlk
 
 using namespace mlk;

@@ -35,6 +35,7 @@ SYMBOLS = [
     "mlk_cw_free", "mlk_cw_info", "mlk_cw_export", "mlk_cw_owner", "mlk_cw_shard_len", "mlk_cw_pack",
     "mlk_cw_unpack", "mlk_cw_values_device", "mlk_cov_matvec", "mlk_cw_matvec", "mlk_partition_lpt",
     "mlk_shard_plan", "mlk_launch_count", "mlk_cw_flops", "mlk_cw_export_async", "mlk_ctx_wait_copies",
+    "mlk_pcg_solve",
 ]
 
 
@@ -100,6 +101,8 @@ _sig = {
     "mlk_cw_flops": (C.c_int, [P, P, P, P]),
     "mlk_cw_export_async": (C.c_int, [P, P, P]),
     "mlk_ctx_wait_copies": (C.c_int, [P]),
+    "mlk_pcg_solve": (C.c_int, [P, P, P, C.POINTER(KernelSpec), P, C.c_int32, P, P, C.c_double, C.c_int32,
+                                C.POINTER(C.c_int32), C.POINTER(C.c_double)]),
 }
 for _n, (_r, _a) in _sig.items():
     _f = getattr(_lib, _n)
@@ -416,6 +419,23 @@ def cw_matvec(ctx, tree, basis, kernel, cw, mode, v, out=None, allreduce=True, g
         else:
             dist.all_reduce(res, group=group)
     return res
+
+
+def pcg_solve(ctx, tree, basis, kernel, cw, z_w, tol=1e-10, max_iter=1000, precond=True, out=None):
+    """gamma_W = C_W^-1 z_W by PCG with the block-diagonal preconditioner (cw's self blocks) or
+    none.  Returns (gamma_W, iterations, true relative residual)."""
+    zp, keep = _ptr(z_w)
+    if out is None:
+        res = np.empty(basis.dim, np.float64)
+        op = _np(res)
+    else:
+        res = out
+        op, _ = _ptr(out)
+    it = C.c_int32()
+    rr = C.c_double()
+    _check(_lib.mlk_pcg_solve(ctx.h, tree.h, basis.h, C.byref(_kspec(kernel)), cw.h if cw is not None else None,
+                              1 if precond else 0, zp, op, float(tol), int(max_iter), C.byref(it), C.byref(rr)))
+    return res, it.value, rr.value
 
 
 def partition_lpt(cost, nranks):

@@ -474,3 +474,31 @@ def test_multirank_emulated_bit_identical(mlk, ctx, R):
     ybs = [mlk.cw_matvec(c, t, b, kern, cw, mlk.MATVEC_BSR, v, allreduce=False)
            for c, t, b, cw in zip(ctxs, trees, bases, cws)]
     assert np.linalg.norm(sum(ybs) - yb1) <= 1e-13 * np.linalg.norm(yb1)
+
+
+# --------------------------------------------------------------------------------- PCG (NEXT-1)
+@pytest.mark.parametrize("n,d,leaf,kind,fam,rho", [
+    (512, 2, 32, 0, OC.MATERN_12, 0.2),      # the oracle pin's instance (cond(C_W) ~ 7e2)
+    (2048, 10, 128, 1, OC.MATERN_32, 0.5),   # cfg2 shape
+])
+def test_pcg_matches_oracle(mlk, ctx, n, d, leaf, kind, fam, rho):
+    """GPU PCG (EXACT products, block-diagonal P_W from the assembled self blocks, or none)
+    against oracle/pcg.py: same iteration count up to one step, same solution to the
+    tolerance's scale, true residual below the tolerance."""
+    from oracle import pcg as OP
+    X, dirs = _setup(n, d, leaf, kind)
+    g, o = _tree_both(mlk, ctx, X, leaf, kind, dirs)
+    gb = mlk.build_basis(ctx, g, 2)
+    ob = OB.build_basis(X, o, 2)
+    kern = dict(family=fam, rho=rho)
+    cw = mlk.assemble_cw(ctx, g, gb, kern, dict(mode=1, tau=1e-6))
+    z = np.random.default_rng([0, 6]).standard_normal(gb.dim)
+    for precond in (True, False):
+        x, it, res = mlk.pcg_solve(ctx, g, gb, kern, cw, z, tol=1e-9, max_iter=3000, precond=precond)
+        xo, ito, reso = OP.solve_cw(X, o, ob, kern, z, tol=1e-9, max_iter=3000, use_precond=precond)
+        assert abs(it - ito) <= 1, (precond, it, ito)
+        assert res <= 2e-9, res
+        assert np.linalg.norm(x - xo) <= 1e-6 * np.linalg.norm(xo)
+    x1, _, _ = mlk.pcg_solve(ctx, g, gb, kern, cw, z, tol=1e-9, max_iter=3000)
+    x2, _, _ = mlk.pcg_solve(ctx, g, gb, kern, cw, z, tol=1e-9, max_iter=3000)
+    assert np.array_equal(x1, x2)   # deterministic
