@@ -181,6 +181,7 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--pcg-tol", type=float, default=1e-8, help="PCG solve reported after the bench (0: skip)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -312,6 +313,23 @@ def main():
     h2d = inp["X"].nbytes + (dirs.nbytes if dirs is not None else 0) + vh.numel() * 8
     d2h = nnz * 8 + yh.numel() * 8
 
+    # ---- NEXT-1 (outside the timed step): one PCG solve C_W gamma = z with P_W, N(0,1) z
+    pcg = None
+    if args.pcg_tol > 0 and ws == 1:
+        trp = mlk.build_tree(ctx, X_d, c["leaf"], c["tree"], dirs_d)
+        Bp = mlk.build_basis(ctx, trp, c["w"])
+        cwp = mlk.assemble_cw(ctx, trp, Bp, kern, spars)
+        zp = torch.from_numpy(wl.vectors(1, Bp.dim, seed=9)[0]).to(dev)
+        gp = torch.empty_like(zp)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, it, rr = mlk.pcg_solve(ctx, trp, Bp, kern, cwp, zp, tol=args.pcg_tol, max_iter=5000, out=gp)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        pcg = {"tol": args.pcg_tol, "precond": "block-diagonal P_W (self blocks)", "iterations": it,
+               "true_rel_residual": rr, "seconds": dt, "ms_per_iteration": 1e3 * dt / max(it, 1)}
+        del trp, Bp, cwp
+
     if rank == 0:
         peak = fp64_peak()
         k5 = stats.get("assemble_tile_contract", {"ms": float("nan"), "launches": 1})
@@ -348,6 +366,7 @@ def main():
                     "d2h_bytes_per_step": int(d2h),
                     "ms_per_step": e2e_total / args.e2e_steps if e2e_ms else None},
             "cpu_baseline": cpu,
+            "pcg": pcg,
         }
         print(json.dumps(line))
     if ws > 1:
