@@ -126,6 +126,12 @@ mlk_status mlk_tree_export(mlk_tree tree, int64_t* perm, int64_t* begin, int64_t
  * reports a numerically rank-deficient merge there (MLK_ERR_RANK_DEFICIENT).
  */
 mlk_status mlk_build_basis(mlk_ctx ctx, mlk_tree tree, int32_t w, mlk_basis* out);
+/* The same with the index set of Table multivariate:table1 (NEXT-3): total degree
+ * (TD, sum p_i <= w, M = C(d + w, w)), hyperbolic cross (HC, prod (p_i + 1) <= w), Smolyak
+ * (SM, sum f(p_i) <= w, f(0) = 0, f(1) = 1, f(p) = ceil(log2 p)) or tensor product (TP,
+ * max p_i <= w), in the graded order of reading R8.  M <= 4096. */
+typedef enum { MLK_INDEX_TD = 0, MLK_INDEX_HC = 1, MLK_INDEX_SM = 2, MLK_INDEX_TP = 3 } mlk_index_set;
+mlk_status mlk_build_basis_ex(mlk_ctx ctx, mlk_tree tree, int32_t index_set, int32_t w, mlk_basis* out);
 void mlk_basis_free(mlk_basis basis); /* NULL-safe */
 /* M; dim = N - M rows of W; n_cells = cells with at least one wavelet. */
 mlk_status mlk_basis_info(mlk_basis basis, int32_t* M, int64_t* dim, int32_t* n_cells);
@@ -144,10 +150,14 @@ mlk_status mlk_apply_w(mlk_ctx ctx, mlk_basis basis, const double* b, double* y,
  * the Matern closed forms nu = 1/2, 3/2, 5/2 with z = sqrt(2 nu) r / rho (R16)
  * or the Gaussian exp(-r^2 / rho^2) (R17).  rho > 0, sigma2 > 0, nugget >= 0.
  */
-typedef enum { MLK_MATERN_12 = 0, MLK_MATERN_32 = 1, MLK_MATERN_52 = 2, MLK_GAUSSIAN = 3 } mlk_family;
+/* MLK_MATERN_NU (NEXT-3): the definition of P:970 for any nu > 0 (the paper's workloads use
+ * nu = 1.25, 3/4), with K_nu evaluated in the kernel (Temme's series below z = 2, Steed's
+ * continued fraction above, upward recurrence in nu); nu is read only for this family. */
+typedef enum { MLK_MATERN_12 = 0, MLK_MATERN_32 = 1, MLK_MATERN_52 = 2, MLK_GAUSSIAN = 3, MLK_MATERN_NU = 4 } mlk_family;
 typedef struct {
   int32_t family;
   double rho, sigma2, nugget;
+  double nu;
 } mlk_kernel;
 
 /* Sparsity: MLK_PAIRS_ALL admits every cell pair (dense C_W); MLK_PAIRS_PAPER_TAU admits the

@@ -38,7 +38,7 @@ def block(X, tree, basis, kern, a, b, dtype=np.float64):
     Xa = np.asarray(X[ia], dtype=dtype)
     Xb = np.asarray(X[ib], dtype=dtype)
     C = cov(Xa, Xb, ia, ib, kern["family"], dtype(kern["rho"]), dtype(kern.get("sigma2", 1.0)),
-            dtype(kern.get("nugget", 0.0)))
+            dtype(kern.get("nugget", 0.0)), nu=kern.get("nu"))
     Wa = np.asarray(basis.W[a], dtype=dtype)
     Wb = np.asarray(basis.W[b], dtype=dtype)
     return Wa @ C @ Wb.T
@@ -77,7 +77,7 @@ def dense_cw(X, tree, basis, kern):
     ids = tree.perm
     Xt = np.asarray(X)[ids]
     C = cov(Xt, Xt, ids, ids, kern["family"], kern["rho"], kern.get("sigma2", 1.0),
-            kern.get("nugget", 0.0))
+            kern.get("nugget", 0.0), nu=kern.get("nu"))
     return W @ C @ W.T, C, W
 
 

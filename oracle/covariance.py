@@ -16,13 +16,17 @@ identity -- so that the oracle is independent of the GPU path.
 """
 import numpy as np
 
-MATERN_12, MATERN_32, MATERN_52, GAUSSIAN = 0, 1, 2, 3
+MATERN_12, MATERN_32, MATERN_52, GAUSSIAN, MATERN_NU = 0, 1, 2, 3, 4
 FAMILY_NU = {MATERN_12: 0.5, MATERN_32: 1.5, MATERN_52: 2.5}
 
 
-def phi(r, family, rho):
-    """Correlation phi(r) for the four supported families (readings R16, R17)."""
+def phi(r, family, rho, nu=None):
+    """Correlation phi(r) for the supported families (readings R16, R17); MATERN_NU is
+    the definition of P:970 for any nu > 0 (NEXT-3: the paper's nu = 1.25, 3/4), by the Bessel
+    function itself."""
     r = np.asarray(r)
+    if family == MATERN_NU:
+        return matern_bessel(r, nu, rho)
     if family == MATERN_12:
         z = r / rho
         return np.exp(-z)
@@ -58,10 +62,10 @@ def distances(Xa, Xb):
     return np.sqrt(np.sum(diff * diff, axis=2))
 
 
-def cov(Xa, Xb, ia, ib, family, rho, sigma2=1.0, nugget=0.0):
+def cov(Xa, Xb, ia, ib, family, rho, sigma2=1.0, nugget=0.0, nu=None):
     """Covariance tile C(X_a, X_b) with global observation indices ia, ib (reading R18)."""
     r = distances(Xa, Xb)
-    C = sigma2 * phi(r, family, rho)
+    C = sigma2 * phi(r, family, rho, nu)
     if nugget != 0.0:
         C = C + nugget * (np.asarray(ia)[:, None] == np.asarray(ib)[None, :])
     return C

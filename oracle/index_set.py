@@ -100,6 +100,37 @@ def sm_f(p):
     return math.ceil(math.log2(p))
 
 
+def sm_exponents(d, w):
+    """Smolyak set {alpha : sum_i f(alpha_i) <= w} (Table multivariate:table1), graded order."""
+    out = []
+
+    def rec(start, budget, cur):
+        out.append(tuple(cur))
+        for k in range(start, d):
+            e = 1
+            while sm_f(e) <= budget:
+                cur[k] = e
+                rec(k + 1, budget - sm_f(e), cur)
+                cur[k] = 0
+                e += 1
+
+    rec(0, w, [0] * d)
+    return sorted(out, key=_graded_key)
+
+
+def tp_exponents(d, w):
+    """Tensor-product set {alpha : max_i alpha_i <= w} (Table multivariate:table1), graded order."""
+    return sorted(itertools.product(range(w + 1), repeat=d), key=_graded_key)
+
+
+TD, HC, SM, TP = 0, 1, 2, 3
+
+
+def exponents(kind, d, w):
+    """The index set Lambda(w) of Table multivariate:table1 in graded order (R8)."""
+    return {TD: td_exponents, HC: hc_exponents, SM: sm_exponents, TP: tp_exponents}[kind](d, w)
+
+
 def monomials(X, exps):
     """Design matrix P(X)[i, m] = prod_k X[i, k]^alpha_m[k] (the matrix M of P:172-173).
 

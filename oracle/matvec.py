@@ -40,7 +40,7 @@ def cov_matvec(X, tree, kern, a, panel=2048, rows=None):
     for s in range(0, rows.size, panel):
         rr = rows[s:s + panel]
         C = cov(Xt[rr], Xt, ids[rr], ids, kern["family"], kern["rho"], kern.get("sigma2", 1.0),
-                kern.get("nugget", 0.0))
+                kern.get("nugget", 0.0), nu=kern.get("nu"))
         b[:, s:s + rr.size] = (C @ a.T).T
     return b
 

@@ -277,8 +277,12 @@ mlk_status mlk_assemble_cw(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const ml
   MLK_REQUIRE(ctx && tree && basis && kernel && sparsity && out, "NULL argument");
   *out = nullptr;
   MLK_REQUIRE(basis->tree == tree, "basis was built for another tree");
-  MLK_REQUIRE(kernel->family >= MLK_MATERN_12 && kernel->family <= MLK_GAUSSIAN, "unknown covariance family");
+  MLK_REQUIRE(kernel->family >= MLK_MATERN_12 && kernel->family <= MLK_MATERN_NU, "unknown covariance family");
   MLK_REQUIRE(kernel->rho > 0 && kernel->sigma2 > 0 && kernel->nugget >= 0, "need rho > 0, sigma2 > 0, nugget >= 0");
+  MLK_REQUIRE(kernel->family != MLK_MATERN_NU || (kernel->nu > 0 && kernel->nu <= 50),
+              "MLK_MATERN_NU needs 0 < nu <= 50");
+  MLK_REQUIRE(precision == MLK_PREC_FP64 || kernel->family != MLK_MATERN_NU,
+              "the double-double mode covers the closed-form families only");
   MLK_REQUIRE(sparsity->mode == MLK_PAIRS_ALL || sparsity->mode == MLK_PAIRS_PAPER_TAU, "unknown sparsity mode");
   MLK_REQUIRE(sparsity->mode == MLK_PAIRS_ALL || (sparsity->tau >= 0 && !std::isnan(sparsity->tau)), "need tau >= 0");
   MLK_REQUIRE(precision == MLK_PREC_FP64 || precision == MLK_PREC_DD, "unknown precision");

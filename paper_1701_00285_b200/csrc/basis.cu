@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <functional>
 #include <memory>
 
 #include "api.cuh"
@@ -15,22 +16,49 @@
 namespace mlk {
 namespace {
 
-// graded total-degree exponent set as factor lists (coordinate indices, nondecreasing),
-// degree 0 first, then combinations with replacement in lexicographic order (R8)
-std::vector<std::vector<int>> td_factors(int d, int w) {
+// Index set Lambda(w) of Table multivariate:table1 as factor lists (coordinate
+// indices, nondecreasing; a monomial is the left-to-right product of its factors), in graded
+// order (R8): total degree, then the factor lists lexicographically -- combinations with
+// replacement for TD.  Depth-first over the nonzero coordinates with the set's (monotone)
+// budget; at most kMaxM members.
+constexpr int kMaxM = 4096;
+int sm_f(int p) {
+  if (p <= 1) return p;
+  int l = 0;
+  while ((1 << l) < p) l++;
+  return l;  // ceil(log2 p)
+}
+std::vector<std::vector<int>> index_set_factors(int kind, int d, int w) {
   std::vector<std::vector<int>> out;
-  out.push_back({});
-  for (int deg = 1; deg <= w; deg++) {
-    std::vector<int> cur(deg, 0);
-    while (true) {
-      out.push_back(cur);
-      int i = deg - 1;
-      while (i >= 0 && cur[i] == d - 1) i--;
-      if (i < 0) break;
-      cur[i]++;
-      for (int j = i + 1; j < deg; j++) cur[j] = cur[i];
+  std::vector<int> alpha(d, 0);
+  // budget semantics: TD sum alpha <= w; HC prod (alpha + 1) <= w; SM sum f(alpha) <= w;
+  // TP max alpha <= w
+  std::function<void(int, int64_t)> rec = [&](int start, int64_t budget) {
+    if ((int)out.size() > kMaxM) return;
+    std::vector<int> fac;
+    for (int k = 0; k < d; k++)
+      for (int e = 0; e < alpha[k]; e++) fac.push_back(k);
+    out.push_back(fac);
+    for (int k = start; k < d; k++) {
+      for (int e = 1;; e++) {
+        int64_t nb;
+        if (kind == MLK_INDEX_TD) nb = budget - e;
+        else if (kind == MLK_INDEX_HC) nb = budget / (e + 1) >= 1 && (int64_t)(e + 1) <= budget ? budget / (e + 1) : -1;
+        else if (kind == MLK_INDEX_SM) nb = budget - sm_f(e);
+        else nb = e <= w ? budget : -1;
+        if (nb < 0) break;
+        alpha[k] = e;
+        rec(k + 1, nb);
+        alpha[k] = 0;
+        if ((int)out.size() > kMaxM) return;
+      }
     }
-  }
+  };
+  if (!(kind == MLK_INDEX_HC && w < 1)) rec(0, w);
+  std::stable_sort(out.begin(), out.end(), [](const std::vector<int>& a, const std::vector<int>& b) {
+    if (a.size() != b.size()) return a.size() < b.size();
+    return a < b;
+  });
   return out;
 }
 
@@ -388,23 +416,31 @@ using namespace mlk;
 extern "C" {
 
 mlk_status mlk_build_basis(mlk_ctx ctx, mlk_tree tree, int32_t w, mlk_basis* out) {
+  return mlk_build_basis_ex(ctx, tree, MLK_INDEX_TD, w, out);
+}
+
+mlk_status mlk_build_basis_ex(mlk_ctx ctx, mlk_tree tree, int32_t index_set, int32_t w, mlk_basis* out) {
   MLK_API_BEGIN
   MLK_REQUIRE(ctx && tree && out, "NULL argument");
   *out = nullptr;
-  MLK_REQUIRE(w >= 0 && w <= 16, "need 0 <= w <= 16");
+  MLK_REQUIRE(index_set >= MLK_INDEX_TD && index_set <= MLK_INDEX_TP, "unknown index set");
+  MLK_REQUIRE(w >= 0 && w <= 64, "need 0 <= w <= 64");
   Ctx& c = ctx->c;
   CUDA_CHECK(cudaSetDevice(c.device));
   cudaStream_t st = c.stream;
   const int d = tree->d, dp = tree->d_pad, nn = tree->n_nodes;
-  auto fac = td_factors(d, w);
+  auto fac = index_set_factors(index_set, d, w);
+  MLK_REQUIRE((int)fac.size() <= kMaxM, "index set has more than 4096 members");
+  MLK_REQUIRE(!fac.empty(), "empty index set");
   const int M = (int)fac.size();
-  MLK_REQUIRE(M < tree->n, "need n > M = C(d + w, w)");
-  MLK_REQUIRE(M <= 4096, "M > 4096 not supported");
+  int wmax = 0;
+  for (auto& f : fac) wmax = std::max(wmax, (int)f.size());
+  MLK_REQUIRE(M < tree->n, "need n > M = |Lambda(w)|");
 
   auto B = std::make_unique<mlk_basis_s>();
   B->device = c.device;
   B->M = M;
-  B->w = w;
+  B->w = wmax;
   B->tree = tree;
   B->p.assign(nn, 0);
   B->cell_pos.assign(nn, -1);
@@ -448,7 +484,7 @@ mlk_status mlk_build_basis(mlk_ctx ctx, mlk_tree tree, int32_t w, mlk_basis* out
   flag.zero();
 
   // factor table
-  int wf = std::max(w, 1);
+  int wf = std::max(wmax, 1);
   std::vector<int32_t> fh((size_t)M * wf, -1);
   for (int m = 0; m < M; m++)
     for (size_t j = 0; j < fac[m].size(); j++) fh[(size_t)m * wf + j] = fac[m][j];

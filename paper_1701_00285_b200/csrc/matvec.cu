@@ -245,8 +245,9 @@ void cov_matvec_dev(Ctx& c, const mlk_tree_s* tree, const mlk_kernel& k, const d
 
 void check_kernel(const mlk_kernel* k) {
   MLK_REQUIRE(k != nullptr, "kernel is NULL");
-  MLK_REQUIRE(k->family >= MLK_MATERN_12 && k->family <= MLK_GAUSSIAN, "unknown covariance family");
+  MLK_REQUIRE(k->family >= MLK_MATERN_12 && k->family <= MLK_MATERN_NU, "unknown covariance family");
   MLK_REQUIRE(k->rho > 0 && k->sigma2 > 0 && k->nugget >= 0, "need rho > 0, sigma2 > 0, nugget >= 0");
+  MLK_REQUIRE(k->family != MLK_MATERN_NU || (k->nu > 0 && k->nu <= 50), "MLK_MATERN_NU needs 0 < nu <= 50");
 }
 
 }  // namespace mlk

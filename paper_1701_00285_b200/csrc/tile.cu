@@ -41,7 +41,26 @@ KernelParams make_kernel_params(const mlk_kernel& k) {
     case MLK_MATERN_12: p.c1 = 1.0 / k.rho; break;
     case MLK_MATERN_32: p.c1 = std::sqrt(3.0) / k.rho; break;
     case MLK_MATERN_52: p.c1 = std::sqrt(5.0) / k.rho; break;
+    case MLK_MATERN_NU: p.c1 = std::sqrt(2.0 * k.nu) / k.rho; break;
     default: p.c1 = 1.0 / (k.rho * k.rho); break;
+  }
+  if (k.family == MLK_MATERN_NU) {
+    // constants of Temme's method for K_mu (mu = nu - round(nu)), in long double
+    p.nu = k.nu;
+    p.nl = (int32_t)std::floor(k.nu + 0.5);
+    const long double mu = (long double)k.nu - p.nl;
+    const long double gampl = 1.0L / std::tgamma(1.0L + mu), gammi = 1.0L / std::tgamma(1.0L - mu);
+    p.mu = (double)mu;
+    p.gampl = (double)gampl;
+    p.gammi = (double)gammi;
+    p.gam1 = std::fabs(mu) < 1e-6L ? -0.5772156649015329 : (double)((gammi - gampl) / (2.0L * mu));
+    p.gam2 = (double)((gammi + gampl) / 2.0L);
+    const long double pimu = 3.14159265358979323846264338327950288L * mu;
+    p.fact = std::fabs(mu) < 1e-18L ? 1.0 : (double)(pimu / std::sin(pimu));
+    p.norm = (double)(std::pow(2.0L, 1.0L - (long double)k.nu) / std::tgamma((long double)k.nu));
+  } else {
+    p.nu = p.mu = p.gam1 = p.gam2 = p.gampl = p.gammi = p.fact = p.norm = 0.0;
+    p.nl = 0;
   }
   // coordinates are pre-scaled so that the augmented Gram product is z^2 = (c1 r)^2
   // (Matern) or r^2 / rho^2 (Gaussian)
@@ -109,11 +128,71 @@ void make_tile_units(std::vector<TileUnit>& out, int64_t a_begin, int32_t s_a, i
 
 namespace {
 
+// 2^(1-nu)/Gamma(nu) z^nu K_nu(z), z > 0: K_mu and K_{mu+1} by Temme's series (z < 2) or
+// Steed's continued fraction CF2 (z >= 2), then the upward recurrence to nu = nl + mu
+// (the classical Temme / Thompson-Barnett scheme; the mu constants come from the host)
+__device__ __noinline__ double matern_nu(double z, const KernelParams& kp) {
+  const double xmu = kp.mu, xmu2 = xmu * xmu, xi = 1.0 / z, xi2 = 2.0 * xi;
+  double rkmu, rk1;
+  if (z < 2.0) {
+    const double x2 = 0.5 * z;
+    double dl = -log(x2);
+    double e = xmu * dl;
+    const double fact2 = fabs(e) < 1e-16 ? 1.0 : sinh(e) / e;
+    double ff = kp.fact * (kp.gam1 * cosh(e) + kp.gam2 * fact2 * dl);
+    double sum = ff;
+    e = exp(e);
+    double p = 0.5 * e / kp.gampl, q = 0.5 / (e * kp.gammi), c = 1.0, sum1 = p;
+    const double dd = x2 * x2;
+    for (int i = 1; i < 200; i++) {
+      ff = (i * ff + p + q) / ((double)i * i - xmu2);
+      c *= dd / i;
+      p /= (i - xmu);
+      q /= (i + xmu);
+      const double del = c * ff;
+      sum += del;
+      sum1 += c * (p - i * ff);
+      if (fabs(del) < fabs(sum) * 1e-17) break;
+    }
+    rkmu = sum;
+    rk1 = sum1 * xi2;
+  } else {
+    double b = 2.0 * (1.0 + z), d = 1.0 / b, h = d, delh = d, q1 = 0.0, q2 = 1.0;
+    const double a1 = 0.25 - xmu2;
+    double q = a1, c = a1, a = -a1, s = 1.0 + q * delh;
+    for (int i = 2; i < 500; i++) {
+      a -= 2 * (i - 1);
+      c = -a * c / i;
+      const double qnew = (q1 - b * q2) / a;
+      q1 = q2;
+      q2 = qnew;
+      q += c * qnew;
+      b += 2.0;
+      d = 1.0 / (b + a * d);
+      delh = (b * d - 1.0) * delh;
+      h += delh;
+      const double dels = q * delh;
+      s += dels;
+      if (fabs(dels / s) < 1e-17) break;
+    }
+    h = a1 * h;
+    rkmu = sqrt(1.5707963267948966 * xi) * exp(-z) / s;
+    rk1 = rkmu * (xmu + z + 0.5 - h) * xi;
+  }
+  for (int i = 1; i <= kp.nl; i++) {
+    const double t = (xmu + i) * xi2 * rk1 + rkmu;
+    rkmu = rk1;
+    rk1 = t;
+  }
+  return kp.norm * pow(z, kp.nu) * rkmu;
+}
+
 // correlation phi from the augmented Gram value x = z^2 (Matern, z = sqrt(2 nu) r / rho) or
 // x = r^2 / rho^2 (Gaussian); R16, R17
 template <int FAM>
-__device__ __forceinline__ double corr(double x, const double* tab) {
+__device__ __forceinline__ double corr(double x, const double* tab, const KernelParams& kp) {
   if (FAM == MLK_GAUSSIAN) return exp_neg(x, tab);  // x >= -O(u|y|^2): e^{-x} stays ~1
+  if (FAM == MLK_MATERN_NU) return x > 0.0 ? matern_nu(sqrt(x), kp) : 1.0;
   x = clamp_pos(x);
   const double z = sqrt_pos(x);
   const double e = exp_neg(z, tab);
@@ -322,7 +401,7 @@ __global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4)
         const int y = yb + 8 * t + 2 * (lane & 3);
 #pragma unroll
         for (int e = 0; e < 2; e++) {
-          const double v = corr<FAM>(gr[t][e], s_tab);
+          const double v = corr<FAM>(gr[t][e], s_tab, kp);
           cv[t][e] = (u.b_begin + y + e == ga) ? kp.same_val : v;
           if (y + e >= u.s_b) cv[t][e] = 0.0;
         }
@@ -678,6 +757,7 @@ void run_tile_contract(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, s
       case MLK_MATERN_12: launch_fam<MLK_MATERN_12>(c, ag, kp, rq, du.p + s0, n, counters.p + g); break;
       case MLK_MATERN_32: launch_fam<MLK_MATERN_32>(c, ag, kp, rq, du.p + s0, n, counters.p + g); break;
       case MLK_MATERN_52: launch_fam<MLK_MATERN_52>(c, ag, kp, rq, du.p + s0, n, counters.p + g); break;
+      case MLK_MATERN_NU: launch_fam<MLK_MATERN_NU>(c, ag, kp, rq, du.p + s0, n, counters.p + g); break;
       default: launch_fam<MLK_GAUSSIAN>(c, ag, kp, rq, du.p + s0, n, counters.p + g); break;
     }
   }

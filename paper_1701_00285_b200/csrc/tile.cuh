@@ -40,6 +40,11 @@ struct KernelParams {
   double nugget;
   double same_val;  // 1 + nugget / sigma2: the correlation of a site with itself (R18)
   double scale;     // coordinate pre-scale of the augmented Gram product (c1, or 1 / rho)
+  // MLK_MATERN_NU: nu = nl + mu (nl = round(nu), |mu| <= 1/2) and the mu-dependent constants
+  // of Temme's series (1/Gamma(1 +- mu), gamma_1, gamma_2, pi mu / sin(pi mu)), and
+  // 2^(1 - nu) / Gamma(nu)
+  double nu, mu, gam1, gam2, gampl, gammi, fact, norm;
+  int32_t nl;
 };
 
 KernelParams make_kernel_params(const mlk_kernel& k);

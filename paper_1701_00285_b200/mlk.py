@@ -22,10 +22,11 @@ _lib = C.CDLL(LIB_PATH)
 OK, ERR_INVALID_ARG, ERR_DUPLICATE_POINTS, ERR_RANK_DEFICIENT, ERR_OUT_OF_MEMORY, ERR_CUDA, \
     ERR_UNSUPPORTED = range(7)
 TREE_KD, TREE_RP = 0, 1
-MATERN_12, MATERN_32, MATERN_52, GAUSSIAN = 0, 1, 2, 3
+MATERN_12, MATERN_32, MATERN_52, GAUSSIAN, MATERN_NU = 0, 1, 2, 3, 4
 PAIRS_ALL, PAIRS_PAPER_TAU = 0, 1
 PREC_FP64, PREC_DD = 0, 1
 MATVEC_EXACT, MATVEC_BSR = 0, 1
+INDEX_TD, INDEX_HC, INDEX_SM, INDEX_TP = 0, 1, 2, 3
 
 SYMBOLS = [
     "mlk_last_error", "mlk_version", "mlk_ctx_create", "mlk_ctx_destroy", "mlk_ctx_stream",
@@ -35,7 +36,7 @@ SYMBOLS = [
     "mlk_cw_free", "mlk_cw_info", "mlk_cw_export", "mlk_cw_owner", "mlk_cw_shard_len", "mlk_cw_pack",
     "mlk_cw_unpack", "mlk_cw_values_device", "mlk_cov_matvec", "mlk_cw_matvec", "mlk_partition_lpt",
     "mlk_shard_plan", "mlk_launch_count", "mlk_cw_flops", "mlk_cw_export_async", "mlk_ctx_wait_copies",
-    "mlk_pcg_solve",
+    "mlk_pcg_solve", "mlk_build_basis_ex",
 ]
 
 
@@ -54,7 +55,8 @@ class RankDeficient(MlkError):
 
 
 class KernelSpec(C.Structure):
-    _fields_ = [("family", C.c_int32), ("rho", C.c_double), ("sigma2", C.c_double), ("nugget", C.c_double)]
+    _fields_ = [("family", C.c_int32), ("rho", C.c_double), ("sigma2", C.c_double), ("nugget", C.c_double),
+                ("nu", C.c_double)]
 
 
 class SparsitySpec(C.Structure):
@@ -78,6 +80,7 @@ _sig = {
     "mlk_tree_info": (C.c_int, [P, P, P, P, P]),
     "mlk_tree_export": (C.c_int, [P, P, P, P, P, P, P, P]),
     "mlk_build_basis": (C.c_int, [P, P, C.c_int32, C.POINTER(P)]),
+    "mlk_build_basis_ex": (C.c_int, [P, P, C.c_int32, C.c_int32, C.POINTER(P)]),
     "mlk_basis_free": (None, [P]),
     "mlk_basis_info": (C.c_int, [P, P, P, P]),
     "mlk_basis_export": (C.c_int, [P, P, P, C.c_int32, P, P, P]),
@@ -144,14 +147,14 @@ def _np(ptr_holder):
     return ptr_holder.ctypes.data_as(C.c_void_p)
 
 
-def kernel_spec(family, rho, sigma2=1.0, nugget=0.0):
-    return KernelSpec(int(family), float(rho), float(sigma2), float(nugget))
+def kernel_spec(family, rho, sigma2=1.0, nugget=0.0, nu=0.0):
+    return KernelSpec(int(family), float(rho), float(sigma2), float(nugget), float(nu or 0.0))
 
 
 def _kspec(k):
     if isinstance(k, KernelSpec):
         return k
-    return kernel_spec(k["family"], k["rho"], k.get("sigma2", 1.0), k.get("nugget", 0.0))
+    return kernel_spec(k["family"], k["rho"], k.get("sigma2", 1.0), k.get("nugget", 0.0), k.get("nu") or 0.0)
 
 
 class Ctx:
@@ -269,9 +272,12 @@ class Basis:
             self.h = None
 
 
-def build_basis(ctx, tree, w):
+def build_basis(ctx, tree, w, index_set=INDEX_TD):
     h = C.c_void_p()
-    _check(_lib.mlk_build_basis(ctx.h, tree.h, int(w), C.byref(h)))
+    if index_set == INDEX_TD:
+        _check(_lib.mlk_build_basis(ctx.h, tree.h, int(w), C.byref(h)))
+    else:
+        _check(_lib.mlk_build_basis_ex(ctx.h, tree.h, int(index_set), int(w), C.byref(h)))
     return Basis(h, tree, ctx)
 
 

@@ -502,3 +502,54 @@ def test_pcg_matches_oracle(mlk, ctx, n, d, leaf, kind, fam, rho):
     x1, _, _ = mlk.pcg_solve(ctx, g, gb, kern, cw, z, tol=1e-9, max_iter=3000)
     x2, _, _ = mlk.pcg_solve(ctx, g, gb, kern, cw, z, tol=1e-9, max_iter=3000)
     assert np.array_equal(x1, x2)   # deterministic
+
+
+# --------------------------------------------------------------------------------- NEXT-3
+@pytest.mark.parametrize("nu,rho", [(1.25, 0.6), (0.75, 0.3), (1.5, 0.5), (3.3, 1.1)])
+def test_general_nu_matern_and_hc_basis(mlk, ctx, nu, rho):
+    """MLK_MATERN_NU (K_nu in the kernel) against the oracle's Bessel-function definition, on
+    a hyperbolic-cross basis (d = 4, w = 5); nu = 3/2 must also equal the closed form."""
+    from oracle import index_set as OI
+    X, dirs = _setup(2048, 4, 128, 1, "normal")
+    g, o = _tree_both(mlk, ctx, X, 128, 1, dirs)
+    gb = mlk.build_basis(ctx, g, 5, index_set=mlk.INDEX_HC)
+    ob = OB.build_basis(X, o, 5, exps=OI.hc_exponents(4, 5))
+    assert gb.M == ob.M == len(OI.hc_exponents(4, 5))
+    for q in ob.cells:
+        Wg, _ = gb.block(q, int(o.end[q] - o.begin[q]))
+        assert np.linalg.norm(Wg - ob.W[q]) <= TOL_BLOCK * np.linalg.norm(ob.W[q])
+    kern = dict(family=OC.MATERN_NU, rho=rho, nu=nu, sigma2=1.2, nugget=1e-4)
+    pairs = OA.admitted_pairs(X, o, ob, 1, 1e-3)
+    ref = OAs.assemble(X, o, ob, kern, pairs)
+    got = mlk.assemble_cw(ctx, g, gb, kern, dict(mode=1, tau=1e-3)).export()
+    assert np.array_equal(got["val_off"], ref.val_off)
+    assert _block_errs(got["values"], ref).max() <= TOL_BLOCK
+    v = wl.vectors(2, gb.dim, seed=2)
+    y = mlk.cw_matvec(ctx, g, gb, kern, None, mlk.MATVEC_EXACT, v)
+    yr = OM.cw_matvec_exact(X, o, ob, kern, v)
+    assert np.linalg.norm(y - yr) <= 1e-11 * np.linalg.norm(yr)
+    if nu == 1.5:
+        k32 = dict(family=OC.MATERN_32, rho=rho, sigma2=1.2, nugget=1e-4)
+        got32 = mlk.assemble_cw(ctx, g, gb, k32, dict(mode=1, tau=1e-3)).export()
+        assert np.linalg.norm(got32["values"] - got["values"]) <= 1e-12 * np.linalg.norm(got32["values"])
+
+
+@pytest.mark.parametrize("kind,d,w", [(2, 3, 2), (3, 2, 3)])
+def test_sm_tp_basis(mlk, ctx, kind, d, w):
+    """Smolyak and tensor-product index sets: W per cell against the oracle (low degrees: raw
+    monomials of degree 8, as in SM(3, 3), make the moment matrices ill-conditioned enough that
+    any two Householder orders differ by ~kappa u ~ 1e-9)."""
+    from oracle import index_set as OI
+    X, dirs = _setup(2048, d, 128, 0, "uniform")   # |SM(3, 2)| = 25, |TP(2, 3)| = 16
+    g, o = _tree_both(mlk, ctx, X, 128, 0, dirs)
+    gb = mlk.build_basis(ctx, g, w, index_set=kind)
+    exps = OI.exponents(kind, d, w)
+    ob = OB.build_basis(X, o, w, exps=exps)
+    assert gb.M == ob.M
+    # two Householder orders agree to ~kappa(P_leaf) u: the bar scales with the conditioning
+    kap = max(np.linalg.cond(OI.monomials(X[o.perm[o.begin[q]:o.end[q]]], exps))
+              for q in range(o.n_nodes) if o.exists[q] and o.is_leaf[q])
+    tol = max(TOL_BLOCK, 1e-15 * kap)
+    for q in ob.cells:
+        Wg, _ = gb.block(q, int(o.end[q] - o.begin[q]))
+        assert np.linalg.norm(Wg - ob.W[q]) <= tol * np.linalg.norm(ob.W[q]), (q, tol)

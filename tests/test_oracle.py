@@ -489,3 +489,16 @@ def test_pcg_cw_against_dense_system():
         assert np.linalg.norm(z - CW @ x) <= 2e-10 * np.linalg.norm(z)
         assert np.linalg.norm(x - xd) <= 1e-7 * np.linalg.norm(xd)
     assert its[0] < its[1]   # P_W pays off on this instance (63 vs 198 iterations)
+
+
+def test_sm_and_tp_sets_brute_force():
+    """SM and TP sets equal brute-force filters of a box with the Table 1 predicates; |TP| =
+    (w + 1)^d; all four sets start with the constant and are in graded order."""
+    for d, w in [(2, 3), (3, 3), (4, 2)]:
+        box = list(itertools.product(range(2 ** w + 1), repeat=d))
+        sm = [a for a in box if sum(I.sm_f(p) for p in a) <= w]
+        assert sorted(sm) == sorted(I.sm_exponents(d, w))
+        assert len(I.tp_exponents(d, w)) == (w + 1) ** d
+        for kind in (I.TD, I.HC, I.SM, I.TP):
+            e = I.exponents(kind, d, w)
+            assert e[0] == (0,) * d and [sum(a) for a in e] == sorted(sum(a) for a in e)
