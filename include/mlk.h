@@ -131,7 +131,14 @@ mlk_status mlk_build_basis(mlk_ctx ctx, mlk_tree tree, int32_t w, mlk_basis* out
  * (SM, sum f(p_i) <= w, f(0) = 0, f(1) = 1, f(p) = ceil(log2 p)) or tensor product (TP,
  * max p_i <= w), in the graded order of reading R8.  M <= 4096. */
 typedef enum { MLK_INDEX_TD = 0, MLK_INDEX_HC = 1, MLK_INDEX_SM = 2, MLK_INDEX_TP = 3 } mlk_index_set;
-mlk_status mlk_build_basis_ex(mlk_ctx ctx, mlk_tree tree, int32_t index_set, int32_t w, mlk_basis* out);
+/* flags: MLK_BASIS_KEEP_DEFICIENT keeps p = M wavelet-free directions in a numerically rank-
+ * deficient cell instead of failing (reading R24: the paper's Table 1 sphere workload, where
+ * sum x_i^2 = 1 makes the HC moment matrix rank M - 1, is built with p = M -- its Size column
+ * 20592 = 8 (4000 - 1426)).  W stays orthonormal and annihilates the polynomials; only the
+ * direction of the deficient column inside the cell is then set by rounding. */
+#define MLK_BASIS_KEEP_DEFICIENT 1
+mlk_status mlk_build_basis_ex(mlk_ctx ctx, mlk_tree tree, int32_t index_set, int32_t w, int32_t flags,
+                              mlk_basis* out);
 void mlk_basis_free(mlk_basis basis); /* NULL-safe */
 /* M; dim = N - M rows of W; n_cells = cells with at least one wavelet. */
 mlk_status mlk_basis_info(mlk_basis basis, int32_t* M, int64_t* dim, int32_t* n_cells);

@@ -83,6 +83,7 @@ struct mlk_basis_s {
   cudaEvent_t ready = nullptr;
   mlk::DevBuf<int> merge_flag;
   mutable bool ready_checked = false;
+  bool keep_deficient = false;     // MLK_BASIS_KEEP_DEFICIENT
 };
 
 struct mlk_cw_s {

@@ -402,7 +402,8 @@ void basis_sync(const mlk_basis_s* B) {
   int f = 0;
   CUDA_CHECK(cudaMemcpy(&f, B->merge_flag.p, sizeof(int), cudaMemcpyDeviceToHost));
   B->ready_checked = true;
-  if (f) throw Error(MLK_ERR_RANK_DEFICIENT, "merged moment matrix is rank deficient (|R_kk| <= 1e-13 max|R_ii|)");
+  if (f && !B->keep_deficient)
+    throw Error(MLK_ERR_RANK_DEFICIENT, "merged moment matrix is rank deficient (|R_kk| <= 1e-13 max|R_ii|)");
 }
 
 void basis_wait(Ctx& c, const mlk_basis_s* B) {
@@ -416,10 +417,11 @@ using namespace mlk;
 extern "C" {
 
 mlk_status mlk_build_basis(mlk_ctx ctx, mlk_tree tree, int32_t w, mlk_basis* out) {
-  return mlk_build_basis_ex(ctx, tree, MLK_INDEX_TD, w, out);
+  return mlk_build_basis_ex(ctx, tree, MLK_INDEX_TD, w, 0, out);
 }
 
-mlk_status mlk_build_basis_ex(mlk_ctx ctx, mlk_tree tree, int32_t index_set, int32_t w, mlk_basis* out) {
+mlk_status mlk_build_basis_ex(mlk_ctx ctx, mlk_tree tree, int32_t index_set, int32_t w, int32_t flags,
+                              mlk_basis* out) {
   MLK_API_BEGIN
   MLK_REQUIRE(ctx && tree && out, "NULL argument");
   *out = nullptr;
@@ -536,8 +538,10 @@ mlk_status mlk_build_basis_ex(mlk_ctx ctx, mlk_tree tree, int32_t index_set, int
   trace.mark("leaves");
   {
     auto fl = flag.download(1);
-    if (fl[0]) throw Error(MLK_ERR_RANK_DEFICIENT, "moment matrix is rank deficient (|R_kk| <= 1e-13 max|R_ii|)");
+    if (fl[0] && !(flags & MLK_BASIS_KEEP_DEFICIENT))
+      throw Error(MLK_ERR_RANK_DEFICIENT, "moment matrix is rank deficient (|R_kk| <= 1e-13 max|R_ii|)");
   }
+  B->keep_deficient = (flags & MLK_BASIS_KEEP_DEFICIENT) != 0;
   trace.mark("leaf_check");
   // ---- internal levels, bottom-up, on the auxiliary stream: the call returns while they run
   // ([R_L; R_R] has full column rank whenever R_L does, so the synchronous leaf check above is

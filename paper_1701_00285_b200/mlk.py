@@ -80,7 +80,7 @@ _sig = {
     "mlk_tree_info": (C.c_int, [P, P, P, P, P]),
     "mlk_tree_export": (C.c_int, [P, P, P, P, P, P, P, P]),
     "mlk_build_basis": (C.c_int, [P, P, C.c_int32, C.POINTER(P)]),
-    "mlk_build_basis_ex": (C.c_int, [P, P, C.c_int32, C.c_int32, C.POINTER(P)]),
+    "mlk_build_basis_ex": (C.c_int, [P, P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(P)]),
     "mlk_basis_free": (None, [P]),
     "mlk_basis_info": (C.c_int, [P, P, P, P]),
     "mlk_basis_export": (C.c_int, [P, P, P, C.c_int32, P, P, P]),
@@ -272,12 +272,15 @@ class Basis:
             self.h = None
 
 
-def build_basis(ctx, tree, w, index_set=INDEX_TD):
+BASIS_KEEP_DEFICIENT = 1
+
+
+def build_basis(ctx, tree, w, index_set=INDEX_TD, flags=0):
     h = C.c_void_p()
-    if index_set == INDEX_TD:
+    if index_set == INDEX_TD and flags == 0:
         _check(_lib.mlk_build_basis(ctx.h, tree.h, int(w), C.byref(h)))
     else:
-        _check(_lib.mlk_build_basis_ex(ctx.h, tree.h, int(index_set), int(w), C.byref(h)))
+        _check(_lib.mlk_build_basis_ex(ctx.h, tree.h, int(index_set), int(w), int(flags), C.byref(h)))
     return Basis(h, tree, ctx)
 
 

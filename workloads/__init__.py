@@ -14,7 +14,7 @@ import math
 import numpy as np
 
 KD, RP = 0, 1
-MATERN_12, MATERN_32, MATERN_52, GAUSSIAN = 0, 1, 2, 3
+MATERN_12, MATERN_32, MATERN_52, GAUSSIAN, MATERN_NU = 0, 1, 2, 3, 4
 PAIRS_ALL, PAIRS_PAPER_TAU = 0, 1
 
 CONFIGS = {
@@ -30,6 +30,11 @@ CONFIGS = {
                  nugget=0.0, pairs=PAIRS_PAPER_TAU, tau=1e-7, points="mixture"),
     "cfg5": dict(n=1048576, d=50, w=2, leaf=2048, tree=RP, family=GAUSSIAN, rho=4.0, sigma2=1.0,
                  nugget=1e-6, pairs=PAIRS_PAPER_TAU, tau=1e-7, points="uniform"),
+    # NEXT-3: the paper's own Table 1 workload: N = 32 000 points on
+    # the sphere S^49 (d = 50), hyperbolic cross w = 5 (p = 1426), Matern nu = 1.25, rho = 10,
+    # RP tree with t = 3 (leaf 4000), tau = 1e-6
+    "paper_t1": dict(n=32000, d=50, w=5, leaf=4000, tree=RP, family=MATERN_NU, rho=10.0, sigma2=1.0,
+                     nugget=0.0, pairs=PAIRS_PAPER_TAU, tau=1e-6, points="sphere", index_set=1, nu=1.25),
 }
 
 
@@ -85,7 +90,8 @@ def make(name_or_cfg, n=None, seed=0):
 
 
 def kernel_dict(cfg):
-    return dict(family=cfg["family"], rho=cfg["rho"], sigma2=cfg["sigma2"], nugget=cfg["nugget"])
+    return dict(family=cfg["family"], rho=cfg["rho"], sigma2=cfg["sigma2"], nugget=cfg["nugget"],
+                nu=cfg.get("nu"))
 
 
 def mtd(d, w):
