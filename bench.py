@@ -218,7 +218,8 @@ def main():
 
     def step(X, D, v_host=None, out_vals=None, out_y=None):
         tr = timed("build_tree", mlk.build_tree, ctx, X, c["leaf"], c["tree"], D)
-        B = timed("build_basis", mlk.build_basis, ctx, tr, c["w"])
+        B = timed("build_basis", mlk.build_basis, ctx, tr, c["w"], c.get("index_set", 0),
+                  mlk.BASIS_KEEP_DEFICIENT if c.get("index_set", 0) else 0)
         cw = timed("assemble_cw", mlk.assemble_cw, ctx, tr, B, kern, spars)
         if ws > 1:
             timed("gather_cw", mlk.gather_cw, ctx, cw)
@@ -317,7 +318,8 @@ def main():
     pcg = None
     if args.pcg_tol > 0 and ws == 1:
         trp = mlk.build_tree(ctx, X_d, c["leaf"], c["tree"], dirs_d)
-        Bp = mlk.build_basis(ctx, trp, c["w"])
+        Bp = mlk.build_basis(ctx, trp, c["w"], c.get("index_set", 0),
+                             mlk.BASIS_KEEP_DEFICIENT if c.get("index_set", 0) else 0)
         cwp = mlk.assemble_cw(ctx, trp, Bp, kern, spars)
         zp = torch.from_numpy(wl.vectors(1, Bp.dim, seed=9)[0]).to(dev)
         gp = torch.empty_like(zp)
