@@ -122,8 +122,10 @@ struct GemmDesc {
   int32_t m, n, k;
   int32_t trans_c;
   int64_t diag = -1;  // >= 0: store [i + diag == j] - (A B)[i][j] instead of (A B)[i][j]
+  int32_t sub = 0;    // 1: C -= A B (read-modify-write; not with diag)
 };
-// Launch all products on the context stream with FP64 DMMA tiles (64 x 64 x 16); large k
+// Launch all products on the context stream with FP64 DMMA tiles (64 x 64, 72 x 72 or
+// 64 x 32, by padded volume; k steps of 16); large k
 // is split into fixed chunks whose partial tiles are reduced in chunk order (deterministic).
 void gemm_batched(Ctx& c, const std::vector<GemmDesc>& descs, const char* name);
 }  // namespace mlk

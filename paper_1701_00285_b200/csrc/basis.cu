@@ -332,10 +332,339 @@ __global__ void k_stack_r(const StackJob* __restrict__ jobs, int M) {
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Blocked Householder QR for matrices that do not fit in shared memory (LAPACK dgeqrf: dgeqr2
+// panels + dlarft + dlarfb, so the reflectors are those of the unblocked kernel above).  The
+// job's matrix is augmented to [A | I] (column-major, lda = m); each 32-column panel is
+// factorised by one CTA (k_qr_panel) and its block reflector B_p^T = I - V_p T_p^T V_p^T is
+// applied to every trailing column on the DMMA GEMM:
+//     Wt = A_tr^T (V_p T_p)            (ntr x 32, k = m - c0)
+//     A_tr^T -= Wt V_p^T               (ntr x (m - c0), k = 32)
+// The identity columns end up holding Q^T I = Q^T, which k_qr_export copies to qlo / qhi.
+constexpr int kPanelKB = 32;
+constexpr int kPanelThreads = 512;
+constexpr int kPanelWarps = kPanelThreads / 32;
+
+struct PanelJob {
+  double* A;    // [A | I], column-major, lda = m
+  int32_t m;
+  double* VT;   // (m - c0) x 32 row-major: V_p T_p
+  double* Vt;   // 32 x (m - c0) row-major (ld m): V_p^T, unit diagonal and zeros made explicit
+};
+
+// lane c ends with sum over the warp of v[c] (recursive halving; 31 shuffles, fixed order)
+__device__ __forceinline__ double warp_reduce_scatter32(double (&v)[32], int lane) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const bool up = (lane & s) != 0;
+#pragma unroll
+    for (int i = 0; i < s; i++) {
+      const double send = up ? v[i] : v[i + s];
+      const double keep = up ? v[i + s] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+  }
+  return v[0];
+}
+
+// Panel columns c0 .. c0 + kb - 1 (kb <= 32), rows c0 .. m - 1, in the dgeqr2 convention of
+// k_qr_wy.  Thread t owns the rows c0 + t + i * 512; step l does ONE pass over the panel that
+// (a) scales x_l into v_l, (b) applies H_l to the columns j > l, (c) accumulates the dots of
+// step l + 1 (x_{l+1} . a_j, j > l) and (d) the Gram column G[q][l] = v_q . v_l (q < l) that
+// dlarft needs — 32 slots, reduced once per step (warp reduce-scatter, then 16 warp partials
+// summed in order by warp 0, which then forms the next reflector).  Two barriers per step.
+__global__ void __launch_bounds__(kPanelThreads) k_qr_panel(const PanelJob* __restrict__ jobs, int c0, int kb) {
+  __shared__ double red[kPanelWarps][kPanelKB + 1];
+  __shared__ double Gp[kPanelKB][kPanelKB + 1];  // Gp[q][l], q < l
+  __shared__ double Tp[kPanelKB][kPanelKB + 1];
+  __shared__ double dsum[kPanelKB];               // dots of the current step, by column
+  __shared__ double gcol[kPanelKB];               // f_j * scal of the current step
+  __shared__ double taus[kPanelKB];
+  __shared__ double s_scal;
+  const PanelJob jb = jobs[blockIdx.x];
+  const int m = jb.m;
+  const int64_t lda = m;
+  double* __restrict__ A = jb.A;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  auto col = [&](int j) { return A + (int64_t)(c0 + j) * lda; };
+
+  // warp 0: reflector of step l from dsum, then f_j for the columns j > l (row k updated)
+  auto pivot = [&](int l) {
+    const int k = c0 + l;
+    double tau = 0.0, scal = 1.0, beta = 0.0;
+    if (lane == 0) {
+      const double alpha = col(l)[k], sum = dsum[l];
+      beta = alpha;
+      if (sum > 0.0) {
+        beta = -copysign(sqrt(fma(alpha, alpha, sum)), alpha);
+        tau = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+    }
+    tau = __shfl_sync(0xffffffffu, tau, 0);
+    scal = __shfl_sync(0xffffffffu, scal, 0);
+    if (lane > l && lane < kb) {
+      double* aj = col(lane);
+      const double a = aj[k];
+      const double f = tau * fma(scal, dsum[lane], a);
+      aj[k] = a - f;
+      gcol[lane] = f * scal;
+    }
+    if (lane == 0) {
+      col(l)[k] = beta;
+      taus[l] = tau;
+      s_scal = scal;
+    }
+  };
+
+  double p[kPanelKB];
+  // initial dots x_0 . a_j over the rows below c0
+#pragma unroll
+  for (int j = 0; j < kPanelKB; j++) p[j] = 0.0;
+  for (int r = c0 + 1 + tid; r < m; r += kPanelThreads) {
+    const double x = col(0)[r];
+#pragma unroll
+    for (int j = 0; j < kPanelKB; j++)
+      if (j < kb) p[j] = fma(x, col(j)[r], p[j]);
+  }
+  {
+    const double s = warp_reduce_scatter32(p, lane);
+    red[warp][lane] = s;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kPanelWarps; w++) s += red[w][lane];
+    dsum[lane] = s;
+    __syncwarp();
+    pivot(0);
+  }
+  __syncthreads();
+  for (int l = 0; l < kb; l++) {
+    const int k = c0 + l;
+    const double scal = s_scal;
+#pragma unroll
+    for (int j = 0; j < kPanelKB; j++) p[j] = 0.0;
+    const double* ak = col(l);
+    for (int r = c0 + tid; r < m; r += kPanelThreads) {
+      if (r <= k) continue;
+      const double x = ak[r];
+      const double v = x * scal;
+      col(l)[r] = v;
+#pragma unroll
+      for (int q = 0; q < kPanelKB; q++)
+        if (q < l) p[q] = fma(v, col(q)[r], p[q]);
+      double xn = 0.0;
+      if (l + 1 < kb && r > k + 1) xn = fma(-gcol[l + 1], x, col(l + 1)[r]);
+#pragma unroll
+      for (int j = 0; j < kPanelKB; j++) {
+        if (j > l && j < kb) {
+          double* aj = col(j);
+          const double y = fma(-gcol[j], x, aj[r]);
+          aj[r] = y;
+          p[j] = fma(xn, y, p[j]);
+        }
+      }
+    }
+    {
+      const double s = warp_reduce_scatter32(p, lane);
+      red[warp][lane] = s;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < kPanelWarps; w++) s += red[w][lane];
+      if (lane < l) Gp[lane][l] = s + col(lane)[k];   // + v_q[k] * v_l[k] (v_l[k] = 1)
+      if (lane > l) dsum[lane] = s;
+      __syncwarp();
+      if (l + 1 < kb) pivot(l + 1);
+    }
+    __syncthreads();
+  }
+  // dlarft (forward, columnwise): T[l][l] = tau_l, T[0:l, l] = -tau_l T[0:l, 0:l] G[0:l, l]
+  if (warp == 0) {
+    for (int l = 0; l < kPanelKB; l++) {
+      double t = 0.0;
+      if (l < kb) {
+        if (lane < l) {
+          double s = 0.0;
+          for (int q = lane; q < l; q++) s = fma(Tp[lane][q], Gp[q][l], s);
+          t = -taus[l] * s;
+        } else if (lane == l) {
+          t = taus[l];
+        }
+      }
+      Tp[lane][l] = t;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // V_p^T (explicit) and V_p T_p, rows c0 .. m - 1
+  for (int r = c0 + tid; r < m; r += kPanelThreads) {
+    const int rho = r - c0;
+    double v[kPanelKB];
+#pragma unroll
+    for (int l = 0; l < kPanelKB; l++) {
+      v[l] = l < kb ? (rho == l ? 1.0 : (rho > l ? col(l)[r] : 0.0)) : 0.0;
+      jb.Vt[(int64_t)l * m + rho] = v[l];
+    }
+    double* vt = jb.VT + (int64_t)rho * kPanelKB;
+#pragma unroll
+    for (int j = 0; j < kPanelKB; j++) {
+      double s = 0.0;
+#pragma unroll
+      for (int l = 0; l <= j; l++) s = fma(v[l], Tp[l][j], s);
+      vt[j] = s;
+    }
+  }
+}
+
+// [A | I] from the job's column-major A
+__global__ void k_qr_aug_init(const QrJob* __restrict__ jobs, double* const* __restrict__ aug, int nc) {
+  const QrJob jb = jobs[blockIdx.y];
+  double* X = aug[blockIdx.y];
+  const int64_t m = jb.m, tot = m * (nc + m);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / m, i = e - j * m;
+    X[e] = j < nc ? jb.A[e] : (i == j - nc ? 1.0 : 0.0);
+  }
+}
+
+// R (row-major) and the rank test of reading R9 from the factorised [A | I]
+__global__ void k_qr_export_r(const QrJob* __restrict__ jobs, double* const* __restrict__ aug, int nc,
+                              int* __restrict__ rank_flag) {
+  const QrJob jb = jobs[blockIdx.x];
+  const double* X = aug[blockIdx.x];
+  const int64_t m = jb.m;
+  for (int e = threadIdx.x; e < nc * nc; e += blockDim.x) {
+    const int i = e / nc, j = e - i * nc;
+    jb.R[e] = j >= i ? X[(int64_t)j * m + i] : 0.0;
+  }
+  if (threadIdx.x == 0) {
+    double mx = 0.0, mn = INFINITY;
+    for (int i = 0; i < nc; i++) {
+      const double v = fabs(X[(int64_t)i * m + i]);
+      mx = fmax(mx, v);
+      mn = fmin(mn, v);
+    }
+    if (!(mn > 1e-13 * mx)) atomicExch(rank_flag, 1);
+  }
+}
+
+// Q^T[i][j] = X[(nc + j) * m + i]: rows i < nc to qlo, rows i >= nc to qhi (32 x 32 tiles
+// through shared memory, both sides coalesced)
+__global__ void k_qr_export_q(const QrJob* __restrict__ jobs, double* const* __restrict__ aug, int nc) {
+  __shared__ double t[32][33];
+  const QrJob jb = jobs[blockIdx.z];
+  const double* X = aug[blockIdx.z];
+  const int m = jb.m;
+  const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+  if (i0 >= m || j0 >= m) return;
+  for (int jj = threadIdx.y; jj < 32; jj += blockDim.y) {
+    const int i = i0 + threadIdx.x, j = j0 + jj;
+    if (i < m && j < m) t[jj][threadIdx.x] = X[(int64_t)(nc + j) * m + i];
+  }
+  __syncthreads();
+  for (int ii = threadIdx.y; ii < 32; ii += blockDim.y) {
+    const int i = i0 + ii, j = j0 + threadIdx.x;
+    if (i < m && j < m) {
+      double* row = i < nc ? jb.qlo + (int64_t)i * jb.ldq : jb.qhi + (int64_t)(i - nc) * jb.ldq;
+      row[j] = t[threadIdx.x][ii];
+    }
+  }
+}
+
+void run_qr_blocked(Ctx& c, const std::vector<QrJob>& all, int nc, int* flag, const char* name) {
+  // group jobs so that the augmented matrices and the panel scratch stay within the budget
+  const int64_t budget = c.scratch_budget_bytes();
+  size_t first = 0;
+  while (first < all.size()) {
+    size_t last = first;
+    int64_t bytes = 0;
+    while (last < all.size()) {
+      const int64_t m = all[last].m;
+      const int64_t b = (m * (nc + m) + 2 * m * kPanelKB + (int64_t)(nc + m) * kPanelKB) * 8;
+      if (last > first && bytes + b > budget) break;
+      bytes += b;
+      last++;
+    }
+    std::vector<QrJob> jobs(all.begin() + first, all.begin() + last);
+    first = last;
+    const size_t nj = jobs.size();
+    int m_max = 0;
+    int64_t tot = 0;
+    for (auto& j : jobs) {
+      m_max = std::max(m_max, j.m);
+      tot += (int64_t)j.m * (nc + j.m) + 2 * (int64_t)j.m * kPanelKB + (int64_t)(nc + j.m) * kPanelKB;
+    }
+    DevBuf<double> scratch(tot, c.stream);
+    std::vector<double*> augp(nj), wtp(nj);
+    std::vector<PanelJob> pj(nj);
+    int64_t off = 0;
+    for (size_t i = 0; i < nj; i++) {
+      const int64_t m = jobs[i].m;
+      augp[i] = scratch.p + off;
+      off += m * (nc + m);
+      pj[i] = {augp[i], (int32_t)m, scratch.p + off, scratch.p + off + m * kPanelKB};
+      off += 2 * m * kPanelKB;
+      wtp[i] = scratch.p + off;
+      off += (int64_t)(nc + m) * kPanelKB;
+    }
+    DevBuf<QrJob> dj(nj, c.stream);
+    dj.upload(jobs);
+    DevBuf<double*> daug(nj, c.stream);
+    daug.upload(augp);
+    DevBuf<PanelJob> dpj(nj, c.stream);
+    dpj.upload(pj);
+    TimedLaunch tl(c, name);
+    {
+      dim3 grid((unsigned)std::min<int64_t>(1024, ceil_div((int64_t)m_max * (nc + m_max), 256)), (unsigned)nj);
+      k_qr_aug_init<<<grid, 256, 0, c.stream>>>(dj.p, daug.p, nc);
+      check_launch("k_qr_aug_init");
+    }
+    for (int c0 = 0; c0 < nc; c0 += kPanelKB) {
+      const int kb = std::min(kPanelKB, nc - c0);
+      k_qr_panel<<<(unsigned)nj, kPanelThreads, 0, c.stream>>>(dpj.p, c0, kb);
+      check_launch("k_qr_panel");
+      std::vector<GemmDesc> g1, g3;
+      for (size_t i = 0; i < nj; i++) {
+        const int32_t m = jobs[i].m;
+        const int32_t ntr = nc + m - c0 - kb, mr = m - c0;
+        double* Atr = augp[i] + (int64_t)(c0 + kb) * m + c0;  // row-major view: A_tr^T, ld m
+        GemmDesc a{Atr, m, pj[i].VT, kPanelKB, wtp[i], kPanelKB, ntr, kb, mr, 0};
+        GemmDesc b{wtp[i], kPanelKB, pj[i].Vt, m, Atr, m, ntr, mr, kb, 0};
+        b.sub = 1;
+        g1.push_back(a);
+        g3.push_back(b);
+      }
+      gemm_batched(c, g1, "qr_panel_w");
+      gemm_batched(c, g3, "qr_panel_update");
+    }
+    k_qr_export_r<<<(unsigned)nj, 256, 0, c.stream>>>(dj.p, daug.p, nc, flag);
+    check_launch("k_qr_export_r");
+    {
+      const unsigned tq = (unsigned)ceil_div(m_max, 32);
+      k_qr_export_q<<<dim3(tq, tq, (unsigned)nj), dim3(32, 8), 0, c.stream>>>(dj.p, daug.p, nc);
+      check_launch("k_qr_export_q");
+    }
+  }
+}
+
 // QR of every job (one CTA each), then Q^T = I - V W1T on the DMMA GEMM, rows < nc to qlo and
-// rows >= nc to qhi.
+// rows >= nc to qhi.  Matrices beyond shared memory (or MLK_QR_BLOCKED=1) take the blocked path.
 void run_qr(Ctx& c, std::vector<QrJob>& jobs, int nc, int* flag, const char* name) {
   if (jobs.empty()) return;
+  {
+    int mm = 0;
+    for (auto& j : jobs) mm = std::max(mm, j.m);
+    const char* eb = std::getenv("MLK_QR_BLOCKED");
+    if (qr_smem(mm, nc, true, false) > (size_t)kQrSmemLimit || (eb && eb[0] == '1')) {
+      run_qr_blocked(c, jobs, nc, flag, name);
+      return;
+    }
+  }
   int m_max = 0;
   for (auto& j : jobs) m_max = std::max(m_max, j.m);
   // scratch for V, T, W1T

@@ -1,8 +1,10 @@
 // Batched variable-size FP64 GEMM on DMMA.8x8x4 (row-major NN, optional transposed store).
-// Used for the basis transfers Phi_q/W_q = Q^T (Phi_L (+) Phi_R) and for the second
-// contraction B = W_a U of the assembly.  Two tilings, chosen per product by the smaller
-// padded volume: 64 x 64 (2 x 2 warps of 32 x 32) and 72 x 72 (3 x 3 warps of 24 x 24; the
-// p = 66 products of cfg2 pad to 72 instead of 128).  k steps of 16 with cp.async double
+// Used for the basis transfers Phi_q/W_q = Q^T (Phi_L (+) Phi_R), the blocked QR's trailing
+// updates and the second contraction B = W_a U of the assembly.  Three tilings, chosen per
+// product by the smallest padded volume: 64 x 64 (2 x 2 warps of 32 x 32), 72 x 72 (3 x 3
+// warps of 24 x 24; the p = 66 products of cfg2 pad to 72 instead of 128) and 64 x 32 (the
+// 32-column panel products of the blocked QR).  Every output element accumulates over k in the
+// same order under every tiling, so the choice does not change results.  k steps of 16 with cp.async double
 // buffering; k > KCHUNK is split into fixed chunks reduced in order (deterministic).
 #include <algorithm>
 
@@ -24,6 +26,7 @@ struct GemmCfg {
 };
 using Cfg64 = GemmCfg<4, 4, 2, 2>;
 using Cfg72 = GemmCfg<3, 3, 3, 3>;
+using Cfg32 = GemmCfg<4, 2, 2, 2>;
 
 struct GemmJob {
   int32_t desc;
@@ -111,8 +114,9 @@ __global__ void __launch_bounds__(32 * WM * WN) k_gemm(const GemmDesc* __restric
           if (gm < g.m && gn < g.n) {
             double v = acc[i][j][e];
             if (g.diag >= 0) v = ((int64_t)gm + g.diag == gn ? 1.0 : 0.0) - v;
-            if (g.trans_c) g.C[(int64_t)gn * g.ldc + gm] = v;
-            else g.C[(int64_t)gm * g.ldc + gn] = v;
+            double* cp = g.trans_c ? g.C + (int64_t)gn * g.ldc + gm : g.C + (int64_t)gm * g.ldc + gn;
+            if (g.sub) v = *cp - v;
+            *cp = v;
           }
         }
       }
@@ -137,8 +141,9 @@ __global__ void k_gemm_reduce(const GemmDesc* __restrict__ descs, const ReduceJo
     double s = 0.0;
     for (int p = 0; p < job.nparts; p++) s += partials[(job.first + p) * BM * BN + e];
     if (g.diag >= 0) s = ((int64_t)gm + g.diag == gn ? 1.0 : 0.0) - s;
-    if (g.trans_c) g.C[(int64_t)gn * g.ldc + gm] = s;
-    else g.C[(int64_t)gm * g.ldc + gn] = s;
+    double* cp = g.trans_c ? g.C + (int64_t)gn * g.ldc + gm : g.C + (int64_t)gm * g.ldc + gn;
+    if (g.sub) s = *cp - s;
+    *cp = s;
   }
 }
 
@@ -188,18 +193,22 @@ void run_tiling(Ctx& c, const GemmDesc* dd, const std::vector<GemmDesc>& descs, 
 
 void gemm_batched(Ctx& c, const std::vector<GemmDesc>& descs, const char* name) {
   if (descs.empty()) return;
-  std::vector<int32_t> s64, s72;
+  std::vector<int32_t> s64, s72, s32;
   for (int32_t di = 0; di < (int32_t)descs.size(); di++) {
     const GemmDesc& g = descs[di];
     if (g.m <= 0 || g.n <= 0) continue;
-    (padded(g, Cfg72::BM, Cfg72::BN) < padded(g, Cfg64::BM, Cfg64::BN) ? s72 : s64).push_back(di);
+    const int64_t v64 = padded(g, Cfg64::BM, Cfg64::BN), v72 = padded(g, Cfg72::BM, Cfg72::BN),
+                  v32 = padded(g, Cfg32::BM, Cfg32::BN);
+    if (v32 < std::min(v64, v72)) s32.push_back(di);
+    else (v72 < v64 ? s72 : s64).push_back(di);
   }
-  if (s64.empty() && s72.empty()) return;
+  if (s64.empty() && s72.empty() && s32.empty()) return;
   DevBuf<GemmDesc> dd(descs.size(), c.stream);
   dd.upload(descs);
   TimedLaunch tl(c, name);
   if (!s72.empty()) run_tiling<Cfg72, 3, 3, 3, 3>(c, dd.p, descs, s72);
   if (!s64.empty()) run_tiling<Cfg64, 4, 4, 2, 2>(c, dd.p, descs, s64);
+  if (!s32.empty()) run_tiling<Cfg32, 4, 2, 2, 2>(c, dd.p, descs, s32);
 }
 
 }  // namespace mlk

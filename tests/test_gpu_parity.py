@@ -553,3 +553,35 @@ def test_sm_tp_basis(mlk, ctx, kind, d, w):
     for q in ob.cells:
         Wg, _ = gb.block(q, int(o.end[q] - o.begin[q]))
         assert np.linalg.norm(Wg - ob.W[q]) <= tol * np.linalg.norm(ob.W[q]), (q, tol)
+
+
+# --------------------------------------------------------------------------------- blocked QR
+@pytest.mark.parametrize("n,d,w,leaf,force", [
+    (4096, 10, 3, 512, False),   # M = 286 > shared memory: 32-column panels, ragged last panel
+    (4096, 10, 2, 256, True),    # cfg2 shape (M = 66) forced through the blocked path
+    (3000, 3, 2, 100, True),     # ragged leaves, M = 10 < one panel
+])
+def test_blocked_qr_basis(mlk, ctx, n, d, w, leaf, force, monkeypatch):
+    """The blocked Householder QR (dgeqr2 panels + block reflectors on the DMMA GEMM) gives the
+    oracle's W per cell, an orthonormal basis and W P(X) = 0; forced on small M it also agrees
+    with the shared-memory kernel."""
+    X, dirs = _setup(n, d, leaf, 1)
+    g, o = _tree_both(mlk, ctx, X, leaf, 1, dirs)
+    if force:
+        ref_gpu = mlk.build_basis(ctx, g, w)
+        monkeypatch.setenv("MLK_QR_BLOCKED", "1")
+    gb = mlk.build_basis(ctx, g, w)
+    ob = OB.build_basis(X, o, w)
+    Wd = np.zeros((gb.dim, n))
+    for i, q in enumerate(gb.cells):
+        Wg, _ = gb.block(q, int(o.end[q] - o.begin[q]))
+        assert np.linalg.norm(Wg - ob.W[q]) <= TOL_BLOCK * np.linalg.norm(ob.W[q]), q
+        if force:
+            Wu, _ = ref_gpu.block(q, int(o.end[q] - o.begin[q]))
+            assert np.linalg.norm(Wg - Wu) <= TOL_BLOCK * np.linalg.norm(Wu), q
+        Wd[gb.row_off[i]:gb.row_off[i + 1], o.begin[q]:o.end[q]] = Wg
+    Pm = np.vstack([Wd, gb.L()])
+    assert np.max(np.abs(Pm @ Pm.T - np.eye(n))) < 1e-12
+    from oracle.index_set import monomials
+    Mx = monomials(X[o.perm], ob.exps)
+    assert np.max(np.abs(Wd @ Mx)) <= 1e-12 * np.max(np.abs(Mx))
