@@ -4,7 +4,7 @@
 
 Writes profiles/launches_cfg2_TAG.txt (per-kernel share of an ncu launch list),
 profiles/k5a_ncu_cfg2_TAG.txt (key counters of the K5a full capture) and
-profiles/k5a_traffic_TAG.json (dram read + write bytes of that launch, read by bench.py).
+profiles/k5a_traffic_CONFIG.json (dram read + write bytes of that launch, read by bench.py).
 """
 import argparse
 import collections
@@ -31,7 +31,7 @@ KEYS = [
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
-def launches(path, tag, note):
+def launches(path, tag, note, cfg="cfg2"):
     rows = [r for r in csv.reader(open(path)) if len(r) > 10]
     h = rows[0]
     ki, vi = h.index("Kernel Name"), h.index("Metric Value")
@@ -51,12 +51,12 @@ def launches(path, tag, note):
     for k, (n, v) in sorted(agg.items(), key=lambda x: -x[1][1]):
         out.append("%-64s %5d %10.3f %5.1f%%" % (k, n, v / 1e6, 100 * v / tot))
     out.append("%-64s %5s %10.3f" % ("TOTAL", "", tot / 1e6))
-    dst = os.path.join(ROOT, "profiles", "launches_cfg2_%s.txt" % tag)
+    dst = os.path.join(ROOT, "profiles", "launches_%s_%s.txt" % (cfg, tag))
     open(dst, "w").write("\n".join(out) + "\n")
     print("\n".join(out[:12]))
 
 
-def k5a(rep, tag, note):
+def k5a(rep, tag, note, cfg="cfg2"):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     h, u, v = rows[0], rows[1], rows[2]
@@ -72,20 +72,24 @@ def k5a(rep, tag, note):
                     out.append("%-84s %s" % (k, m[k][1]))
             except ValueError:
                 pass
-    open(os.path.join(ROOT, "profiles", "k5a_ncu_cfg2_%s.txt" % tag), "w").write("\n".join(out) + "\n")
+    open(os.path.join(ROOT, "profiles", "k5a_ncu_%s_%s.txt" % (cfg, tag)), "w").write("\n".join(out) + "\n")
     print("\n".join(out))
     rd = float(m["dram__bytes_read.sum"][1].replace(",", "")) * SCALE[m["dram__bytes_read.sum"][0]]
     wr = float(m["dram__bytes_write.sum"][1].replace(",", "")) * SCALE[m["dram__bytes_write.sum"][0]]
     json.dump({"what": "dram__bytes_read.sum + dram__bytes_write.sum of one K5a launch (%s), ncu --set full"
                % m["Kernel Name"][1].split("(")[0], "bytes_per_launch": rd + wr, "read": rd, "write": wr,
                "source": rep + " (" + tag + ")"},
-              open(os.path.join(ROOT, "profiles", "k5a_traffic_r01.json"), "w"), indent=1)
+              open(os.path.join(ROOT, "profiles", "k5a_traffic_%s.json" % cfg), "w"), indent=1)
 
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("tag")
-    ap.add_argument("--note", default="cfg2, python bench.py --steps 1 --warmup 1 --e2e-steps 0 --no-cpu-baseline")
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--note", default=None)
     a = ap.parse_args()
-    launches(os.path.join(ROOT, "gpurun_out", "launches_%s.csv" % a.tag), a.tag, a.note)
-    k5a(os.path.join(ROOT, "gpurun_out", "k5a_%s.ncu-rep" % a.tag), a.tag, a.note)
+    note = a.note or ("%s, python bench.py --steps 1 --warmup 1 --e2e-steps 0 --no-cpu-baseline --pcg-tol 0 --config %s"
+                      % (a.config, a.config))
+    sfx = a.tag if a.config == "cfg2" else "%s_%s" % (a.config, a.tag)
+    launches(os.path.join(ROOT, "gpurun_out", "launches_%s.csv" % sfx), a.tag, note, a.config)
+    k5a(os.path.join(ROOT, "gpurun_out", "k5a_%s.ncu-rep" % sfx), a.tag, note, a.config)
