@@ -197,6 +197,18 @@ typedef enum { MLK_PREC_FP64 = 0, MLK_PREC_DD = 1 } mlk_precision;
  */
 mlk_status mlk_assemble_cw(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const mlk_kernel* kernel,
                            const mlk_sparsity* sparsity, int32_t precision, mlk_cw* out);
+/* mlk_assemble_cw_ex -- as mlk_assemble_cw, with the placement of the nnz BSR values:
+ *  MLK_VALUES_DEVICE: device memory (what mlk_assemble_cw does);
+ *  MLK_VALUES_HOST:   mapped pinned host memory allocated by the library (cudaHostAlloc), for
+ *                     matrices beyond HBM (BASELINE cfg5: 184 GB of values next to 106 GB of
+ *                     W).  The kernels store the finished blocks straight over the host link;
+ *                     the piece shards and all scratch stay on the device.  nranks == 1 only
+ *                     (MLK_ERR_UNSUPPORTED-class argument error otherwise).  mlk_cw_values_device
+ *                     then returns the host pointer; mlk_cw_matvec BSR reads the values over
+ *                     the host link. */
+typedef enum { MLK_VALUES_DEVICE = 0, MLK_VALUES_HOST = 1 } mlk_values_placement;
+mlk_status mlk_assemble_cw_ex(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const mlk_kernel* kernel,
+                              const mlk_sparsity* sparsity, int32_t precision, int32_t placement, mlk_cw* out);
 void mlk_cw_free(mlk_cw cw); /* NULL-safe */
 /* n_cells; n_blocks; nnz values; entries = sum over blocks |row cell| |col cell| (the
  * covariance pairs C~_W is made of); flops = FP64 flops the kernels execute (Gram 2d per
@@ -233,7 +245,16 @@ mlk_status mlk_cw_owner(mlk_cw cw, int32_t* owner);
 mlk_status mlk_cw_shard_len(mlk_cw cw, int64_t* shard_len, int64_t* max_shard_len);
 mlk_status mlk_cw_pack(mlk_ctx ctx, mlk_cw cw, double* dst);
 mlk_status mlk_cw_unpack(mlk_ctx ctx, mlk_cw cw, const double* gathered);
-/* Device pointer to the BSR values (valid while cw lives). */
+/* The piece layout behind the gather (for checking one rank's share without the all-gather):
+ * piece_ptr[n_blocks+1] (block k = sum of pieces piece_ptr[k] .. piece_ptr[k+1]-1 in order),
+ * piece_off[n_pieces] (offset in its owner's shard; meaningful for pieces not written straight
+ * into the values, i.e. all pieces when nranks > 1), piece_owner[n_pieces], and a copy of this
+ * rank's shard (shard_len doubles, host or device).  Any output may be NULL; n_pieces =
+ * piece_ptr[n_blocks]. */
+mlk_status mlk_cw_export_pieces(mlk_cw cw, int64_t* piece_ptr, int64_t* piece_off, int32_t* piece_owner,
+                                double* shard);
+/* Pointer to the BSR values (device memory, or mapped host memory under MLK_VALUES_HOST;
+ * valid while cw lives; with nranks > 1 NULL until mlk_cw_unpack allocated them). */
 mlk_status mlk_cw_values_device(mlk_cw cw, double** values);
 
 /* ------------------------------------------------------------------------------------------

@@ -60,6 +60,56 @@ def _check_rank(R, M):
         raise RankDeficient("moment matrix is rank deficient")
 
 
+def _node_step(X, tree, exps, B, q):
+    """Phi_q, W_q, R_q of one node from its points (leaf, steps (a)-(b)) or from its
+    children's R and Phi (internal, steps (c)-(e)), readings R7-R9."""
+    M = len(exps)
+    b, e = tree.begin[q], tree.end[q]
+    if tree.is_leaf[q]:
+        s = e - b
+        if s < M:
+            raise RankDeficient("leaf with fewer points than monomials")
+        P = monomials(X[tree.perm[b:e]], exps)   # calM^T for the leaf unit vectors
+        Q, R = np.linalg.qr(P, mode="complete")
+        _check_rank(R, M)
+        B.Phi[q] = Q[:, :M].T.copy()
+        B.W[q] = Q[:, M:].T.copy()
+        B.R[q] = R[:M, :].copy()
+    else:
+        lq, rq = 2 * q + 1, 2 * q + 2
+        A = np.vstack([B.R[lq], B.R[rq]])          # calM^T = [R_L; R_R]
+        Q, R = np.linalg.qr(A, mode="complete")
+        _check_rank(R, M)
+        nl = tree.end[lq] - tree.begin[lq]
+        V = np.zeros((2 * M, e - b))
+        V[:M, :nl] = B.Phi[lq]
+        V[M:, nl:] = B.Phi[rq]
+        B.Phi[q] = Q[:, :M].T @ V
+        B.W[q] = Q[:, M:].T @ V
+        B.R[q] = R[:M, :].copy()
+
+
+def build_subtree_basis(X, tree, w, root, exps=None):
+    """W, Phi, R of the nodes of the subtree rooted at `root` only.  The construction is
+    bottom-up and a node's blocks depend only on its own points, so these equal the
+    corresponding blocks of build_basis (same steps, same order); used to check sampled
+    cells of workloads whose full basis does not fit the host (BASELINE cfg5).  `cells`,
+    `row_off` and `L` are left empty."""
+    X = np.asarray(X, dtype=np.float64)
+    exps = td_exponents(tree.d, w) if exps is None else list(exps)
+    B = Basis(M=len(exps), exps=exps)
+    sub, stack = [], [root]
+    while stack:
+        q = stack.pop()
+        if q < tree.n_nodes and tree.exists[q]:
+            sub.append(q)
+            if not tree.is_leaf[q]:
+                stack += [2 * q + 1, 2 * q + 2]
+    for q in sorted(sub, reverse=True):              # children before parents
+        _node_step(X, tree, exps, B, q)
+    return B
+
+
 def build_basis(X, tree, w, exps=None):
     """Steps (a)-(f) of P:1427-1515 with readings R7-R11 (TD set unless `exps` is given)."""
     X = np.asarray(X, dtype=np.float64)
@@ -69,31 +119,8 @@ def build_basis(X, tree, w, exps=None):
         raise RankDeficient("need n > M")
     B = Basis(M=M, exps=exps)
     for q in range(tree.n_nodes - 1, -1, -1):       # children before parents, finest first
-        if not tree.exists[q]:
-            continue
-        b, e = tree.begin[q], tree.end[q]
-        if tree.is_leaf[q]:
-            s = e - b
-            if s < M:
-                raise RankDeficient("leaf with fewer points than monomials")
-            P = monomials(X[tree.perm[b:e]], exps)   # calM^T for the leaf unit vectors
-            Q, R = np.linalg.qr(P, mode="complete")
-            _check_rank(R, M)
-            B.Phi[q] = Q[:, :M].T.copy()
-            B.W[q] = Q[:, M:].T.copy()
-            B.R[q] = R[:M, :].copy()
-        else:
-            lq, rq = 2 * q + 1, 2 * q + 2
-            A = np.vstack([B.R[lq], B.R[rq]])          # calM^T = [R_L; R_R]
-            Q, R = np.linalg.qr(A, mode="complete")
-            _check_rank(R, M)
-            nl = tree.end[lq] - tree.begin[lq]
-            V = np.zeros((2 * M, e - b))
-            V[:M, :nl] = B.Phi[lq]
-            V[M:, nl:] = B.Phi[rq]
-            B.Phi[q] = Q[:, :M].T @ V
-            B.W[q] = Q[:, M:].T @ V
-            B.R[q] = R[:M, :].copy()
+        if tree.exists[q]:
+            _node_step(X, tree, exps, B, q)
     # C_W order (R11)
     order = sorted((q for q in range(tree.n_nodes) if tree.exists[q]),
                    key=lambda q: (-int(tree.depth[q]), q))

@@ -100,7 +100,9 @@ struct mlk_cw_s {
   bool complete = false;           // values hold every block (nranks == 1 or unpacked)
   double entries = 0, flops = 0, own_entries = 0, own_flops = 0;
   double f_gram = 0, f_c1 = 0, f_c2 = 0;
-  mlk::DevBuf<double> values;      // nnz (complete for nranks == 1 or after unpack)
+  mlk::DevBuf<double> values;      // nnz on the device (nranks == 1: at assembly; else at unpack)
+  double* hvals = nullptr;         // MLK_VALUES_HOST: nnz in mapped pinned host memory instead
+  double* vals() const { return hvals ? hvals : values.p; }
   mlk::DevBuf<double> shard;       // this rank's packed values (nranks > 1)
   // device structure for the BSR matvec
   mlk::DevBuf<int32_t> brow_d, bcol_d, owner_d;

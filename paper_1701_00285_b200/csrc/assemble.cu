@@ -261,7 +261,7 @@ void reduce_pieces(Ctx& c, mlk_cw_s* cw, const double* gathered) {
   const int64_t ms = cw->nranks > 1 ? cw->max_shard_len : 0;
   k_reduce_pieces<<<(unsigned)cw->reduce_blocks.size(), 256, 0, c.stream>>>(
       cw->reduce_d.p, cw->piece_ptr_d.p, cw->piece_off_d.p, cw->piece_owner_d.p, gathered, ms, cw->val_off_d.p,
-      cw->values.p);
+      cw->vals());
   check_launch("k_reduce_pieces");
 }
 
@@ -273,8 +273,15 @@ extern "C" {
 
 mlk_status mlk_assemble_cw(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const mlk_kernel* kernel,
                            const mlk_sparsity* sparsity, int32_t precision, mlk_cw* out) {
+  return mlk_assemble_cw_ex(ctx, tree, basis, kernel, sparsity, precision, MLK_VALUES_DEVICE, out);
+}
+
+mlk_status mlk_assemble_cw_ex(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const mlk_kernel* kernel,
+                              const mlk_sparsity* sparsity, int32_t precision, int32_t placement, mlk_cw* out) {
   MLK_API_BEGIN
   MLK_REQUIRE(ctx && tree && basis && kernel && sparsity && out, "NULL argument");
+  MLK_REQUIRE(placement == MLK_VALUES_DEVICE || placement == MLK_VALUES_HOST, "unknown value placement");
+  MLK_REQUIRE(placement == MLK_VALUES_DEVICE || ctx->c.nranks == 1, "MLK_VALUES_HOST needs nranks == 1");
   *out = nullptr;
   MLK_REQUIRE(basis->tree == tree, "basis was built for another tree");
   MLK_REQUIRE(kernel->family >= MLK_MATERN_12 && kernel->family <= MLK_MATERN_NU, "unknown covariance family");
@@ -469,14 +476,21 @@ mlk_status mlk_assemble_cw(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const ml
   cw->piece_owner = powner;
   cw->shard_len = shard_fill[c.rank];
   cw->max_shard_len = *std::max_element(shard_fill.begin(), shard_fill.end());
-  cw->values.alloc(std::max<int64_t>(cw->nnz, 1), st);
-  if (c.nranks > 1) cw->values.zero();
+  // the values: device memory now when nranks == 1 (ranks > 1 allocate at mlk_cw_unpack, so a
+  // rank holds only its shard until the gather), or mapped pinned host memory (MLK_VALUES_HOST,
+  // for matrices beyond HBM: the kernels store the blocks straight over the host link)
+  if (placement == MLK_VALUES_HOST) {
+    CUDA_CHECK(cudaHostAlloc((void**)&cw->hvals, sizeof(double) * std::max<int64_t>(cw->nnz, 1),
+                             cudaHostAllocMapped | cudaHostAllocPortable));
+  } else if (c.nranks == 1) {
+    cw->values.alloc(std::max<int64_t>(cw->nnz, 1), st);
+  }
   cw->shard.alloc(std::max<int64_t>(cw->max_shard_len, 1), st);
   for (int64_t k = 0; k < nb; k++)
     if (!direct[k]) cw->reduce_blocks.push_back((int32_t)k);
   auto piece_dst = [&](int64_t i) {
     int64_t k = pieces[i].blk;
-    return direct[k] ? cw->values.p + cw->val_off[k] : cw->shard.p + cw->piece_off[i];
+    return direct[k] ? cw->vals() + cw->val_off[k] : cw->shard.p + cw->piece_off[i];
   };
 
   trace.mark("plan");
@@ -605,6 +619,8 @@ void mlk_cw_free(mlk_cw cw) {
   // the creating context's stream may already be gone: drain the device, free on stream 0
   cudaDeviceSynchronize();
   cw->values.s = nullptr;
+  if (cw->hvals) cudaFreeHost(cw->hvals);
+  cw->hvals = nullptr;
   cw->shard.s = nullptr;
   cw->brow_d.s = nullptr;
   cw->bcol_d.s = nullptr;
@@ -640,7 +656,8 @@ mlk_status mlk_cw_export(mlk_cw cw, int32_t* brow_ptr, int32_t* bcol, int64_t* v
   if (brow_ptr) std::copy(cw->brow_ptr.begin(), cw->brow_ptr.end(), brow_ptr);
   if (bcol) std::copy(cw->bcol.begin(), cw->bcol.end(), bcol);
   if (val_off) std::copy(cw->val_off.begin(), cw->val_off.end(), val_off);
-  if (values && cw->nnz > 0) CUDA_CHECK(cudaMemcpy(values, cw->values.p, sizeof(double) * cw->nnz, cudaMemcpyDefault));
+  MLK_REQUIRE(!values || cw->complete, "values are complete only after mlk_cw_unpack (nranks > 1)");
+  if (values && cw->nnz > 0) CUDA_CHECK(cudaMemcpy(values, cw->vals(), sizeof(double) * cw->nnz, cudaMemcpyDefault));
   MLK_API_END
 }
 
@@ -657,7 +674,7 @@ mlk_status mlk_cw_export_async(mlk_ctx ctx, mlk_cw cw, double* values) {
   CUDA_CHECK(cudaEventRecord(c.copy_ready, c.stream));
   CUDA_CHECK(cudaStreamWaitEvent(c.copy_stream, c.copy_ready, 0));
   if (cw->nnz > 0)
-    CUDA_CHECK(cudaMemcpyAsync(values, cw->values.p, sizeof(double) * cw->nnz, cudaMemcpyDefault, c.copy_stream));
+    CUDA_CHECK(cudaMemcpyAsync(values, cw->vals(), sizeof(double) * cw->nnz, cudaMemcpyDefault, c.copy_stream));
   MLK_API_END
 }
 
@@ -707,6 +724,7 @@ mlk_status mlk_cw_unpack(mlk_ctx ctx, mlk_cw cw, const double* gathered) {
   CUDA_CHECK(cudaSetDevice(c.device));
   MLK_REQUIRE(is_device_ptr(gathered), "gathered must be device memory");
   if (cw->nranks > 1) {
+    if (!cw->hvals && !cw->values.p) cw->values.alloc(std::max<int64_t>(cw->nnz, 1), c.stream);
     TimedLaunch tl(c, "cw_unpack");
     reduce_pieces(c, cw, gathered);
   }
@@ -715,10 +733,23 @@ mlk_status mlk_cw_unpack(mlk_ctx ctx, mlk_cw cw, const double* gathered) {
   MLK_API_END
 }
 
+mlk_status mlk_cw_export_pieces(mlk_cw cw, int64_t* piece_ptr, int64_t* piece_off, int32_t* piece_owner,
+                                double* shard) {
+  MLK_API_BEGIN
+  MLK_REQUIRE(cw, "cw is NULL");
+  CUDA_CHECK(cudaSetDevice(cw->device));
+  if (piece_ptr) std::copy(cw->piece_ptr.begin(), cw->piece_ptr.end(), piece_ptr);
+  if (piece_off) std::copy(cw->piece_off.begin(), cw->piece_off.end(), piece_off);
+  if (piece_owner) std::copy(cw->piece_owner.begin(), cw->piece_owner.end(), piece_owner);
+  if (shard && cw->shard_len > 0)
+    CUDA_CHECK(cudaMemcpy(shard, cw->shard.p, sizeof(double) * cw->shard_len, cudaMemcpyDefault));
+  MLK_API_END
+}
+
 mlk_status mlk_cw_values_device(mlk_cw cw, double** values) {
   MLK_API_BEGIN
   MLK_REQUIRE(cw && values, "NULL argument");
-  *values = cw->values.p;
+  *values = cw->vals();
   MLK_API_END
 }
 

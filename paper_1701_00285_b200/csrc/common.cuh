@@ -62,7 +62,8 @@ struct Ctx {
   // device memory free when the context first needed a scratch budget (cudaMemGetInfo is
   // slow and erratic -- 0.3 to 14 ms per call on B200 while NVML is polled -- so it is queried
   // once per context, not per call)
-  int64_t free_at_first_use = -1;
+  int64_t free_at_first_use = -1;  // cudaMemGetInfo once per context (it stalls under NVML polling)
+  int64_t live_at_first_use = 0;
   cudaStream_t copy_stream = nullptr;  // mlk_cw_export_async (created on first use)
   cudaStream_t aux_stream = nullptr;   // asynchronous basis merge levels (created on first use)
   cudaEvent_t copy_ready = nullptr;
@@ -107,6 +108,9 @@ inline void check_launch(const char* name) {
 // device; src: host memory.
 void upload_async(void* dst, const void* src, size_t bytes, cudaStream_t s);
 
+// bytes held by live DevBufs in this process (the scratch budget subtracts what handles keep)
+extern std::atomic<int64_t> g_live_bytes;
+
 // Stream-ordered device buffer.
 template <typename T>
 struct DevBuf {
@@ -119,7 +123,10 @@ struct DevBuf {
     release();
     s = stream;
     n = count;
-    if (count) CUDA_CHECK(cudaMallocAsync((void**)&p, count * sizeof(T), stream));
+    if (count) {
+      CUDA_CHECK(cudaMallocAsync((void**)&p, count * sizeof(T), stream));
+      g_live_bytes.fetch_add((int64_t)(count * sizeof(T)), std::memory_order_relaxed);
+    }
   }
   void zero() {
     if (n) CUDA_CHECK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
@@ -140,7 +147,10 @@ struct DevBuf {
     return h;
   }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (p) {
+      cudaFreeAsync(p, s);
+      g_live_bytes.fetch_sub((int64_t)(n * sizeof(T)), std::memory_order_relaxed);
+    }
     p = nullptr;
     n = 0;
   }

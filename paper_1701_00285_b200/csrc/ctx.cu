@@ -96,13 +96,19 @@ void upload_async(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   r.head += len;
 }
 
+std::atomic<int64_t> g_live_bytes{0};
+
 int64_t Ctx::scratch_budget_bytes() {
   if (free_at_first_use < 0) {
     size_t freeb = 0, totalb = 0;
     CUDA_CHECK(cudaMemGetInfo(&freeb, &totalb));
     free_at_first_use = (int64_t)freeb;
+    live_at_first_use = g_live_bytes.load();
   }
-  return free_at_first_use / 3;
+  // a third of what was free at first use, less what live handles (W, BSR values, shards)
+  // have taken since; at least 256 MB so small problems never starve
+  const int64_t avail = free_at_first_use - (g_live_bytes.load() - live_at_first_use);
+  return std::max<int64_t>(avail / 3, (int64_t)256 << 20);
 }
 
 cudaEvent_t Ctx::get_event() {

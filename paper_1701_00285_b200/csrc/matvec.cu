@@ -341,7 +341,7 @@ mlk_status mlk_cw_matvec(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const mlk_
       TimedLaunch tl(c, "bsr_matvec");
       k_bsr_matvec<<<cw->n_cells, 256, smem, c.stream>>>(brp.p, cw->bcol_d.p, cw->val_off_d.p, cw->owner_d.p, c.rank,
                                                           cw->csc_ptr_d.p, cw->csc_blk_d.p, cw->brow_d.p, ro.p,
-                                                          cw->values.p, vin.p, yout.p, dim, nvec);
+                                                          cw->vals(), vin.p, yout.p, dim, nvec);
       check_launch("k_bsr_matvec");
     }
     yout.finish();

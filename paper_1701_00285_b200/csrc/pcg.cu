@@ -222,7 +222,7 @@ mlk_status mlk_pcg_solve(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const mlk_
     flag.zero();
     {
       TimedLaunch tl(c, "pcg_factor");
-      k_gather_blocks<<<(unsigned)blocks.size(), kPcgThreads, 0, st>>>(pb_d.p, src_d.p, cw->values.p, Lf.p);
+      k_gather_blocks<<<(unsigned)blocks.size(), kPcgThreads, 0, st>>>(pb_d.p, src_d.p, cw->vals(), Lf.p);
       check_launch("k_gather_blocks");
       k_cholesky<<<(unsigned)blocks.size(), kPcgThreads, 0, st>>>(pb_d.p, Lf.p, flag.p);
       check_launch("k_cholesky");

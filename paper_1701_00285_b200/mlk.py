@@ -25,6 +25,7 @@ TREE_KD, TREE_RP = 0, 1
 MATERN_12, MATERN_32, MATERN_52, GAUSSIAN, MATERN_NU = 0, 1, 2, 3, 4
 PAIRS_ALL, PAIRS_PAPER_TAU = 0, 1
 PREC_FP64, PREC_DD = 0, 1
+VALUES_DEVICE, VALUES_HOST = 0, 1
 MATVEC_EXACT, MATVEC_BSR = 0, 1
 INDEX_TD, INDEX_HC, INDEX_SM, INDEX_TP = 0, 1, 2, 3
 
@@ -36,7 +37,7 @@ SYMBOLS = [
     "mlk_cw_free", "mlk_cw_info", "mlk_cw_export", "mlk_cw_owner", "mlk_cw_shard_len", "mlk_cw_pack",
     "mlk_cw_unpack", "mlk_cw_values_device", "mlk_cov_matvec", "mlk_cw_matvec", "mlk_partition_lpt",
     "mlk_shard_plan", "mlk_launch_count", "mlk_cw_flops", "mlk_cw_export_async", "mlk_ctx_wait_copies",
-    "mlk_pcg_solve", "mlk_build_basis_ex",
+    "mlk_pcg_solve", "mlk_build_basis_ex", "mlk_assemble_cw_ex", "mlk_cw_export_pieces",
 ]
 
 
@@ -88,6 +89,9 @@ _sig = {
     "mlk_apply_w": (C.c_int, [P, P, P, P, C.c_int32]),
     "mlk_assemble_cw": (C.c_int, [P, P, P, C.POINTER(KernelSpec), C.POINTER(SparsitySpec), C.c_int32,
                                   C.POINTER(P)]),
+    "mlk_assemble_cw_ex": (C.c_int, [P, P, P, C.POINTER(KernelSpec), C.POINTER(SparsitySpec), C.c_int32,
+                                     C.c_int32, C.POINTER(P)]),
+    "mlk_cw_export_pieces": (C.c_int, [P, P, P, P, P]),
     "mlk_cw_free": (None, [P]),
     "mlk_cw_info": (C.c_int, [P, P, P, P, P, P, P, P]),
     "mlk_cw_export": (C.c_int, [P, P, P, P, P]),
@@ -362,19 +366,46 @@ class CW:
         _check(_lib.mlk_cw_values_device(self.h, C.byref(p)))
         return p.value
 
+    def pieces(self, with_shard=True):
+        """(piece_ptr, piece_off, piece_owner, shard): the piece layout and this rank's shard."""
+        pp = np.empty(self.n_blocks + 1, np.int64)
+        _check(_lib.mlk_cw_export_pieces(self.h, _np(pp), None, None, None))
+        npc = int(pp[-1])
+        po = np.empty(max(npc, 1), np.int64)
+        pw = np.empty(max(npc, 1), np.int32)
+        sl, _ = self.shard_len()
+        sh = np.empty(max(sl, 1), np.float64) if with_shard else None
+        _check(_lib.mlk_cw_export_pieces(self.h, None, _np(po), _np(pw), _np(sh) if with_shard else None))
+        return pp, po[:npc], pw[:npc], (sh[:sl] if with_shard else None)
+
+    def host_values(self):
+        """Zero-copy NumPy view of the values of a VALUES_HOST matrix (valid while cw lives)."""
+        if getattr(self, "placement", VALUES_DEVICE) != VALUES_HOST:
+            raise MlkError(1, "host_values() needs placement VALUES_HOST")
+        arr = np.ctypeslib.as_array(C.cast(self.values_ptr(), C.POINTER(C.c_double)), shape=(max(self.nnz, 1),))
+        return arr[:self.nnz]
+
     def __del__(self):
         if getattr(self, "h", None):
             _lib.mlk_cw_free(self.h)
             self.h = None
 
 
-def assemble_cw(ctx, tree, basis, kernel, sparsity, precision=PREC_FP64):
+def assemble_cw(ctx, tree, basis, kernel, sparsity, precision=PREC_FP64, placement=VALUES_DEVICE):
+    """mlk_assemble_cw (placement VALUES_DEVICE) or mlk_assemble_cw_ex (VALUES_HOST: the values
+    in mapped pinned host memory, for matrices beyond HBM)."""
     h = C.c_void_p()
     ks = _kspec(kernel)
     sp = sparsity if isinstance(sparsity, SparsitySpec) else SparsitySpec(int(sparsity["mode"]),
                                                                            float(sparsity.get("tau", 0.0)))
-    _check(_lib.mlk_assemble_cw(ctx.h, tree.h, basis.h, C.byref(ks), C.byref(sp), int(precision), C.byref(h)))
-    return CW(h, (ctx, tree, basis))
+    if placement == VALUES_DEVICE:
+        _check(_lib.mlk_assemble_cw(ctx.h, tree.h, basis.h, C.byref(ks), C.byref(sp), int(precision), C.byref(h)))
+    else:
+        _check(_lib.mlk_assemble_cw_ex(ctx.h, tree.h, basis.h, C.byref(ks), C.byref(sp), int(precision),
+                                       int(placement), C.byref(h)))
+    cw = CW(h, (ctx, tree, basis))
+    cw.placement = placement
+    return cw
 
 
 def gather_cw(ctx, cw, group=None):

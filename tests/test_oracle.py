@@ -178,6 +178,26 @@ def test_basis_orthonormal_and_vanishing_moments_cfg1():
     assert Bm.level_rows(tr, B) == {5: 832, 4: 96, 3: 48, 2: 24, 1: 12, 0: 6}   # Lemma 1 counts
 
 
+def test_subtree_basis_equals_full_basis_blocks():
+    """build_subtree_basis (used for sampled cfg5 cells) reproduces build_basis exactly on every
+    node of the subtree, and its W blocks are orthonormal and annihilate the monomials."""
+    inp = wl.make("cfg2", n=4096)
+    c = inp["cfg"]
+    X = inp["X"]
+    tr = T.build_tree(X, c["leaf"], c["tree"], inp["dirs"])
+    B = Bm.build_basis(X, tr, c["w"])
+    for root in (1, 4, 2 ** tr.t - 1):
+        S = Bm.build_subtree_basis(X, tr, c["w"], root)
+        assert root in S.W
+        for q in S.W:
+            assert np.array_equal(S.W[q], B.W[q]) and np.array_equal(S.Phi[q], B.Phi[q])
+        ids = tr.perm[tr.begin[root]:tr.end[root]]
+        Wr = S.W[root]
+        assert np.max(np.abs(Wr @ Wr.T - np.eye(Wr.shape[0]))) < 1e-13
+        Mx = I.monomials(X[ids], B.exps)
+        assert np.max(np.abs(Wr @ Mx)) / np.max(np.abs(Mx)) < 1e-12
+
+
 def test_table1_size_column_reproduced():
     """Size of C~^i_W = sum of rows(W_q) for q >= i, Table numericalresults:table1."""
     g = json.load(open(os.path.join(GOLD, "table1_structure.json")))
