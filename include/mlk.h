@@ -137,6 +137,12 @@ typedef enum { MLK_INDEX_TD = 0, MLK_INDEX_HC = 1, MLK_INDEX_SM = 2, MLK_INDEX_T
  * 20592 = 8 (4000 - 1426)).  W stays orthonormal and annihilates the polynomials; only the
  * direction of the deficient column inside the cell is then set by rounding. */
 #define MLK_BASIS_KEEP_DEFICIENT 1
+/* MLK_BASIS_DROP_PHI retains only L = Phi_root after the construction instead of the Phi block
+ * of every node (M x n doubles per tree level: 111 GB at BASELINE cfg5).  It is also applied
+ * automatically when the Phi blocks exceed half of the free device memory.  mlk_basis_export
+ * of a non-root Phi_block then fails with MLK_ERR_UNSUPPORTED; W, L and every other call are
+ * unaffected. */
+#define MLK_BASIS_DROP_PHI 2
 mlk_status mlk_build_basis_ex(mlk_ctx ctx, mlk_tree tree, int32_t index_set, int32_t w, int32_t flags,
                               mlk_basis* out);
 void mlk_basis_free(mlk_basis basis); /* NULL-safe */

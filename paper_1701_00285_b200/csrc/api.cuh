@@ -84,6 +84,7 @@ struct mlk_basis_s {
   mlk::DevBuf<int> merge_flag;
   mutable bool ready_checked = false;
   bool keep_deficient = false;     // MLK_BASIS_KEEP_DEFICIENT
+  bool phi_dropped = false;        // only L = Phi_root retained (phi_off[0] = 0, others -1)
 };
 
 struct mlk_cw_s {

@@ -756,6 +756,7 @@ mlk_status mlk_build_basis_ex(mlk_ctx ctx, mlk_tree tree, int32_t index_set, int
   *out = nullptr;
   MLK_REQUIRE(index_set >= MLK_INDEX_TD && index_set <= MLK_INDEX_TP, "unknown index set");
   MLK_REQUIRE(w >= 0 && w <= 64, "need 0 <= w <= 64");
+  MLK_REQUIRE((flags & ~(MLK_BASIS_KEEP_DEFICIENT | MLK_BASIS_DROP_PHI)) == 0, "unknown basis flags");
   Ctx& c = ctx->c;
   CUDA_CHECK(cudaSetDevice(c.device));
   cudaStream_t st = c.stream;
@@ -809,7 +810,31 @@ mlk_status mlk_build_basis_ex(mlk_ctx ctx, mlk_tree tree, int32_t index_set, int
   }
   B->dim = row;
   B->W.alloc(std::max<int64_t>(woff, 1), st);
-  B->Phi.alloc(std::max<int64_t>(phioff, 1), st);
+  // Phi blocks of every node cost M x n doubles per level (cfg5: 111 GB next to 106 GB of W).
+  // They are kept (for mlk_basis_export) only when W + Phi fit in half of the free memory or
+  // MLK_BASIS_DROP_PHI is not set; otherwise the construction keeps the leaves' Phi and two
+  // alternating level buffers (node q at M begin[q]) and retains only L = Phi_root.
+  bool drop_phi = (flags & MLK_BASIS_DROP_PHI) != 0;
+  if (!drop_phi && (woff + phioff) * (int64_t)sizeof(double) > ((int64_t)1 << 30)) {
+    size_t freeb = 0, totalb = 0;
+    CUDA_CHECK(cudaMemGetInfo(&freeb, &totalb));
+    drop_phi = phioff * (int64_t)sizeof(double) > (int64_t)freeb / 2;
+  }
+  B->phi_dropped = drop_phi;
+  const int64_t mn = (int64_t)M * tree->n;
+  DevBuf<double> leafphi, lvlphi[2];
+  if (drop_phi) {
+    leafphi.alloc((size_t)std::max<int64_t>(mn, 1), st);
+    std::fill(B->phi_off.begin(), B->phi_off.end(), -1);
+    B->phi_off[0] = 0;
+  } else {
+    B->Phi.alloc(std::max<int64_t>(phioff, 1), st);
+  }
+  auto phi_ptr = [&](int q) -> double* {
+    if (!drop_phi) return B->Phi.p + B->phi_off[q];
+    if (tree->state[q] == 1) return leafphi.p + (int64_t)M * tree->begin[q];
+    return lvlphi[tree->depth[q] & 1].p + (int64_t)M * tree->begin[q];
+  };
   DevBuf<double> Rbuf((size_t)nn * M * M, st);
   DevBuf<int> flag(1, st);
   flag.zero();
@@ -855,7 +880,7 @@ mlk_status mlk_build_basis_ex(mlk_ctx ctx, mlk_tree tree, int32_t index_set, int
       jb.m = s;
       jb.nc = M;
       jb.R = Rbuf.p + (int64_t)q * M * M;
-      jb.qlo = B->Phi.p + B->phi_off[q];
+      jb.qlo = phi_ptr(q);
       jb.qhi = B->W.p + B->w_off[q];
       jb.ldq = s;
       jb.stacked = 0;
@@ -890,6 +915,9 @@ mlk_status mlk_build_basis_ex(mlk_ctx ctx, mlk_tree tree, int32_t index_set, int
   B->merge_flag.alloc(1, st);
   B->merge_flag.zero();
   Rbuf.s = st;  // freed behind the merges
+  leafphi.s = st;
+  if (drop_phi)
+    for (auto& lb : lvlphi) lb.alloc((size_t)std::max<int64_t>(mn, 1), st);
   DevBuf<double> Qt(0, st);
   DevBuf<double> Ast(0, st);
   for (int dep = tree->t - 1; dep >= 0; dep--) {
@@ -936,10 +964,10 @@ mlk_status mlk_build_basis_ex(mlk_ctx ctx, mlk_tree tree, int32_t index_set, int
       int32_t nl = (int32_t)(tree->end[l] - tree->begin[l]), nr = (int32_t)(tree->end[r] - tree->begin[r]);
       const double* Qrow = Qt.p + i * 4 * (size_t)M * M;  // (Q^T)[i][c] at Qrow[i*2M + c]
       for (int half = 0; half < 2; half++) {
-        const double* Pc = B->Phi.p + B->phi_off[half ? r : l];
+        const double* Pc = phi_ptr(half ? r : l);
         int32_t ncol = half ? nr : nl;
         int64_t coff = half ? nl : 0;
-        GemmDesc g1{Qrow + (half ? M : 0), 2 * M, Pc, ncol, B->Phi.p + B->phi_off[q] + coff, s, M, ncol, M, 0};
+        GemmDesc g1{Qrow + (half ? M : 0), 2 * M, Pc, ncol, phi_ptr(q) + coff, s, M, ncol, M, 0};
         GemmDesc g2{Qrow + (int64_t)M * 2 * M + (half ? M : 0), 2 * M, Pc, ncol, B->W.p + B->w_off[q] + coff, s, M,
                     ncol, M, 0};
         gd.push_back(g1);
@@ -950,6 +978,11 @@ mlk_status mlk_build_basis_ex(mlk_ctx ctx, mlk_tree tree, int32_t index_set, int
     trace.mark("lvl_gemm");
   }
   trace.mark("levels");
+  if (drop_phi) {
+    // L = Phi_root: the root's level buffer (or the leaf buffer when the root is a leaf)
+    B->Phi = std::move(tree->state[0] == 1 ? leafphi : lvlphi[0]);
+    B->Phi.s = st;
+  }
   CUDA_CHECK(cudaEventRecord(B->ready, st));
   *out = B.release();
   MLK_API_END
@@ -993,9 +1026,13 @@ mlk_status mlk_basis_export(mlk_basis basis, int32_t* cells, int64_t* cell_row_o
     if (W_block && basis->p[node] > 0)
       CUDA_CHECK(cudaMemcpy(W_block, basis->W.p + basis->w_off[node], sizeof(double) * basis->p[node] * s,
                             cudaMemcpyDefault));
-    if (Phi_block)
+    if (Phi_block) {
+      if (basis->phi_off[node] < 0)
+        throw Error(MLK_ERR_UNSUPPORTED, "Phi blocks of non-root cells were not retained (MLK_BASIS_DROP_PHI "
+                                         "or W + Phi beyond half of the free device memory); L is available");
       CUDA_CHECK(cudaMemcpy(Phi_block, basis->Phi.p + basis->phi_off[node], sizeof(double) * basis->M * s,
                             cudaMemcpyDefault));
+    }
   }
   if (L)
     CUDA_CHECK(cudaMemcpy(L, basis->Phi.p + basis->phi_off[0], sizeof(double) * basis->M * tree->n, cudaMemcpyDefault));

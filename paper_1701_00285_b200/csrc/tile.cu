@@ -206,10 +206,12 @@ struct TileCfg {
   // b points per stage.  BN = 8 (mod 16) makes a W row 8 BN doubles = 64 (mod 128) bytes, so
   // the 16-byte B-fragment loads of a quarter-warp (2 rows x 4 chunks) hit distinct banks
   // without any swizzle -- which a 1-D bulk copy could not apply
-  static constexpr int BN = RQ >= 6 ? 24 : 56;
-  // stages in the smem ring: the one-group class (C a, tiny cells) has short stages, so it
-  // needs a deeper ring to cover the TMA latency
+  static constexpr int BN = RQ >= 6 ? 24 : (RQ == 1 ? 56 : 40);
+  // maximum stages in the smem ring (the launch uses the deepest ring that keeps the target
+  // occupancy, >= 2): the one-group class (C a, tiny cells) has short stages, so it wants a
+  // deeper ring to cover the TMA latency
   static constexpr int NST = RQ == 1 ? 6 : (RQ >= 16 ? 2 : 3);
+  static constexpr int MIN_CTAS = RQ >= 20 ? 3 : 4;  // __launch_bounds__ minimum
   static constexpr int G = RQ <= 12 ? RQ : 8;    // W_b fragments held per DMMA group
   static constexpr int NACC = 1;                 // accumulator sets (2 measured no faster)
 };
@@ -248,11 +250,11 @@ __global__ void k_tile_aug(const double* __restrict__ Xt, int dpt, int d, int64_
 // with DFMAs per lane instead of 8-column DMMAs; the four lanes of a quad hold disjoint column
 // subsets of a row and are summed by two shuffles in the epilogue (fixed order).
 //
-// Staging: a ring of NST stages, each {BN rows of Pb, 8 RQ rows x BN columns of W_b}, filled by
+// Staging: a ring of nring <= NST stages, each {BN rows of Pb, 8 RQ rows x BN columns of W_b}, filled by
 // two 2-D TMA box loads (tensor maps built by run_tile_contract) that complete on the stage's
 // mbarrier; out-of-range rows / columns arrive zero-filled.  Units whose W_b cannot be described
 // by a tensor map (odd row stride or unaligned base) use 8-byte cp.async instead.  The last
-// warp to finish a stage (a shared counter) refills it with the stage NST ahead, so warps never
+// warp to finish a stage (a shared counter) refills it with the stage nring ahead, so warps never
 // wait on a CTA barrier inside a unit.
 // SYM (with NV > 0): symmetric C a.  A task (32-row tile I) covers the points j >= its first
 // row; the row part b_i += C_ij a_j keeps j >= i, the column part b_j += C_ij a_i (j > i) is
@@ -260,10 +262,10 @@ __global__ void k_tile_aug(const double* __restrict__ Xt, int dpt, int d, int64_
 // vector); k_colpart_sum adds them in (tile, warp) order.  Half the covariance evaluations,
 // deterministic.
 template <int RQ, int FAM, int NV, bool SYM = false>
-__global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4)
+__global__ void __launch_bounds__(128, TileCfg<RQ>::MIN_CTAS)
     k_tile_contract(const TileUnit* __restrict__ units, const int32_t* __restrict__ task_range,
                     const int32_t* __restrict__ task_first, int n_units, int* __restrict__ counter,
-                    const double* __restrict__ Pa, const double* __restrict__ Pb, int dpa, int sdp,
+                    const double* __restrict__ Pa, const double* __restrict__ Pb, int dpa, int sdp, int nring,
                     KernelParams kp, const CUtensorMap* __restrict__ maps, double* __restrict__ colpart) {
   constexpr int BN = TileCfg<RQ>::BN;
   constexpr int G = TileCfg<RQ>::G;
@@ -273,21 +275,21 @@ __global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4)
   __shared__ __align__(8) uint64_t full[NST];
   __shared__ int cnt[NST];
   __shared__ int s_unit;
-  __shared__ double s_tab[64];
+  __shared__ double s_tab[kExpTabN];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int sd = stage_doubles(RQ, BN, sdp);
   double* As = sm;                  // 32 x sdp
-  double* St = sm + 32 * sdp;       // NST stages
-  if (tid < 64) s_tab[tid] = kExp2Tab64[tid];
+  double* St = sm + 32 * sdp;       // nring stages
+  for (int i = tid; i < kExpTabN; i += blockDim.x) s_tab[i] = kExp2Tab[i];
   if (tid == 0) {
-    for (int i = 0; i < NST; i++) {
+    for (int i = 0; i < nring; i++) {
       mbar_init(&full[i], 1);
       cnt[i] = 0;
     }
     fence_mbar_init();
   }
   // stale stage contents are only ever multiplied by zeroed covariances: keep them finite
-  for (int e = tid; e < NST * sd; e += 128) St[e] = 0.0;
+  for (int e = tid; e < nring * sd; e += 128) St[e] = 0.0;
   fence_proxy_async_smem();
   const int ks_n = dpa >> 2;
   int gs = 0;  // stages consumed so far by this CTA (ring position and mbarrier phases)
@@ -317,7 +319,7 @@ __global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4)
 
     // fill the ring slot of stage s (called by one whole warp)
     auto issue = [&](int s) {
-      const int slot = (gs + s) % NST;
+      const int slot = (gs + s) % nring;
       double* Xs = St + slot * sd;
       double* Ws = Xs + BN * sdp;
       const int b0 = s * BN, nb = min(BN, u.s_b - b0);
@@ -346,7 +348,7 @@ __global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4)
     };
 
     if (warp == 0)
-      for (int s = 0; s < min(NST, nst); s++) issue(s);
+      for (int s = 0; s < min(nring, nst); s++) issue(s);
     cp_async_wait<0>();
     __syncthreads();  // As visible
 
@@ -376,8 +378,8 @@ __global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4)
         arow[l] = (ar < rows && l < u.qc) ? kp.sigma2 * u.Wb[(int64_t)l * u.ldw + ga] : 0.0;
     }
     for (int s = 0; s < nst; s++) {
-      const int g = gs + s, slot = g % NST;
-      mbar_wait(&full[slot], (unsigned)((g / NST) & 1));
+      const int g = gs + s, slot = g % nring;
+      mbar_wait(&full[slot], (unsigned)((g / nring) & 1));
       const double* Xs = St + slot * sd;
       const double* Ws = Xs + BN * sdp;
       const int yb = s * BN;                       // first b point of the stage (local index)
@@ -487,14 +489,14 @@ __global__ void __launch_bounds__(128, RQ >= 20 ? 3 : 4)
           }
         }
       }
-      // release the slot: the last of the four warps refills it with stage s + NST
+      // release the slot: the last of the four warps refills it with stage s + nring
       __syncwarp();
       int last = 0;
       if (lane == 0) last = atomicAdd(&cnt[slot], 1) == 3;
       last = __shfl_sync(0xffffffffu, last, 0);
       if (last) {
         if (lane == 0) cnt[slot] = 0;
-        if (s + NST < nst) issue(s + NST);
+        if (s + nring < nst) issue(s + nring);
       }
     }
     gs += nst;
@@ -593,7 +595,8 @@ CUtensorMap make_map_2d(const double* base, uint64_t rows, uint64_t cols, uint64
 
 int class_bn(int rq) {
   switch (rq) {
-    case 1: case 2: case 3: case 4: case -1: case -2: case -4: return TileCfg<1>::BN;
+    case 1: case -1: case -2: case -4: return TileCfg<1>::BN;
+    case 2: case 3: case 4: return TileCfg<2>::BN;
     default: return TileCfg<24>::BN;
   }
 }
@@ -602,20 +605,35 @@ template <int RQ, int FAM, int NV = 0, bool SYM = false>
 void launch_class(Ctx& c, const AugArgs& ag, const KernelParams& kp, const TileUnit* units, int n, int* counter) {
   // units = this class's ranges; n = its tasks (ag.task_range / ag.task_first are class-relative)
   constexpr int BN = TileCfg<RQ>::BN;
-  size_t smem = sizeof(double) * (size_t)(32 * ag.sdp + TileCfg<RQ>::NST * stage_doubles(RQ, BN, ag.sdp));
   auto fn = k_tile_contract<RQ, FAM, NV, SYM>;
-  // attribute / occupancy queries are driver round trips: once per instantiation and size
-  static size_t smem_set = 0;
-  static int occ = 0;
-  if (smem != smem_set) {
+  // ring depth: the deepest ring (<= NST, >= 2) that keeps MIN_CTAS resident CTAs per SM (the
+  // stage size grows with d: a fixed depth cut cfg3 / cfg4 to 1-2 CTAs per SM).  Attribute and
+  // occupancy queries are driver round trips: once per instantiation and row stride.
+  static int sdp_set = -1, nring = 0, occ = 0;
+  static size_t smem = 0;
+  if (ag.sdp != sdp_set) {
+    nring = 0;
+    for (int ns = TileCfg<RQ>::NST; ns >= 2; ns--) {
+      const size_t sm_ns = sizeof(double) * (size_t)(32 * ag.sdp + ns * stage_doubles(RQ, BN, ag.sdp));
+      if (sm_ns > 227 * 1024) continue;
+      CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_ns));
+      int o = 0;
+      CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, 128, sm_ns));
+      if (nring == 0 || o > occ) {  // deepest ring at the best occupancy seen
+        nring = ns;
+        occ = o;
+        smem = sm_ns;
+      }
+      if (o >= TileCfg<RQ>::MIN_CTAS) break;
+    }
+    if (nring == 0) throw Error(MLK_ERR_UNSUPPORTED, "tile stages do not fit shared memory");
     CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 128, smem));
     occ = std::max(occ, 1);
-    smem_set = smem;
+    sdp_set = ag.sdp;
   }
   int grid = std::min<int64_t>(n, (int64_t)num_sms(c.device) * occ);
-  fn<<<grid, 128, smem, c.stream>>>(units, ag.task_range, ag.task_first, n, counter, ag.Pa, ag.Pb, ag.dpa, ag.sdp, kp,
-                                    ag.maps, ag.colpart);
+  fn<<<grid, 128, smem, c.stream>>>(units, ag.task_range, ag.task_first, n, counter, ag.Pa, ag.Pb, ag.dpa, ag.sdp,
+                                    nring, kp, ag.maps, ag.colpart);
   check_launch("k_tile_contract");
 }
 

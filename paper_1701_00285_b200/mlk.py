@@ -256,13 +256,14 @@ class Basis:
         self.row_off = np.empty(self.n_cells + 1, np.int64)
         _check(_lib.mlk_basis_export(h, _np(self.cells), _np(self.row_off), -1, None, None, None))
 
-    def block(self, node, size):
-        """(W_node, Phi_node) host copies; size = number of points of the node."""
+    def block(self, node, size, phi=True):
+        """(W_node, Phi_node) host copies; size = number of points of the node.  phi=False
+        skips Phi (returns None for it), as needed when the basis kept only L (BASIS_DROP_PHI)."""
         pos = np.nonzero(self.cells == node)[0]
         p = int(self.row_off[pos[0] + 1] - self.row_off[pos[0]]) if pos.size else 0
         W = np.empty((p, size), np.float64)
-        Phi = np.empty((self.M, size), np.float64)
-        _check(_lib.mlk_basis_export(self.h, None, None, int(node), _np(W), _np(Phi), None))
+        Phi = np.empty((self.M, size), np.float64) if phi else None
+        _check(_lib.mlk_basis_export(self.h, None, None, int(node), _np(W), _np(Phi) if phi else None, None))
         return W, Phi
 
     def L(self):
@@ -277,6 +278,7 @@ class Basis:
 
 
 BASIS_KEEP_DEFICIENT = 1
+BASIS_DROP_PHI = 2
 
 
 def build_basis(ctx, tree, w, index_set=INDEX_TD, flags=0):

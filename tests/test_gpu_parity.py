@@ -585,3 +585,71 @@ def test_blocked_qr_basis(mlk, ctx, n, d, w, leaf, force, monkeypatch):
     from oracle.index_set import monomials
     Mx = monomials(X[o.perm], ob.exps)
     assert np.max(np.abs(Wd @ Mx)) <= 1e-12 * np.max(np.abs(Mx))
+
+
+# --------------------------------------------------------------------------------- beyond HBM (cfg5)
+def test_drop_phi_and_host_values_match(mlk, ctx):
+    """MLK_BASIS_DROP_PHI (only L retained, two alternating level buffers) gives W and L
+    bit-identical to the keep-all construction; MLK_VALUES_HOST (values stored over the host
+    link into mapped pinned memory) gives the same BSR values bit for bit, and the BSR / EXACT
+    products and the PCG preconditioner read them."""
+    X, dirs = _setup(8192, 10, 256, 1)
+    kern = dict(family=OC.MATERN_32, rho=1.0)
+    sp = dict(mode=1, tau=1e-6)
+    g = mlk.build_tree(ctx, X, 256, 1, dirs)
+    keep = mlk.build_basis(ctx, g, 2)
+    drop = mlk.build_basis(ctx, g, 2, flags=mlk.BASIS_DROP_PHI)
+    assert np.array_equal(keep.L(), drop.L())
+    for q in (0, 1, 5, 2 ** g.t - 1, 2 ** (g.t + 1) - 2):
+        s = int(g.export()["end"][q] - g.export()["begin"][q])
+        assert np.array_equal(keep.block(q, s)[0], drop.block(q, s, phi=False)[0])
+    with pytest.raises(mlk.MlkError):
+        drop.block(1, 4096, phi=True)
+    ref_cw = mlk.assemble_cw(ctx, g, keep, kern, sp)
+    ref = ref_cw.export()["values"]
+    hcw = mlk.assemble_cw(ctx, g, drop, kern, sp, placement=mlk.VALUES_HOST)
+    assert np.array_equal(hcw.host_values(), ref)
+    assert np.array_equal(hcw.export()["values"], ref)
+    v = wl.vectors(2, keep.dim, seed=5)
+    yb = mlk.cw_matvec(ctx, g, keep, kern, ref_cw, mlk.MATVEC_BSR, v)
+    assert np.array_equal(mlk.cw_matvec(ctx, g, drop, kern, hcw, mlk.MATVEC_BSR, v), yb)
+    ye = mlk.cw_matvec(ctx, g, keep, kern, None, mlk.MATVEC_EXACT, v)
+    assert np.array_equal(mlk.cw_matvec(ctx, g, drop, kern, None, mlk.MATVEC_EXACT, v), ye)
+    z = wl.vectors(1, keep.dim, seed=6)[0]
+    g1, it1, _ = mlk.pcg_solve(ctx, g, keep, kern, ref_cw, z, tol=1e-8, max_iter=2000)
+    g2, it2, _ = mlk.pcg_solve(ctx, g, drop, kern, hcw, z, tol=1e-8, max_iter=2000)
+    assert it1 == it2 and np.array_equal(g1, g2)
+
+
+def test_rank_share_blocks_from_pieces(mlk, ctx):
+    """One rank's share of an R-rank assembly, checked without the all-gather (what
+    tools/cfg5_share.py does at full cfg5 size): every block whose pieces this rank owns equals
+    the sum of its pieces in the rank's shard, and matches the oracle within 1e-11."""
+    X, dirs = _setup(16384, 10, 256, 1)
+    kern = dict(family=OC.MATERN_32, rho=1.0)
+    sp = dict(mode=1, tau=1e-6)
+    o = OT.build_tree(X, 256, 1, dirs)
+    ob = OB.build_basis(X, o, 2)
+    pairs = OA.admitted_pairs(X, o, ob, 1, 1e-6)
+    _, _, _, _, vo = OAs.bsr_structure(ob, pairs)
+    R, r = 4, 1
+    c = mlk.Ctx(0, R, r)
+    g = mlk.build_tree(c, X, 256, 1, dirs)
+    gb = mlk.build_basis(c, g, 2, flags=mlk.BASIS_DROP_PHI)
+    cw = mlk.assemble_cw(c, g, gb, kern, sp)
+    pp, po, pw, shard = cw.pieces()
+    assert np.array_equal(cw.structure()[2], vo)
+    checked = 0
+    for k in range(len(pairs)):
+        own = pw[pp[k]:pp[k + 1]]
+        if len(own) == 0 or np.any(own != r):
+            continue
+        ln = vo[k + 1] - vo[k]
+        got = np.zeros(ln)
+        for i in range(pp[k], pp[k + 1]):
+            got = got + shard[po[i]:po[i] + ln]
+        a, b = pairs[k]
+        ref = OAs.block(X, o, ob, kern, a, b).ravel()
+        assert np.linalg.norm(got - ref) <= TOL_BLOCK * np.linalg.norm(ref), (a, b)
+        checked += 1
+    assert checked >= 0.1 * len(pairs) / R
