@@ -522,3 +522,32 @@ def test_sm_and_tp_sets_brute_force():
         for kind in (I.TD, I.HC, I.SM, I.TP):
             e = I.exponents(kind, d, w)
             assert e[0] == (0,) * d and [sum(a) for a in e] == sorted(sum(a) for a in e)
+
+
+@pytest.mark.parametrize("name,count", [("cfg3", 20819), ("cfg4", 13668), ("cfg5", 16803)])
+def test_golden_pair_lists(name, count):
+    """tests/golden/pairs_<cfg>.npz (tools/make_golden_pairs.py, oracle only) at full BASELINE
+    size: unique unordered pairs in C_W order, a superset of the ancestor/descendant-or-self
+    pattern (the tau = 0 structure, sum_j 2^j (j + 1) = 9217 pairs at t = 9), the root row dense
+    (R21), and the count the survey measured independently on the same recipe (S§8 [M13])."""
+    g = np.load(os.path.join(GOLD, "pairs_%s.npz" % name))
+    P = g["pairs"]
+    assert len(P) == count
+    t = 9
+    depth = lambda q: int(np.floor(np.log2(q + 1)))
+    key = lambda q: (-depth(q), q)                        # C_W order (R11)
+    assert all(key(a) <= key(b) for a, b in P)
+    assert len({(int(a), int(b)) for a, b in P}) == len(P)
+    S = {(int(a), int(b)) for a, b in P}
+    anc = 0
+    for q in range(2 ** (t + 1) - 1):
+        a = q
+        while True:
+            pr = (q, a) if key(q) <= key(a) else (a, q)
+            assert pr in S
+            anc += 1
+            if a == 0:
+                break
+            a = (a - 1) // 2
+    assert anc == sum(2 ** j * (j + 1) for j in range(t + 1)) == 9217
+    assert all(((0, q) in S or (q, 0) in S) for q in range(2 ** (t + 1) - 1))
