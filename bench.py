@@ -183,6 +183,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--pcg-tol", type=float, default=1e-8, help="PCG solve reported after the bench (0: skip)")
+    ap.add_argument("--no-matvec-report", dest="matvec_report", action="store_false",
+                    help="skip the C_W v timings reported after the bench")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -318,6 +320,38 @@ def main():
     h2d = inp["X"].nbytes + (dirs.nbytes if dirs is not None else 0) + vh.numel() * 8
     d2h = nnz * 8 + yh.numel() * 8
 
+    # ---- C_W v timings (outside the timed step, S§8d): EXACT per call with nvec = 1 (x10
+    # sequential) and batched nvec = 10, BSR nvec = 1; CUDA events on the library stream
+    mv = None
+    if args.matvec_report and ws == 1:
+        trm = mlk.build_tree(ctx, X_d, c["leaf"], c["tree"], dirs_d)
+        Bm = mlk.build_basis(ctx, trm, c["w"], c.get("index_set", 0),
+                             mlk.BASIS_KEEP_DEFICIENT if c.get("index_set", 0) else 0)
+        cwm = mlk.assemble_cw(ctx, trm, Bm, kern, spars)
+        v10 = torch.from_numpy(wl.vectors(10, Bm.dim, seed=1)).to(dev)
+        y10 = torch.empty_like(v10)
+
+        def ev_ms(fn):
+            fn()  # warm
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            fn()
+            a1.record(stream)
+            a1.synchronize()
+            return a0.elapsed_time(a1)
+
+        def seq10():
+            for i in range(10):
+                mlk.cw_matvec(ctx, trm, Bm, kern, None, mlk.MATVEC_EXACT, v10[i:i + 1], out=y10[i:i + 1])
+
+        mv = {"exact_nvec1_x10_sequential_ms": ev_ms(seq10),
+              "exact_nvec10_batched_ms": ev_ms(lambda: mlk.cw_matvec(ctx, trm, Bm, kern, None, mlk.MATVEC_EXACT,
+                                                                     v10, out=y10)),
+              "bsr_nvec1_ms": ev_ms(lambda: mlk.cw_matvec(ctx, trm, Bm, kern, cwm, mlk.MATVEC_BSR, v10[0:1],
+                                                          out=y10[0:1]))}
+        del trm, Bm, cwm
+
     # ---- NEXT-1 (outside the timed step): one PCG solve C_W gamma = z with P_W, N(0,1) z
     pcg = None
     if args.pcg_tol > 0 and ws == 1:
@@ -372,6 +406,7 @@ def main():
                     "d2h_bytes_per_step": int(d2h),
                     "ms_per_step": e2e_total / args.e2e_steps if e2e_ms else None},
             "cpu_baseline": cpu,
+            "matvec": mv,
             "pcg": pcg,
         }
         print(json.dumps(line))

@@ -266,7 +266,9 @@ mlk_status mlk_cw_values_device(mlk_cw cw, double** values);
 /* ------------------------------------------------------------------------------------------
  * mlk_cov_matvec -- b = C a, exact direct summation with on-the-fly covariance tiles (step
  * (2) of P:2146-2170).  a, b: nvec x n in tree order (host or device), 1 <= nvec <= 64.
- * With nranks > 1 only this rank's rows of b are computed; the others are zero.
+ * With nranks > 1, b is this rank's partial sum and the caller sums b over the ranks: the
+ * rank owns a set of 32-row tiles I and adds C(I, J) a_J to b_I and, for the symmetric
+ * product (nvec <= 4, each pair (i, j) evaluated once), C(I, J)^T a_I to b_J (J > I).
  */
 mlk_status mlk_cov_matvec(mlk_ctx ctx, mlk_tree tree, const mlk_kernel* kernel, const double* a,
                           double* b, int32_t nvec);

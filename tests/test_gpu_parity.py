@@ -483,8 +483,10 @@ def test_multirank_emulated_bit_identical(mlk, ctx, R):
 ])
 def test_pcg_matches_oracle(mlk, ctx, n, d, leaf, kind, fam, rho):
     """GPU PCG (EXACT products, block-diagonal P_W from the assembled self blocks, or none)
-    against oracle/pcg.py: same iteration count up to one step, same solution to the
-    tolerance's scale, true residual below the tolerance."""
+    against oracle/pcg.py: same iteration count up to one step with P_W (up to 3% of the count
+    without it: unpreconditioned CG loses orthogonality and its count at 1e-9 moves with the
+    last-bit rounding of the products -- 181 vs 184 after a 1-ulp change of the exp), same
+    solution to the tolerance's scale, true residual below the tolerance."""
     from oracle import pcg as OP
     X, dirs = _setup(n, d, leaf, kind)
     g, o = _tree_both(mlk, ctx, X, leaf, kind, dirs)
@@ -496,7 +498,7 @@ def test_pcg_matches_oracle(mlk, ctx, n, d, leaf, kind, fam, rho):
     for precond in (True, False):
         x, it, res = mlk.pcg_solve(ctx, g, gb, kern, cw, z, tol=1e-9, max_iter=3000, precond=precond)
         xo, ito, reso = OP.solve_cw(X, o, ob, kern, z, tol=1e-9, max_iter=3000, use_precond=precond)
-        assert abs(it - ito) <= 1, (precond, it, ito)
+        assert abs(it - ito) <= (1 if precond else max(1, int(np.ceil(0.03 * ito)))), (precond, it, ito)
         assert res <= 2e-9, res
         assert np.linalg.norm(x - xo) <= 1e-6 * np.linalg.norm(xo)
     x1, _, _ = mlk.pcg_solve(ctx, g, gb, kern, cw, z, tol=1e-9, max_iter=3000)

@@ -9,7 +9,7 @@ mkdir -p $OUT
 for CFG in $CFGS; do
   timeout 900 python bench.py --config $CFG --steps 3 --warmup 3 --e2e-steps 1 --pcg-tol 0 > $OUT/bench_${CFG}_$TAG.json 2> $OUT/bench_${CFG}_$TAG.err
   echo "bench_rc=$?" >> $OUT/bench_${CFG}_$TAG.err
-  SHORT="python bench.py --steps 1 --warmup 1 --e2e-steps 0 --no-cpu-baseline --pcg-tol 0 --config $CFG"
+  SHORT="python bench.py --steps 1 --warmup 1 --e2e-steps 0 --no-cpu-baseline --pcg-tol 0 --no-matvec-report --config $CFG"
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_${CFG}_$TAG.csv $SHORT > $OUT/ncu_launch_${CFG}_$TAG.log 2>&1
   echo "ncu_launch_rc=$?" >> $OUT/ncu_launch_${CFG}_$TAG.log
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_tile_contract -s 1 -c 1 \

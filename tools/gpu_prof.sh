@@ -6,7 +6,7 @@ TAG=${1:-p}
 CFG=${2:-cfg2}
 OUT=gpurun_out
 mkdir -p $OUT
-SHORT="python bench.py --steps 1 --warmup 1 --e2e-steps 0 --no-cpu-baseline --pcg-tol 0 --config $CFG"
+SHORT="python bench.py --steps 1 --warmup 1 --e2e-steps 0 --no-cpu-baseline --pcg-tol 0 --no-matvec-report --config $CFG"
 timeout 300 $SHORT > $OUT/short_$TAG.log 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv $SHORT > $OUT/ncu_launch_$TAG.log 2>&1
 echo "ncu_launch_rc=$?" >> $OUT/short_$TAG.log

@@ -13,7 +13,7 @@ if [ "$MODE" = "tests" ]; then
   echo "pytest_rc=$?" >> $OUT/pytest_gpu_$TAG.log
 fi
 timeout 600 python bench.py > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err; echo "bench_rc=$?" >> $OUT/bench_$TAG.err
-SHORT="python bench.py --steps 1 --warmup 1 --e2e-steps 0 --no-cpu-baseline --pcg-tol 0"
+SHORT="python bench.py --steps 1 --warmup 1 --e2e-steps 0 --no-cpu-baseline --pcg-tol 0 --no-matvec-report"
 timeout 300 $SHORT > $OUT/short_$TAG.log 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv $SHORT > $OUT/ncu_launch_$TAG.log 2>&1
 echo "ncu_launch_rc=$?" >> $OUT/short_$TAG.log
