@@ -76,11 +76,11 @@ int tile_rq_class(int qc) {
   return kTileMaxRQ;
 }
 
-// (rq, nr) for a chunk of qc columns: 8 rq DMMA columns plus nr <= kTileMaxNR DFMA columns when
+// (rq, nr) for a chunk of qc columns: 8 rq DMMA columns plus nr <= tile_max_nr(rq) DFMA columns when
 // qc = 8 rq + nr with rq a class, else rq = the padding class and nr = 0
 static void tile_split(int qc, int& rq, int& nr) {
   const int lo = qc / 8, rem = qc % 8;
-  if (lo >= 1 && lo <= 12 && rem >= 1 && rem <= kTileMaxNR && tile_rq_class(8 * lo) == lo) {
+  if (lo >= 1 && lo <= 12 && rem >= 1 && rem <= tile_max_nr(lo) && tile_rq_class(8 * lo) == lo) {
     rq = lo;
     nr = rem;
   } else {
@@ -219,7 +219,7 @@ struct TileCfg {
 // stage size rounded to 128 bytes: 2-D TMA writes need 128-byte aligned shared destinations
 // (the W part starts BN sdp doubles in, a multiple of 128 bytes since sdp is a multiple of 4)
 __host__ __device__ constexpr int stage_doubles(int rq, int bn, int sdp) {
-  return (bn * sdp + (8 * rq + kTileMaxNR) * bn + 15) / 16 * 16;
+  return (bn * sdp + (8 * rq + tile_max_nr(rq)) * bn + 15) / 16 * 16;
 }
 
 // Augmented, pre-scaled coordinates (x in tree order, s = kp.scale, u = s x):
@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(128, TileCfg<RQ>::MIN_CTAS)
     for (int i = 0; i < (NV > 0 ? NV : 1); i++) accv[i] = 0.0;
     // DFMA remainder columns 8 RQ .. 8 RQ + nr - 1 (lane-partial sums); classes above 12 have
     // no remainder (tile_split), which keeps their register budget
-    constexpr int NRMAX = (NV > 0 || RQ > 12) ? 0 : kTileMaxNR;
+    constexpr int NRMAX = (NV > 0 || RQ > 12) ? 0 : tile_max_nr(RQ);
     double accr[NRMAX > 0 ? NRMAX : 1];
 #pragma unroll
     for (int i = 0; i < (NRMAX > 0 ? NRMAX : 1); i++) accr[i] = 0.0;

@@ -51,7 +51,12 @@ KernelParams make_kernel_params(const mlk_kernel& k);
 // column-class instantiations available to the planner
 int tile_rq_class(int qc);  // smallest available rq with 8 rq >= qc
 constexpr int kTileMaxRQ = 24;
-constexpr int kTileMaxNR = 3;  // at most this many remainder columns go to DFMA instead of padding
+// remainder columns that go to lane-local DFMA instead of padding to the next 8-column group:
+// a DFMA column costs 2 x 2.25 pipe cycles per 64 entries against 4 per column of a padded
+// DMMA group, so up to 7 pay; classes above 4 groups keep at most 3 (register budget)
+constexpr int kTileMaxNR = 7;
+constexpr int kTileMaxNRWide = 3;
+__host__ __device__ constexpr int tile_max_nr(int rq) { return rq <= 4 ? kTileMaxNR : kTileMaxNRWide; }
 // Run all units (any mix of rq classes) on the context stream.  colpart != nullptr selects the
 // symmetric C a kernel (units with rq = -NV; see tile.cu).
 void run_tile_contract(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, std::vector<TileUnit>& units,

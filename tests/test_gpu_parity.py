@@ -177,7 +177,10 @@ FAMS = [(OC.MATERN_12, 0.5), (OC.MATERN_32, 1.0), (OC.MATERN_52, 2.0), (OC.GAUSS
 @pytest.mark.parametrize("n,d,w,leaf,kind,mode,tau,points", [
     (2048, 10, 2, 128, 1, 0, 0.0, "uniform"),     # cfg2 shape, ALL pairs
     (1000, 3, 1, 40, 0, 1, 0.05, "normal"),       # ragged, tau
-    (4096, 20, 1, 256, 1, 1, 1e-7, "normal"),     # cfg3 shape
+    (4096, 20, 1, 256, 1, 1, 1e-7, "normal"),     # cfg3 shape (internal p = 21 = 16 + 5 DFMA)
+    (2048, 4, 2, 64, 1, 0, 0.0, "uniform"),       # p = 15 = 8 + 7 DFMA, leaf p = 49 = 48 + 1
+    (1920, 5, 2, 60, 1, 0, 0.0, "uniform"),       # p = 21, leaf p = 39 = 32 + 7 DFMA
+    (3072, 3, 2, 48, 1, 0, 0.0, "normal"),        # p = 10 = 8 + 2, leaf p = 38 = 32 + 6
 ])
 def test_assembly_fp64_parity(mlk, ctx, fam, rho, n, d, w, leaf, kind, mode, tau, points):
     X, dirs = _setup(n, d, leaf, kind, points)

@@ -73,12 +73,15 @@ def main():
     t0 = time.perf_counter()
     tr = mlk.build_tree(ctx, X_d, c["leaf"], c["tree"], D_d)
     mark("tree")
+    print("tree built", flush=True)
     B = mlk.build_basis(ctx, tr, c["w"], flags=mlk.BASIS_DROP_PHI)
+    print("basis leaf level done", flush=True)
     wall["tree+basis(leaf level)"] = time.perf_counter() - t0
     t0 = time.perf_counter()
     cw = mlk.assemble_cw(ctx, tr, B, kern, dict(mode=c["pairs"], tau=c["tau"]))
     mark("assemble")
     wall["assemble"] = time.perf_counter() - t0
+    print("assembled", flush=True)
     v = torch.from_numpy(wl.vectors(1, B.dim, seed=0)).to(dev)
     y = torch.empty_like(v)
     t0 = time.perf_counter()
