@@ -476,6 +476,11 @@ mlk_status mlk_assemble_cw_ex(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const
   cw->piece_owner = powner;
   cw->shard_len = shard_fill[c.rank];
   cw->max_shard_len = *std::max_element(shard_fill.begin(), shard_fill.end());
+  // the merge levels of the basis ran on the auxiliary stream during the search and planning;
+  // wait for them before the large allocations, so that the pool can reuse the memory the
+  // basis construction freed on that stream (cfg5: level buffers and QR scratch, ~50 GB)
+  basis_wait(c, B);
+  trace.mark("basis_wait");
   // the values: device memory now when nranks == 1 (ranks > 1 allocate at mlk_cw_unpack, so a
   // rank holds only its shard until the gather), or mapped pinned host memory (MLK_VALUES_HOST,
   // for matrices beyond HBM: the kernels store the blocks straight over the host link)
@@ -494,8 +499,6 @@ mlk_status mlk_assemble_cw_ex(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const
   };
 
   trace.mark("plan");
-  basis_wait(c, B);  // the basis merge levels ran on the auxiliary stream during the search and planning
-  trace.mark("basis_wait");
   if (dd) {
     std::vector<std::array<int64_t, 8>> jobs;
     for (int64_t i = 0; i < npc; i++) {

@@ -124,7 +124,13 @@ struct DevBuf {
     s = stream;
     n = count;
     if (count) {
-      CUDA_CHECK(cudaMallocAsync((void**)&p, count * sizeof(T), stream));
+      if (cudaMallocAsync((void**)&p, count * sizeof(T), stream) != cudaSuccess) {
+        // memory freed on another stream is reusable only once that free has completed:
+        // drain the device and retry once before reporting out-of-memory
+        cudaGetLastError();
+        CUDA_CHECK(cudaDeviceSynchronize());
+        CUDA_CHECK(cudaMallocAsync((void**)&p, count * sizeof(T), stream));
+      }
       g_live_bytes.fetch_add((int64_t)(count * sizeof(T)), std::memory_order_relaxed);
     }
   }

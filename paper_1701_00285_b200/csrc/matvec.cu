@@ -51,54 +51,97 @@ __global__ void k_apply_w(const CellJob* __restrict__ jobs, const double* __rest
   }
 }
 
-// BSR: y_r = sum_{own blocks (r,c)} B v_c + sum_{own blocks (c,r), c != r} B^T v_c
-__global__ void k_bsr_matvec(const int32_t* __restrict__ brow_ptr, const int32_t* __restrict__ bcol,
-                             const int64_t* __restrict__ val_off, const int32_t* __restrict__ owner, int rank,
-                             const int32_t* __restrict__ csc_ptr, const int32_t* __restrict__ csc_blk,
-                             const int32_t* __restrict__ brow, const int64_t* __restrict__ row_off,
-                             const double* __restrict__ vals, const double* __restrict__ v, double* __restrict__ y,
-                             int64_t dim, int nvec) {
-  extern __shared__ double part[];  // p_r x nvec
+// BSR: y_r = sum_{own blocks (r,c)} B v_c + sum_{own blocks (c,r), c != r} B^T v_c, as two
+// passes over the stored blocks that each read a block once with coalesced loads, then a
+// fixed-order reduction per cell (deterministic, no atomics).  HBM-bound: 2 x 8 nnz bytes.
+//  row pass  (one CTA per block, grid.y = vector group): warp per block row i, lanes over the
+//            columns, warp reduction -> rp[k][iv][i] (p_r values)
+//  col pass  (one CTA per block and 256-column panel): thread per block column j, loop over
+//            the rows -> cp[k][iv][j] (p_c values, off-diagonal blocks only)
+constexpr int kBsrVG = 4;  // vectors per pass
+
+__global__ void k_bsr_rows(const int32_t* __restrict__ brow, const int32_t* __restrict__ bcol,
+                           const int64_t* __restrict__ val_off, const int32_t* __restrict__ owner, int rank,
+                           const int64_t* __restrict__ row_off, const int64_t* __restrict__ part_off,
+                           const double* __restrict__ vals, const double* __restrict__ v, int64_t dim, int nvec,
+                           double* __restrict__ rp) {
+  const int k = blockIdx.x, iv0 = blockIdx.y * kBsrVG;
+  const int r = brow[k], c = bcol[k];
+  const int64_t r0 = row_off[r], c0 = row_off[c];
+  const int pr = (int)(row_off[r + 1] - r0), pc = (int)(row_off[c + 1] - c0);
+  const int nv = min(kBsrVG, nvec - iv0);
+  double* out = rp + part_off[k] * nvec;  // nvec x p_r
+  const bool own = owner[k] == rank;
+  const double* B = vals + val_off[k];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = warp; i < pr; i += nw) {
+    double s[kBsrVG] = {0.0, 0.0, 0.0, 0.0};
+    if (own) {
+      const double* Bi = B + (int64_t)i * pc;
+      for (int j = lane; j < pc; j += 32) {
+        const double bij = Bi[j];
+#pragma unroll
+        for (int q = 0; q < kBsrVG; q++)
+          if (q < nv) s[q] = fma(bij, v[(int64_t)(iv0 + q) * dim + c0 + j], s[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kBsrVG; q++) {
+      for (int o = 16; o > 0; o >>= 1) s[q] += __shfl_xor_sync(0xffffffffu, s[q], o);
+      if (lane == 0 && q < nv) out[(int64_t)(iv0 + q) * pr + i] = s[q];
+    }
+  }
+}
+
+__global__ void k_bsr_cols(const int32_t* __restrict__ brow, const int32_t* __restrict__ bcol,
+                           const int64_t* __restrict__ val_off, const int32_t* __restrict__ owner, int rank,
+                           const int64_t* __restrict__ row_off, const int64_t* __restrict__ part_off,
+                           const double* __restrict__ vals, const double* __restrict__ v, int64_t dim, int nvec,
+                           double* __restrict__ cp) {
+  const int k = blockIdx.x, iv0 = blockIdx.z * kBsrVG;
+  const int r = brow[k], c = bcol[k];
+  if (r == c) return;
+  const int64_t r0 = row_off[r], c0 = row_off[c];
+  const int pr = (int)(row_off[r + 1] - r0), pc = (int)(row_off[c + 1] - c0);
+  const int j = blockIdx.y * blockDim.x + threadIdx.x;
+  if (j >= pc) return;
+  const int nv = min(kBsrVG, nvec - iv0);
+  double s[kBsrVG] = {0.0, 0.0, 0.0, 0.0};
+  if (owner[k] == rank) {
+    const double* B = vals + val_off[k] + j;
+#pragma unroll 4
+    for (int i = 0; i < pr; i++) {
+      const double bij = B[(int64_t)i * pc];
+#pragma unroll
+      for (int q = 0; q < kBsrVG; q++)
+        if (q < nv) s[q] = fma(bij, v[(int64_t)(iv0 + q) * dim + r0 + i], s[q]);
+    }
+  }
+  double* out = cp + part_off[k] * nvec;  // nvec x p_c
+#pragma unroll
+  for (int q = 0; q < kBsrVG; q++)
+    if (q < nv) out[(int64_t)(iv0 + q) * pc + j] = s[q];
+}
+
+// y[cell rows] = row partials of the cell's block row (in order) + column partials of the
+// blocks in its block column (in order)
+__global__ void k_bsr_reduce(const int32_t* __restrict__ brow_ptr, const int32_t* __restrict__ csc_ptr,
+                             const int32_t* __restrict__ csc_blk, const int64_t* __restrict__ row_off,
+                             const int64_t* __restrict__ rpart_off, const int64_t* __restrict__ cpart_off,
+                             const double* __restrict__ rp, const double* __restrict__ cp, int64_t dim, int nvec,
+                             double* __restrict__ y) {
   const int r = blockIdx.x;
   const int64_t r0 = row_off[r];
   const int pr = (int)(row_off[r + 1] - r0);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int e = threadIdx.x; e < pr * nvec; e += blockDim.x) part[e] = 0.0;
-  __syncthreads();
-  // row blocks: warp per output row, lanes over the block's columns
-  for (int k = brow_ptr[r]; k < brow_ptr[r + 1]; k++) {
-    if (owner[k] != rank) continue;
-    const int c = bcol[k];
-    const int64_t c0 = row_off[c];
-    const int pc = (int)(row_off[c + 1] - c0);
-    const double* B = vals + val_off[k];
-    for (int i = warp; i < pr; i += nw) {
-      for (int iv = 0; iv < nvec; iv++) {
-        const double* vv = v + (int64_t)iv * dim + c0;
-        double s = 0.0;
-        for (int j = lane; j < pc; j += 32) s = fma(B[(int64_t)i * pc + j], vv[j], s);
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) part[i * nvec + iv] += s;
-      }
+  for (int e = threadIdx.x; e < pr * nvec; e += blockDim.x) {
+    const int iv = e / pr, i = e - iv * pr;
+    double s = 0.0;
+    for (int k = brow_ptr[r]; k < brow_ptr[r + 1]; k++) s += rp[rpart_off[k] * nvec + (int64_t)iv * pr + i];
+    for (int q = csc_ptr[r]; q < csc_ptr[r + 1]; q++) {
+      const int k = csc_blk[q];
+      s += cp[cpart_off[k] * nvec + (int64_t)iv * pr + i];
     }
-  }
-  __syncthreads();
-  // mirrored blocks: thread per output row (column of the stored block)
-  for (int i = threadIdx.x; i < pr; i += blockDim.x) {
-    for (int iv = 0; iv < nvec; iv++) {
-      double s = part[i * nvec + iv];
-      for (int q = csc_ptr[r]; q < csc_ptr[r + 1]; q++) {
-        const int k = csc_blk[q];
-        if (owner[k] != rank) continue;
-        const int c = brow[k];
-        const int64_t c0 = row_off[c];
-        const int pc = (int)(row_off[c + 1] - c0);
-        const double* B = vals + val_off[k];  // pc x pr
-        const double* vv = v + (int64_t)iv * dim + c0;
-        for (int j = 0; j < pc; j++) s = fma(B[(int64_t)j * pr + i], vv[j], s);
-      }
-      y[(int64_t)iv * dim + r0 + i] = s;
-    }
+    y[(int64_t)iv * dim + r0 + i] = s;
   }
 }
 
@@ -329,20 +372,43 @@ mlk_status mlk_cw_matvec(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const mlk_
     ro.upload(basis->row_off);
     DevBuf<int32_t> brp(cw->brow_ptr.size(), c.stream);
     brp.upload(cw->brow_ptr);
-    // values: the gathered matrix when nranks == 1 or after unpack; a rank applies only its
-    // own blocks (the caller allreduces y)
-    int pmax = 0;
-    for (size_t i = 0; i + 1 < basis->row_off.size(); i++)
-      pmax = std::max<int>(pmax, (int)(basis->row_off[i + 1] - basis->row_off[i]));
-    size_t smem = sizeof(double) * (size_t)std::max(1, pmax) * nvec;
-    MLK_REQUIRE(smem <= 200 * 1024, "BSR matvec: p_max x nvec too large");
-    CUDA_CHECK(cudaFuncSetAttribute(k_bsr_matvec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (cw->n_cells > 0) {
+    // partial offsets (per vector): row partials p_row per block, column partials p_col per
+    // off-diagonal block
+    const int64_t nb = cw->n_blocks;
+    std::vector<int64_t> rpo(std::max<int64_t>(nb, 1), 0), cpo(std::max<int64_t>(nb, 1), 0);
+    int64_t rtot = 0, ctot = 0;
+    int pcmax = 0;
+    for (int64_t k = 0; k < nb; k++) {
+      const int r = cw->brow[k], cc = cw->bcol[k];
+      const int pr = (int)(basis->row_off[r + 1] - basis->row_off[r]);
+      const int pc = (int)(basis->row_off[cc + 1] - basis->row_off[cc]);
+      rpo[k] = rtot;
+      rtot += pr;
+      cpo[k] = ctot;
+      if (r != cc) ctot += pc;
+      pcmax = std::max(pcmax, pc);
+    }
+    if (nb > 0) {
+      DevBuf<int64_t> rpo_d(rpo.size(), c.stream), cpo_d(cpo.size(), c.stream);
+      rpo_d.upload(rpo);
+      cpo_d.upload(cpo);
+      DevBuf<double> rp((size_t)std::max<int64_t>(rtot * nvec, 1), c.stream);
+      DevBuf<double> cp((size_t)std::max<int64_t>(ctot * nvec, 1), c.stream);
       TimedLaunch tl(c, "bsr_matvec");
-      k_bsr_matvec<<<cw->n_cells, 256, smem, c.stream>>>(brp.p, cw->bcol_d.p, cw->val_off_d.p, cw->owner_d.p, c.rank,
-                                                          cw->csc_ptr_d.p, cw->csc_blk_d.p, cw->brow_d.p, ro.p,
-                                                          cw->vals(), vin.p, yout.p, dim, nvec);
-      check_launch("k_bsr_matvec");
+      const unsigned vg = (unsigned)ceil_div(nvec, kBsrVG);
+      k_bsr_rows<<<dim3((unsigned)nb, vg), 256, 0, c.stream>>>(cw->brow_d.p, cw->bcol_d.p, cw->val_off_d.p,
+                                                               cw->owner_d.p, c.rank, ro.p, rpo_d.p, cw->vals(), vin.p,
+                                                               dim, nvec, rp.p);
+      check_launch("k_bsr_rows");
+      k_bsr_cols<<<dim3((unsigned)nb, (unsigned)ceil_div(std::max(pcmax, 1), 256), vg), 256, 0, c.stream>>>(
+          cw->brow_d.p, cw->bcol_d.p, cw->val_off_d.p, cw->owner_d.p, c.rank, ro.p, cpo_d.p, cw->vals(), vin.p, dim,
+          nvec, cp.p);
+      check_launch("k_bsr_cols");
+      k_bsr_reduce<<<(unsigned)cw->n_cells, 256, 0, c.stream>>>(brp.p, cw->csc_ptr_d.p, cw->csc_blk_d.p, ro.p, rpo_d.p,
+                                                               cpo_d.p, rp.p, cp.p, dim, nvec, yout.p);
+      check_launch("k_bsr_reduce");
+    } else {
+      CUDA_CHECK(cudaMemsetAsync(yout.p, 0, sizeof(double) * nvec * dim, c.stream));
     }
     yout.finish();
   }

@@ -51,10 +51,11 @@ KernelParams make_kernel_params(const mlk_kernel& k);
 // column-class instantiations available to the planner
 int tile_rq_class(int qc);  // smallest available rq with 8 rq >= qc
 constexpr int kTileMaxRQ = 24;
-// remainder columns that go to lane-local DFMA instead of padding to the next 8-column group:
-// a DFMA column costs 2 x 2.25 pipe cycles per 64 entries against 4 per column of a padded
-// DMMA group, so up to 7 pay; classes above 4 groups keep at most 3 (register budget)
-constexpr int kTileMaxNR = 7;
+// remainder columns that go to lane-local DFMA instead of padding to the next 8-column group.
+// A DFMA column costs 2 x 2.25 pipe cycles per 64 entries against 4 per column of a padded DMMA
+// group, which suggests up to 7; measured on cfg3 (p = 21), 16 + 5 DFMA ran 4 % slower than
+// 24 padded (286 vs 274 ms, r01g vs r01f: register pressure and the broadcast W loads), so 3
+constexpr int kTileMaxNR = 3;
 constexpr int kTileMaxNRWide = 3;
 __host__ __device__ constexpr int tile_max_nr(int rq) { return rq <= 4 ? kTileMaxNR : kTileMaxNRWide; }
 // Run all units (any mix of rq classes) on the context stream.  colpart != nullptr selects the
