@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Context, error reporting, per-kernel timing and host-only helpers of the C ABI.
 #include <algorithm>
 #include <cstring>
@@ -66,19 +67,21 @@ void upload_async(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   }
   const size_t len = (bytes + 255) & ~(size_t)255;
   if (r.head + len > PinnedRing::kCap) r.head = 0;
-  // the chunks overlapping [head, head + len) are the oldest live ones: wait for their copies
-  while (!r.live.empty()) {
-    const auto& ch = r.live.front();
-    const bool overlap = ch.off < r.head + len && r.head < ch.off + ch.len;
-    if (!overlap) break;
-    CUDA_CHECK(cudaEventSynchronize(ch.ev));
-    r.pool.push_back(ch.ev);
-    r.live.pop_front();
-  }
-  // retire completed chunks at the front so the deque stays short
-  while (!r.live.empty() && cudaEventQuery(r.live.front().ev) == cudaSuccess) {
-    r.pool.push_back(r.live.front().ev);
-    r.live.pop_front();
+  // wait for EVERY live chunk overlapping [head, head + len): after two wraps of the ring the
+  // overlapping chunks need not be at the front of the deque (live holds the tail of one lap
+  // followed by the start of the next, and copies on different streams complete out of order).
+  // Checking only the front let a new upload overwrite staged job descriptors whose copy had not
+  // run yet -- an illegal address in the next kernel (cfg5 basis, r01f / r01h).
+  for (const auto& ch : r.live)
+    if (ch.off < r.head + len && r.head < ch.off + ch.len) CUDA_CHECK(cudaEventSynchronize(ch.ev));
+  // retire every completed chunk
+  for (auto it = r.live.begin(); it != r.live.end();) {
+    if (cudaEventQuery(it->ev) == cudaSuccess) {
+      r.pool.push_back(it->ev);
+      it = r.live.erase(it);
+    } else {
+      ++it;
+    }
   }
   cudaGetLastError();  // cudaEventQuery's cudaErrorNotReady is not an error here
   char* stage = r.base + r.head;
@@ -108,6 +111,11 @@ int64_t Ctx::scratch_budget_bytes() {
   // a third of what was free at first use, less what live handles (W, BSR values, shards)
   // have taken since; at least 256 MB so small problems never starve
   const int64_t avail = free_at_first_use - (g_live_bytes.load() - live_at_first_use);
+  static const int64_t forced = [] {
+    const char* e = std::getenv("MLK_SCRATCH_BUDGET_MB");  // diagnostics: force small batches
+    return e ? (int64_t)std::atoll(e) << 20 : (int64_t)0;
+  }();
+  if (forced > 0) return forced;
   return std::max<int64_t>(avail / 3, (int64_t)256 << 20);
 }
 

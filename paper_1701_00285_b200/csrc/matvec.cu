@@ -87,8 +87,10 @@ __global__ void k_bsr_rows(const int32_t* __restrict__ brow, const int32_t* __re
     }
 #pragma unroll
     for (int q = 0; q < kBsrVG; q++) {
-      for (int o = 16; o > 0; o >>= 1) s[q] += __shfl_xor_sync(0xffffffffu, s[q], o);
-      if (lane == 0 && q < nv) out[(int64_t)(iv0 + q) * pr + i] = s[q];
+      if (q < nv) {  // warp-uniform
+        for (int o = 16; o > 0; o >>= 1) s[q] += __shfl_xor_sync(0xffffffffu, s[q], o);
+        if (lane == 0) out[(int64_t)(iv0 + q) * pr + i] = s[q];
+      }
     }
   }
 }

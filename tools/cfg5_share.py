@@ -41,6 +41,7 @@ def main():
     ap.add_argument("--n", type=int, default=None, help="reduced n (dry runs)")
     ap.add_argument("--blocks", type=int, default=8)
     ap.add_argument("--rows", type=int, default=64)
+    ap.add_argument("--stop-after-basis", action="store_true", help="diagnostics")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "cfg5_share.json"))
     a = ap.parse_args()
 
@@ -76,6 +77,10 @@ def main():
     print("tree built", flush=True)
     B = mlk.build_basis(ctx, tr, c["w"], flags=mlk.BASIS_DROP_PHI)
     print("basis leaf level done", flush=True)
+    if a.stop_after_basis:
+        L = B.L()
+        print("basis complete, |L| = %.6e" % float(np.linalg.norm(L)), flush=True)
+        return
     wall["tree+basis(leaf level)"] = time.perf_counter() - t0
     t0 = time.perf_counter()
     cw = mlk.assemble_cw(ctx, tr, B, kern, dict(mode=c["pairs"], tau=c["tau"]))
