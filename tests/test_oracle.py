@@ -551,3 +551,56 @@ def test_golden_pair_lists(name, count):
             a = (a - 1) // 2
     assert anc == sum(2 ** j * (j + 1) for j in range(t + 1)) == 9217
     assert all(((0, q) in S or (q, 0) in S) for q in range(2 ** (t + 1) - 1))
+
+
+from oracle import likelihood as Ll  # noqa: E402
+
+
+def test_loglik_dense_matches_scipy_gaussian_logpdf():
+    """The oracle's Cholesky log-likelihood equals the Gaussian
+    log-density of scipy.stats on a random SPD matrix and on a small C~_W."""
+    from scipy.stats import multivariate_normal
+    rng = np.random.default_rng([0, 11])
+    R = rng.standard_normal((40, 40))
+    S = R @ R.T + 40 * np.eye(40)
+    z = rng.standard_normal(40)
+    l, ld, q = Ll.loglik_dense(S, z)
+    assert abs(l - multivariate_normal(mean=np.zeros(40), cov=S).logpdf(z)) <= 1e-10 * abs(l)
+    assert abs(ld - np.linalg.slogdet(S)[1]) <= 1e-12 * abs(ld)
+    assert abs(q - z @ np.linalg.solve(S, z)) <= 1e-12 * q
+    inp = wl.make("cfg1", n=256)
+    c = inp["cfg"]
+    X = inp["X"]
+    tr = T.build_tree(X, 16, c["tree"], inp["dirs"])
+    B = Bm.build_basis(X, tr, c["w"])
+    kern = dict(family=cv.MATERN_12, rho=0.5)
+    pairs = A.admitted_pairs(X, tr, B, A.PAIRS_PAPER_TAU, 0.05)
+    bsr = As.assemble(X, tr, B, kern, pairs)
+    zw = rng.standard_normal(B.dim)
+    for level in (0, 2, tr.t):
+        l, ld, q, nt = Ll.loglik(bsr, tr, B, zw, level)
+        Ct = As.bsr_to_dense(bsr)[:nt, :nt]
+        ref = multivariate_normal(mean=np.zeros(nt), cov=Ct).logpdf(zw[:nt])
+        assert abs(l - ref) <= 1e-10 * abs(ref)
+
+
+def test_loglik_truncation_sizes_and_identity_pin():
+    """N~ per level is the Lemma 1 row count of levels t .. n (cfg1: 832, 96, 48, 24, 12, 6),
+    and the identity pin (Gaussian rho = 1e-5 => C = I => C~_W = I) gives log det = 0 and
+    quad = |Z^n_W|^2."""
+    inp = wl.make("cfg1")
+    c = inp["cfg"]
+    X = inp["X"]
+    tr = T.build_tree(X, c["leaf"], c["tree"], inp["dirs"])
+    B = Bm.build_basis(X, tr, c["w"])
+    rows = [832, 96, 48, 24, 12, 6]            # levels 5 .. 0
+    for level in range(6):
+        assert Ll.truncation(tr, B, level)[1] == sum(rows[:6 - level])
+    kern = dict(family=cv.GAUSSIAN, rho=1e-5)
+    pairs = A.admitted_pairs(X, tr, B, A.PAIRS_PAPER_TAU, 1e-7)
+    bsr = As.assemble(X, tr, B, kern, pairs)
+    zw = np.random.default_rng([0, 12]).standard_normal(B.dim)
+    for level in (0, 3, 5):
+        l, ld, q, nt = Ll.loglik(bsr, tr, B, zw, level)
+        assert abs(ld) <= 1e-12 * nt and abs(q - zw[:nt] @ zw[:nt]) <= 1e-12 * q
+        assert abs(l - (-0.5 * nt * np.log(2 * np.pi) - 0.5 * zw[:nt] @ zw[:nt])) <= 1e-12 * abs(l)
