@@ -299,6 +299,22 @@ mlk_status mlk_pcg_solve(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const mlk_
                          int32_t* iters, double* rel_residual);
 
 /* ------------------------------------------------------------------------------------------
+ * mlk_loglik -- the level-truncated multi-level log-likelihood of P:1954-1971 (the survey's
+ * NEXT-4):
+ *   l~^n_W = -N~/2 log(2 pi) - 1/2 log det C~^n_W - 1/2 (Z^n_W)^T (C~^n_W)^-1 Z^n_W,
+ * with C~^n_W the upper-left N~ x N~ block of the assembled C~_W = the rows of the cells of
+ * levels t .. `level` (0 <= level <= t; level 0 is the whole C~_W), and Z^n_W the first N~
+ * entries of z_w = W Z (dim doubles, host or device; e.g. from mlk_apply_w).  Computed from a
+ * block-sparse Cholesky factor of C~^n_W (log det = 2 sum log G_ii, the quadratic
+ * form by the same factor), right-looking over the BSR cells in C_W order with the fill of
+ * the block pattern; deterministic.  Outputs (any may be NULL): loglik, logdet, quad =
+ * (Z^n_W)^T (C~^n_W)^-1 Z^n_W, n_tilde = N~.  cw must be complete; nranks == 1.
+ * MLK_ERR_RANK_DEFICIENT if a pivot is not positive (C~^n_W not positive definite).
+ */
+mlk_status mlk_loglik(mlk_ctx ctx, mlk_basis basis, mlk_cw cw, int32_t level, const double* z_w,
+                      double* loglik, double* logdet, double* quad, int64_t* n_tilde);
+
+/* ------------------------------------------------------------------------------------------
  * Host-only helpers (no device needed).
  * mlk_partition_lpt: longest-processing-time assignment of n units with the given costs to
  * nranks ranks (largest first to the least-loaded rank; ties to the lower rank), the

@@ -126,6 +126,7 @@ struct GemmDesc {
   int32_t trans_c;
   int64_t diag = -1;  // >= 0: store [i + diag == j] - (A B)[i][j] instead of (A B)[i][j]
   int32_t sub = 0;    // 1: C -= A B (read-modify-write; not with diag)
+  int32_t trans_a = 0;  // 1: A is stored k x m (row-major, lda >= m) and read transposed
 };
 // Launch all products on the context stream with FP64 DMMA tiles (64 x 64, 72 x 72 or
 // 64 x 32, by padded volume; k steps of 16); large k

@@ -920,62 +920,69 @@ mlk_status mlk_build_basis_ex(mlk_ctx ctx, mlk_tree tree, int32_t index_set, int
     for (auto& lb : lvlphi) lb.alloc((size_t)std::max<int64_t>(mn, 1), st);
   DevBuf<double> Qt(0, st);
   DevBuf<double> Ast(0, st);
+  // cells of a level in groups whose stacked matrices and Q^T (6 M^2 doubles per cell) fit a
+  // quarter of the scratch budget (cfg5: 84 MB per cell; a whole level of 256 took 22 GB)
+  const int64_t per_cell = 6 * (int64_t)M * M * (int64_t)sizeof(double);
+  const size_t group_max = (size_t)std::max<int64_t>(1, c.scratch_budget_bytes() / 4 / per_cell);
   for (int dep = tree->t - 1; dep >= 0; dep--) {
-    std::vector<int> cellsq;
+    std::vector<int> level_cells;
     for (int q = (1 << dep) - 1; q < (2 << dep) - 1; q++)
-      if (tree->state[q] == 0) cellsq.push_back(q);
-    if (cellsq.empty()) continue;
-    size_t nc = cellsq.size();
-    Ast.alloc(nc * 2 * M * M, st);
-    Qt.alloc(nc * 4 * (size_t)M * M, st);
-    std::vector<StackJob> sj;
-    std::vector<QrJob> qj;
-    for (size_t i = 0; i < nc; i++) {
-      int q = cellsq[i];
-      sj.push_back({Rbuf.p + (int64_t)(2 * q + 1) * M * M, Rbuf.p + (int64_t)(2 * q + 2) * M * M,
-                    Ast.p + i * 2 * M * M});
-      QrJob jb;
-      jb.A = Ast.p + i * 2 * M * M;
-      jb.m = 2 * M;
-      jb.nc = M;
-      jb.R = Rbuf.p + (int64_t)q * M * M;
-      jb.qlo = Qt.p + i * 4 * (size_t)M * M;       // Q column-major == Q^T row-major
-      jb.qhi = jb.qlo + (size_t)M * 2 * M;
-      jb.ldq = 2 * M;
-      jb.stacked = 1;
-      qj.push_back(jb);
-    }
-    DevBuf<StackJob> sjd(nc, st);
-    sjd.upload(sj);
-    {
-      TimedLaunch tl(c, "basis_stack");
-      k_stack_r<<<(unsigned)nc, 256, 0, st>>>(sjd.p, M);
-      check_launch("k_stack_r");
-    }
-    trace.mark("lvl_stack");
-    run_qr(c, qj, M, B->merge_flag.p, "basis_merge_qr");
-    trace.mark("lvl_qr");
-    // Phi_q / W_q = (Q^T)[rows, cols of child] x Phi_child
-    std::vector<GemmDesc> gd;
-    for (size_t i = 0; i < nc; i++) {
-      int q = cellsq[i];
-      int l = 2 * q + 1, r = 2 * q + 2;
-      int64_t s = tree->end[q] - tree->begin[q];
-      int32_t nl = (int32_t)(tree->end[l] - tree->begin[l]), nr = (int32_t)(tree->end[r] - tree->begin[r]);
-      const double* Qrow = Qt.p + i * 4 * (size_t)M * M;  // (Q^T)[i][c] at Qrow[i*2M + c]
-      for (int half = 0; half < 2; half++) {
-        const double* Pc = phi_ptr(half ? r : l);
-        int32_t ncol = half ? nr : nl;
-        int64_t coff = half ? nl : 0;
-        GemmDesc g1{Qrow + (half ? M : 0), 2 * M, Pc, ncol, phi_ptr(q) + coff, s, M, ncol, M, 0};
-        GemmDesc g2{Qrow + (int64_t)M * 2 * M + (half ? M : 0), 2 * M, Pc, ncol, B->W.p + B->w_off[q] + coff, s, M,
-                    ncol, M, 0};
-        gd.push_back(g1);
-        gd.push_back(g2);
+      if (tree->state[q] == 0) level_cells.push_back(q);
+    for (size_t g0 = 0; g0 < level_cells.size(); g0 += group_max) {
+      std::vector<int> cellsq(level_cells.begin() + g0,
+                              level_cells.begin() + std::min(level_cells.size(), g0 + group_max));
+      size_t nc = cellsq.size();
+      Ast.alloc(nc * 2 * M * M, st);
+      Qt.alloc(nc * 4 * (size_t)M * M, st);
+      std::vector<StackJob> sj;
+      std::vector<QrJob> qj;
+      for (size_t i = 0; i < nc; i++) {
+        int q = cellsq[i];
+        sj.push_back({Rbuf.p + (int64_t)(2 * q + 1) * M * M, Rbuf.p + (int64_t)(2 * q + 2) * M * M,
+                      Ast.p + i * 2 * M * M});
+        QrJob jb;
+        jb.A = Ast.p + i * 2 * M * M;
+        jb.m = 2 * M;
+        jb.nc = M;
+        jb.R = Rbuf.p + (int64_t)q * M * M;
+        jb.qlo = Qt.p + i * 4 * (size_t)M * M;       // Q column-major == Q^T row-major
+        jb.qhi = jb.qlo + (size_t)M * 2 * M;
+        jb.ldq = 2 * M;
+        jb.stacked = 1;
+        qj.push_back(jb);
       }
+      DevBuf<StackJob> sjd(nc, st);
+      sjd.upload(sj);
+      {
+        TimedLaunch tl(c, "basis_stack");
+        k_stack_r<<<(unsigned)nc, 256, 0, st>>>(sjd.p, M);
+        check_launch("k_stack_r");
+      }
+      trace.mark("lvl_stack");
+      run_qr(c, qj, M, B->merge_flag.p, "basis_merge_qr");
+      trace.mark("lvl_qr");
+      // Phi_q / W_q = (Q^T)[rows, cols of child] x Phi_child
+      std::vector<GemmDesc> gd;
+      for (size_t i = 0; i < nc; i++) {
+        int q = cellsq[i];
+        int l = 2 * q + 1, r = 2 * q + 2;
+        int64_t s = tree->end[q] - tree->begin[q];
+        int32_t nl = (int32_t)(tree->end[l] - tree->begin[l]), nr = (int32_t)(tree->end[r] - tree->begin[r]);
+        const double* Qrow = Qt.p + i * 4 * (size_t)M * M;  // (Q^T)[i][c] at Qrow[i*2M + c]
+        for (int half = 0; half < 2; half++) {
+          const double* Pc = phi_ptr(half ? r : l);
+          int32_t ncol = half ? nr : nl;
+          int64_t coff = half ? nl : 0;
+          GemmDesc g1{Qrow + (half ? M : 0), 2 * M, Pc, ncol, phi_ptr(q) + coff, s, M, ncol, M, 0};
+          GemmDesc g2{Qrow + (int64_t)M * 2 * M + (half ? M : 0), 2 * M, Pc, ncol, B->W.p + B->w_off[q] + coff, s, M,
+                      ncol, M, 0};
+          gd.push_back(g1);
+          gd.push_back(g2);
+        }
+      }
+      gemm_batched(c, gd, "basis_transfer_gemm");
+      trace.mark("lvl_gemm");
     }
-    gemm_batched(c, gd, "basis_transfer_gemm");
-    trace.mark("lvl_gemm");
   }
   trace.mark("levels");
   if (drop_phi) {

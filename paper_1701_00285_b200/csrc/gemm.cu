@@ -1,4 +1,4 @@
-// Batched variable-size FP64 GEMM on DMMA.8x8x4 (row-major NN, optional transposed store).
+// Batched variable-size FP64 GEMM on DMMA.8x8x4 (row-major NN or TN, optional transposed store).
 // Used for the basis transfers Phi_q/W_q = Q^T (Phi_L (+) Phi_R), the blocked QR's trailing
 // updates and the second contraction B = W_a U of the assembly.  Three tilings, chosen per
 // product by the smallest padded volume: 64 x 64 (2 x 2 warps of 32 x 32), 72 x 72 (3 x 3
@@ -39,12 +39,22 @@ template <class CF>
 __device__ __forceinline__ void load_tiles(const GemmDesc& g, int m0, int n0, int64_t kk, int64_t k1, double* As,
                                            double* Bs) {
   const int tid = threadIdx.x;
-  for (int e = tid; e < CF::BM * BK; e += CF::NT) {
-    const int row = e / BK, col = e % BK;
-    const int gm = m0 + row;
-    const int64_t gk = kk + col;
-    const bool ok = gm < g.m && gk < k1;
-    cp_async8(As + row * CF::AS + col, ok ? g.A + (int64_t)gm * g.lda + gk : g.A, ok);
+  if (g.trans_a) {  // A(m, k) at A[k lda + m]: rows of the tile fastest, coalesced along m
+    for (int e = tid; e < CF::BM * BK; e += CF::NT) {
+      const int row = e % CF::BM, col = e / CF::BM;
+      const int gm = m0 + row;
+      const int64_t gk = kk + col;
+      const bool ok = gm < g.m && gk < k1;
+      cp_async8(As + row * CF::AS + col, ok ? g.A + gk * g.lda + gm : g.A, ok);
+    }
+  } else {
+    for (int e = tid; e < CF::BM * BK; e += CF::NT) {
+      const int row = e / BK, col = e % BK;
+      const int gm = m0 + row;
+      const int64_t gk = kk + col;
+      const bool ok = gm < g.m && gk < k1;
+      cp_async8(As + row * CF::AS + col, ok ? g.A + (int64_t)gm * g.lda + gk : g.A, ok);
+    }
   }
   for (int e = tid; e < BK * CF::BN; e += CF::NT) {
     const int row = e / CF::BN, col = e % CF::BN;

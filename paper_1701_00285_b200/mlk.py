@@ -37,7 +37,7 @@ SYMBOLS = [
     "mlk_cw_free", "mlk_cw_info", "mlk_cw_export", "mlk_cw_owner", "mlk_cw_shard_len", "mlk_cw_pack",
     "mlk_cw_unpack", "mlk_cw_values_device", "mlk_cov_matvec", "mlk_cw_matvec", "mlk_partition_lpt",
     "mlk_shard_plan", "mlk_launch_count", "mlk_cw_flops", "mlk_cw_export_async", "mlk_ctx_wait_copies",
-    "mlk_pcg_solve", "mlk_build_basis_ex", "mlk_assemble_cw_ex", "mlk_cw_export_pieces",
+    "mlk_pcg_solve", "mlk_build_basis_ex", "mlk_assemble_cw_ex", "mlk_cw_export_pieces", "mlk_loglik",
 ]
 
 
@@ -92,6 +92,7 @@ _sig = {
     "mlk_assemble_cw_ex": (C.c_int, [P, P, P, C.POINTER(KernelSpec), C.POINTER(SparsitySpec), C.c_int32,
                                      C.c_int32, C.POINTER(P)]),
     "mlk_cw_export_pieces": (C.c_int, [P, P, P, P, P]),
+    "mlk_loglik": (C.c_int, [P, P, P, C.c_int32, P, P, P, P, P]),
     "mlk_cw_free": (None, [P]),
     "mlk_cw_info": (C.c_int, [P, P, P, P, P, P, P, P]),
     "mlk_cw_export": (C.c_int, [P, P, P, P, P]),
@@ -478,6 +479,15 @@ def pcg_solve(ctx, tree, basis, kernel, cw, z_w, tol=1e-10, max_iter=1000, preco
     _check(_lib.mlk_pcg_solve(ctx.h, tree.h, basis.h, C.byref(_kspec(kernel)), cw.h if cw is not None else None,
                               1 if precond else 0, zp, op, float(tol), int(max_iter), C.byref(it), C.byref(rr)))
     return res, it.value, rr.value
+
+
+def loglik(ctx, basis, cw, z_w, level=0):
+    """Level-truncated multi-level log-likelihood (mlk_loglik): returns dict(loglik, logdet,
+    quad, n_tilde) for the cells of levels t .. level."""
+    zp, keep = _ptr(z_w)
+    ll, ld, q, nt = C.c_double(), C.c_double(), C.c_double(), C.c_int64()
+    _check(_lib.mlk_loglik(ctx.h, basis.h, cw.h, int(level), zp, C.byref(ll), C.byref(ld), C.byref(q), C.byref(nt)))
+    return dict(loglik=ll.value, logdet=ld.value, quad=q.value, n_tilde=nt.value)
 
 
 def partition_lpt(cost, nranks):
