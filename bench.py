@@ -368,6 +368,16 @@ def main():
         dt = time.perf_counter() - t0
         pcg = {"tol": args.pcg_tol, "precond": "block-diagonal P_W (self blocks)", "iterations": it,
                "true_rel_residual": rr, "seconds": dt, "ms_per_iteration": 1e3 * dt / max(it, 1)}
+        # NEXT-4: the level-truncated log-likelihood l~^n_W of the same data, full (n = 0) and
+        # the finest level only (n = t)
+        ll = {}
+        for lev in (0, trp.t):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = mlk.loglik(ctx, Bp, cwp, zp, lev)
+            torch.cuda.synchronize()
+            ll["level%d" % lev] = dict(r, seconds=time.perf_counter() - t0)
+        pcg["loglik"] = ll
         del trp, Bp, cwp
 
     if rank == 0:

@@ -658,3 +658,47 @@ def test_rank_share_blocks_from_pieces(mlk, ctx):
         assert np.linalg.norm(got - ref) <= TOL_BLOCK * np.linalg.norm(ref), (a, b)
         checked += 1
     assert checked >= 0.1 * len(pairs) / R
+
+
+# --------------------------------------------------------------------------------- NEXT-4
+@pytest.mark.parametrize("n,d,w,leaf,kind,fam,rho,tau,points", [
+    (1024, 2, 2, 32, 0, OC.MATERN_12, 0.5, 0.05, "uniform"),    # cfg1 shape, tau pattern with fill
+    (4096, 10, 2, 128, 1, OC.MATERN_32, 1.0, 1e-6, "uniform"),  # cfg2 shape
+    (2048, 4, 1, 64, 1, OC.GAUSSIAN, 1.5, 0.2, "normal"),
+])
+def test_loglik_matches_oracle(mlk, ctx, n, d, w, leaf, kind, fam, rho, tau, points):
+    """mlk_loglik (block-sparse Cholesky of C~^n_W on the GPU) against oracle/likelihood.py
+    (dense numpy Cholesky of the oracle's C~^n_W) at several truncation levels: N~ exact,
+    log-likelihood, log det and quadratic form within 1e-10 relative (Cholesky is backward
+    stable: the errors are ~ N~ kappa u on log det and ~ kappa u on the quadratic form)."""
+    from oracle import likelihood as OL
+    X, dirs = _setup(n, d, leaf, kind, points)
+    g, o = _tree_both(mlk, ctx, X, leaf, kind, dirs)
+    gb = mlk.build_basis(ctx, g, w)
+    ob = OB.build_basis(X, o, w)
+    kern = dict(family=fam, rho=rho)
+    cw = mlk.assemble_cw(ctx, g, gb, kern, dict(mode=1, tau=tau))
+    pairs = OA.admitted_pairs(X, o, ob, 1, tau)
+    bsr = OAs.assemble(X, o, ob, kern, pairs)
+    zw = np.random.default_rng([0, 13]).standard_normal(gb.dim)
+    for level in sorted({0, g.t // 2, g.t}):
+        r = mlk.loglik(ctx, gb, cw, zw, level)
+        l, ld, q, nt = OL.loglik(bsr, o, ob, zw, level)
+        assert r["n_tilde"] == nt
+        assert abs(r["loglik"] - l) <= 1e-10 * abs(l), (level, r["loglik"], l)
+        assert abs(r["logdet"] - ld) <= 1e-10 * max(abs(ld), 1.0), (level, r["logdet"], ld)
+        assert abs(r["quad"] - q) <= 1e-10 * q, (level, r["quad"], q)
+    a = mlk.loglik(ctx, gb, cw, zw, 0)
+    assert a == mlk.loglik(ctx, gb, cw, zw, 0)   # deterministic
+
+
+def test_loglik_identity_pin_on_gpu(mlk, ctx):
+    """Gaussian rho = 1e-5 on cfg1 points: C = I, so C~_W = I: log det = 0, quad = |Z_W|^2."""
+    X, dirs = _setup(1024, 2, 32, 0)
+    g = mlk.build_tree(ctx, X, 32, 0, dirs)
+    gb = mlk.build_basis(ctx, g, 2)
+    cw = mlk.assemble_cw(ctx, g, gb, dict(family=OC.GAUSSIAN, rho=1e-5), dict(mode=1, tau=1e-7))
+    zw = np.random.default_rng([0, 14]).standard_normal(gb.dim)
+    r = mlk.loglik(ctx, gb, cw, zw, 0)
+    assert r["n_tilde"] == gb.dim
+    assert abs(r["logdet"]) <= 1e-12 * gb.dim and abs(r["quad"] - zw @ zw) <= 1e-12 * (zw @ zw)
