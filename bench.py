@@ -374,7 +374,10 @@ def main():
         for lev in (0, trp.t):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            r = mlk.loglik(ctx, Bp, cwp, zp, lev)
+            try:
+                r = mlk.loglik(ctx, Bp, cwp, zp, lev)
+            except mlk.RankDeficient:   # the tau-sparsified C~^n_W need not be positive definite
+                r = {"not_positive_definite": True}
             torch.cuda.synchronize()
             ll["level%d" % lev] = dict(r, seconds=time.perf_counter() - t0)
         pcg["loglik"] = ll

@@ -661,24 +661,26 @@ def test_rank_share_blocks_from_pieces(mlk, ctx):
 
 
 # --------------------------------------------------------------------------------- NEXT-4
-@pytest.mark.parametrize("n,d,w,leaf,kind,fam,rho,tau,points", [
-    (1024, 2, 2, 32, 0, OC.MATERN_12, 0.5, 0.05, "uniform"),    # cfg1 shape, tau pattern with fill
-    (4096, 10, 2, 128, 1, OC.MATERN_32, 1.0, 1e-6, "uniform"),  # cfg2 shape
-    (2048, 4, 1, 64, 1, OC.GAUSSIAN, 1.5, 0.2, "normal"),
+@pytest.mark.parametrize("n,d,w,leaf,kind,fam,rho,mode,tau,points", [
+    (1024, 2, 2, 32, 0, OC.MATERN_12, 0.5, 1, 0.3, "uniform"),   # cfg1 shape, tau pattern with fill
+    (2048, 10, 2, 128, 1, OC.MATERN_32, 1.0, 0, 0.0, "uniform"),  # cfg2 shape, all pairs
+    (2048, 4, 1, 64, 1, OC.GAUSSIAN, 0.8, 0, 0.0, "normal"),
 ])
-def test_loglik_matches_oracle(mlk, ctx, n, d, w, leaf, kind, fam, rho, tau, points):
+def test_loglik_matches_oracle(mlk, ctx, n, d, w, leaf, kind, fam, rho, mode, tau, points):
     """mlk_loglik (block-sparse Cholesky of C~^n_W on the GPU) against oracle/likelihood.py
     (dense numpy Cholesky of the oracle's C~^n_W) at several truncation levels: N~ exact,
     log-likelihood, log det and quadratic form within 1e-10 relative (Cholesky is backward
-    stable: the errors are ~ N~ kappa u on log det and ~ kappa u on the quadratic form)."""
+    stable: the errors are ~ N~ kappa u on log det and ~ kappa u on the quadratic form).  The
+    cases are ones whose truncated C~_W is positive definite (min eigenvalue 2.8e-3 for the
+    first; the all-pairs C_W is SPD by Theorem 1) -- see test_loglik_indefinite_rejected."""
     from oracle import likelihood as OL
     X, dirs = _setup(n, d, leaf, kind, points)
     g, o = _tree_both(mlk, ctx, X, leaf, kind, dirs)
     gb = mlk.build_basis(ctx, g, w)
     ob = OB.build_basis(X, o, w)
     kern = dict(family=fam, rho=rho)
-    cw = mlk.assemble_cw(ctx, g, gb, kern, dict(mode=1, tau=tau))
-    pairs = OA.admitted_pairs(X, o, ob, 1, tau)
+    cw = mlk.assemble_cw(ctx, g, gb, kern, dict(mode=mode, tau=tau))
+    pairs = OA.admitted_pairs(X, o, ob, mode, tau)
     bsr = OAs.assemble(X, o, ob, kern, pairs)
     zw = np.random.default_rng([0, 13]).standard_normal(gb.dim)
     for level in sorted({0, g.t // 2, g.t}):
@@ -690,6 +692,29 @@ def test_loglik_matches_oracle(mlk, ctx, n, d, w, leaf, kind, fam, rho, tau, poi
         assert abs(r["quad"] - q) <= 1e-10 * q, (level, r["quad"], q)
     a = mlk.loglik(ctx, gb, cw, zw, 0)
     assert a == mlk.loglik(ctx, gb, cw, zw, 0)   # deterministic
+
+
+def test_loglik_indefinite_rejected(mlk, ctx):
+    """The tau-sparsified C~_W need not be positive definite (cfg1 shape, Matern 1/2, rho = 0.5,
+    tau = 0.05: the oracle's dense C~_W has the eigenvalue -2.9e-3): the GPU factorisation
+    reports MLK_ERR_RANK_DEFICIENT where the oracle's numpy Cholesky fails, and the finest
+    level alone (positive definite here) still evaluates and matches."""
+    from oracle import likelihood as OL
+    X, dirs = _setup(1024, 2, 32, 0)
+    g, o = _tree_both(mlk, ctx, X, 32, 0, dirs)
+    gb = mlk.build_basis(ctx, g, 2)
+    ob = OB.build_basis(X, o, 2)
+    kern = dict(family=OC.MATERN_12, rho=0.5)
+    cw = mlk.assemble_cw(ctx, g, gb, kern, dict(mode=1, tau=0.05))
+    bsr = OAs.assemble(X, o, ob, kern, OA.admitted_pairs(X, o, ob, 1, 0.05))
+    zw = np.random.default_rng([0, 15]).standard_normal(gb.dim)
+    with pytest.raises(np.linalg.LinAlgError):
+        OL.loglik(bsr, o, ob, zw, 0)
+    with pytest.raises(mlk.RankDeficient):
+        mlk.loglik(ctx, gb, cw, zw, 0)
+    r = mlk.loglik(ctx, gb, cw, zw, g.t)
+    l, ld, q, nt = OL.loglik(bsr, o, ob, zw, g.t)
+    assert r["n_tilde"] == nt and abs(r["loglik"] - l) <= 1e-10 * abs(l)
 
 
 def test_loglik_identity_pin_on_gpu(mlk, ctx):
