@@ -6,13 +6,14 @@
 // log det = 2 sum log G_ii and the quadratic form from the same factor.
 //
 // The factorisation is a block-sparse right-looking Cholesky over the BSR cells: symbolic fill
-// on the host (block pattern of the factor's rows), then per block row j (in C_W order)
-//   1. L_jj = chol(A^_jj) and Linv = L_jj^-1                   (one CTA each)
-//   2. T_jk = Linv A^_jk for the k in the row's pattern, y_j = Linv z^_j   (one DMMA GEMM batch)
-//   3. A^_kl -= T_jk^T T_jl (k <= l in the pattern), z^_k -= T_jk^T y_j   (one DMMA GEMM batch)
-// T_j* is the block row j of G^T and is discarded after its step; y = G^-1 Z^n_W, so the
-// quadratic form is |y|^2.  Every update of a block happens in its own step, in row order:
-// deterministic.  The paper reorders with nested dissection before a sparse Cholesky (SuiteSparse);
+// on the host (block pattern of the factor's rows), then, for each wave of consecutive block
+// rows none of which is in another's pattern (e.g. the leaves not joined by extra pairs),
+//   1. L_jj = chol(A^_jj) and Linv_j = L_jj^-1                 (one CTA per row, batched)
+//   2. T_jk = Linv_j A^_jk for the k in row j's pattern, y_j = Linv_j z^_j   (one GEMM batch)
+//   3. partials T_jk^T T_jl (k <= l) and T_jk^T y_j             (one DMMA GEMM batch, TN mode)
+//   4. A^_kl -= the partials of (k, l) summed in row order, z^_k likewise (one kernel)
+// T_j* is the block row j of G^T and is discarded after its wave; y = G^-1 Z^n_W, so the
+// quadratic form is |y|^2.  Fixed summation orders throughout: deterministic.  The paper reorders with nested dissection before a sparse Cholesky (SuiteSparse);
 // the C_W order (finest level first, root last) already eliminates the leaves first, whose fill
 // stays among their ancestors (mutually admitted) except for the extra pairs of the tau search.
 #include <algorithm>
@@ -27,11 +28,20 @@ namespace {
 
 constexpr int kLlThreads = 256;
 
-// in-place lower Cholesky of one symmetric p x p block (row-major; the strict upper triangle is
-// zeroed), non-positive pivot -> flag; logd = sum log L_ii (fixed order)
-__global__ void __launch_bounds__(kLlThreads) k_ll_chol(double* __restrict__ A, int p, int* __restrict__ flag,
+struct DiagJob {
+  double* A;      // p x p symmetric block (row-major), factored in place (lower)
+  double* Linv;   // p x p output: L^-1
+  int32_t p, row; // size; block row (index into logd)
+};
+
+// in-place lower Cholesky of one symmetric p x p block per CTA (row-major; the strict upper
+// triangle is zeroed), non-positive pivot -> flag; logd[row] = sum log L_ii (fixed order).  The
+// trailing update is spread over all threads (element-wise), three barriers per column.
+__global__ void __launch_bounds__(kLlThreads) k_ll_chol(const DiagJob* __restrict__ jobs, int* __restrict__ flag,
                                                         double* __restrict__ logd) {
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const DiagJob jb = jobs[blockIdx.x];
+  double* A = jb.A;
+  const int p = jb.p, tid = threadIdx.x, nt = blockDim.x;
   __shared__ double s_d;
   for (int k = 0; k < p; k++) {
     if (tid == 0) {
@@ -44,9 +54,15 @@ __global__ void __launch_bounds__(kLlThreads) k_ll_chol(double* __restrict__ A, 
     const double inv = 1.0 / s_d;
     for (int i = k + 1 + tid; i < p; i += nt) A[(int64_t)i * p + k] *= inv;
     __syncthreads();
-    for (int j = k + 1 + tid; j < p; j += nt) {
-      const double ljk = A[(int64_t)j * p + k];
-      for (int i = j; i < p; i++) A[(int64_t)i * p + j] = fma(-A[(int64_t)i * p + k], ljk, A[(int64_t)i * p + j]);
+    // A[i][j] -= A[i][k] A[j][k] for k < j <= i < p: the (p-k-1)(p-k)/2 elements, row-major
+    const int m = p - k - 1;
+    for (int e = tid; e < m * (m + 1) / 2; e += nt) {
+      int i = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);  // row of the packed lower triangle
+      while (i * (i + 1) / 2 > e) i--;
+      while ((i + 1) * (i + 2) / 2 <= e) i++;
+      const int j = e - i * (i + 1) / 2;
+      const int gi = k + 1 + i, gj = k + 1 + j;
+      A[(int64_t)gi * p + gj] = fma(-A[(int64_t)gi * p + k], A[(int64_t)gj * p + k], A[(int64_t)gi * p + gj]);
     }
     __syncthreads();
   }
@@ -57,14 +73,17 @@ __global__ void __launch_bounds__(kLlThreads) k_ll_chol(double* __restrict__ A, 
   if (tid == 0) {
     double s = 0.0;
     for (int i = 0; i < p; i++) s += log(A[(int64_t)i * p + i]);
-    *logd = s;
+    logd[jb.row] = s;
   }
 }
 
-// X = L^-1 for a lower-triangular p x p L (row-major): thread per column c, forward
-// substitution of L x = e_c; X's strict upper triangle is zero
-__global__ void __launch_bounds__(kLlThreads) k_ll_trinv(const double* __restrict__ L, int p,
-                                                         double* __restrict__ X) {
+// Linv = L^-1 for the lower-triangular L of each job (row-major): thread per column c, forward
+// substitution of L x = e_c; the strict upper triangle of Linv is zero
+__global__ void __launch_bounds__(kLlThreads) k_ll_trinv(const DiagJob* __restrict__ jobs) {
+  const DiagJob jb = jobs[blockIdx.x];
+  const double* L = jb.A;
+  double* X = jb.Linv;
+  const int p = jb.p;
   for (int c = threadIdx.x; c < p; c += blockDim.x) {
     for (int i = 0; i < c; i++) X[(int64_t)i * p + c] = 0.0;
     for (int i = c; i < p; i++) {
@@ -72,6 +91,22 @@ __global__ void __launch_bounds__(kLlThreads) k_ll_trinv(const double* __restric
       for (int k = c; k < i; k++) s = fma(-L[(int64_t)i * p + k], X[(int64_t)k * p + c], s);
       X[(int64_t)i * p + c] = s / L[(int64_t)i * p + i];
     }
+  }
+}
+
+// target -= sum of its partials in row order (one CTA per target; partials of one target are
+// consecutive in `part`, `len` doubles each)
+struct RedJob {
+  double* dst;
+  int64_t first, len;
+  int32_t count;
+};
+__global__ void k_ll_reduce(const RedJob* __restrict__ jobs, const double* __restrict__ part) {
+  const RedJob jb = jobs[blockIdx.x];
+  for (int64_t e = threadIdx.x; e < jb.len; e += blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < jb.count; r++) s += part[jb.first + (int64_t)r * jb.len + e];
+    jb.dst[e] -= s;
   }
 }
 
@@ -169,59 +204,139 @@ mlk_status mlk_loglik(mlk_ctx ctx, mlk_basis basis, mlk_cw cw, int32_t level, co
   CUDA_CHECK(cudaMemcpyAsync(zh.p, zin.p, sizeof(double) * nt, cudaMemcpyDeviceToDevice, st));
   DevBuf<int> flag(1, st);
   flag.zero();
-  int pmax = 0;
-  int64_t rowmax = 0;
-  for (int j = 0; j < K; j++) {
-    pmax = std::max(pmax, p[j]);
-    int64_t r = 0;
-    for (int k : pat[j]) r += (int64_t)p[j] * p[k];
-    rowmax = std::max(rowmax, r);
+  // ---- numeric, in waves: consecutive block rows none of which appears in another's pattern
+  // (so no row of a wave updates another) are factored together; their updates go to per-row
+  // partials that are subtracted from each target in row order (deterministic)
+  std::vector<std::pair<int, int>> waves;  // [first, last) rows
+  {
+    int w0 = 0;
+    std::set<int> touched;  // rows updated by the current wave
+    const int64_t cap = std::max<int64_t>(c.scratch_budget_bytes() / 8 / 4, (int64_t)1 << 20);  // doubles
+    int64_t wbytes = 0;
+    for (int j = 0; j < K; j++) {
+      int64_t need = (int64_t)p[j] * p[j];
+      for (int k : pat[j]) need += (int64_t)p[j] * p[k] + (int64_t)p[k];
+      for (int k : pat[j])
+        for (int l : pat[j])
+          if (k <= l) need += (int64_t)p[k] * p[l];
+      if (j > w0 && (touched.count(j) || wbytes + need > cap)) {
+        waves.push_back({w0, j});
+        w0 = j;
+        touched.clear();
+        wbytes = 0;
+      }
+      wbytes += need;
+      for (int k : pat[j]) touched.insert(k);
+    }
+    waves.push_back({w0, K});
   }
-  DevBuf<double> Linv((size_t)pmax * pmax, st), T((size_t)std::max<int64_t>(rowmax, 1), st);
-
-  for (int j = 0; j < K; j++) {
-    const int pj = p[j];
-    double* Ajj = Ah.p + diag_off[j];
+  for (auto& wv : waves) {
+    const int j0 = wv.first, j1 = wv.second;
+    // scratch layout: Linv per row, T_jk per (row, pattern column), partials per target
+    std::vector<DiagJob> dj;
+    std::vector<GemmDesc> g1, g2;
+    std::map<std::pair<int, int>, std::vector<int64_t>> tpart;  // target (k, l) -> partial offsets
+    std::map<int, std::vector<int64_t>> zpart;                  // k -> z partial offsets
+    int64_t off = 0;
+    std::vector<int64_t> linv_off(j1 - j0);
+    std::vector<std::vector<std::pair<int, int64_t>>> trow(j1 - j0);
+    for (int j = j0; j < j1; j++) {
+      linv_off[j - j0] = off;
+      off += (int64_t)p[j] * p[j];
+      for (int k : pat[j]) {
+        trow[j - j0].push_back({k, off});
+        off += (int64_t)p[j] * p[k];
+      }
+    }
+    const int64_t part0 = off;
+    for (int j = j0; j < j1; j++)
+      for (size_t a = 0; a < trow[j - j0].size(); a++) {
+        const int k = trow[j - j0][a].first;
+        for (size_t b = a; b < trow[j - j0].size(); b++) {
+          const int l = trow[j - j0][b].first;
+          tpart[{k, l}].push_back(off);
+          off += (int64_t)p[k] * p[l];
+        }
+        zpart[k].push_back(off);
+        off += p[k];
+      }
+    // partials of one target must be consecutive: lay them out target by target
+    std::map<int64_t, int64_t> remap;  // provisional offset -> final offset
+    {
+      int64_t o2 = part0;
+      for (auto& kv : tpart)
+        for (int64_t x : kv.second) {
+          remap[x] = o2;
+          o2 += (int64_t)p[kv.first.first] * p[kv.first.second];
+        }
+      for (auto& kv : zpart)
+        for (int64_t x : kv.second) {
+          remap[x] = o2;
+          o2 += p[kv.first];
+        }
+    }
+    DevBuf<double> S((size_t)std::max<int64_t>(off, 1), st);
+    for (int j = j0; j < j1; j++)
+      dj.push_back({Ah.p + diag_off[j], S.p + linv_off[j - j0], p[j], j});
+    DevBuf<DiagJob> djd(dj.size(), st);
+    djd.upload(dj);
     {
       TimedLaunch tl(c, "loglik_diag_chol");
-      k_ll_chol<<<1, kLlThreads, 0, st>>>(Ajj, pj, flag.p, logd.p + j);
+      k_ll_chol<<<(unsigned)dj.size(), kLlThreads, 0, st>>>(djd.p, flag.p, logd.p);
       check_launch("k_ll_chol");
-      k_ll_trinv<<<1, kLlThreads, 0, st>>>(Ajj, pj, Linv.p);
+      k_ll_trinv<<<(unsigned)dj.size(), kLlThreads, 0, st>>>(djd.p);
       check_launch("k_ll_trinv");
     }
-    const double* zj = zh.p + basis->row_off[j];
-    double* yj = y.p + basis->row_off[j];
-    std::vector<GemmDesc> g1, g2;
-    std::vector<std::pair<int, int64_t>> trow;  // (k, offset of T_jk in T)
-    int64_t to = 0;
-    for (int k : pat[j]) {
-      trow.push_back({k, to});
-      to += (int64_t)pj * p[k];
+    // 2. T_jk = Linv_j A^_jk, y_j = Linv_j z^_j
+    for (int j = j0; j < j1; j++) {
+      const int pj = p[j];
+      const double* Lj = S.p + linv_off[j - j0];
+      for (auto& tk : trow[j - j0])
+        g1.push_back(GemmDesc{Lj, pj, Ah.p + boff[j][tk.first], p[tk.first], S.p + tk.second, p[tk.first], pj,
+                              p[tk.first], pj, 0});
+      g1.push_back(GemmDesc{Lj, pj, zh.p + basis->row_off[j], 1, y.p + basis->row_off[j], 1, pj, 1, pj, 0});
     }
-    // 2. T_jk = Linv A^_jk, y_j = Linv z^_j
-    for (auto& tk : trow) {
-      const int k = tk.first;
-      g1.push_back(GemmDesc{Linv.p, pj, Ah.p + boff[j][k], p[k], T.p + tk.second, p[k], pj, p[k], pj, 0});
-    }
-    g1.push_back(GemmDesc{Linv.p, pj, zj, 1, yj, 1, pj, 1, pj, 0});
     gemm_batched(c, g1, "loglik_rowsolve");
-    // 3. A^_kl -= T_jk^T T_jl (k <= l), z^_k -= T_jk^T y_j
-    for (size_t a = 0; a < trow.size(); a++) {
-      const int k = trow[a].first;
-      for (size_t b = a; b < trow.size(); b++) {
-        const int l = trow[b].first;
-        double* dst = k == l ? Ah.p + diag_off[k] : Ah.p + boff[k][l];
-        GemmDesc g{T.p + trow[a].second, p[k], T.p + trow[b].second, p[l], dst, p[l], p[k], p[l], pj, 0};
-        g.sub = 1;
-        g.trans_a = 1;
-        g2.push_back(g);
+    // 3. partials T_jk^T T_jl (k <= l) and T_jk^T y_j, in the provisional (row-major) order
+    {
+      int64_t o = part0;
+      for (int j = j0; j < j1; j++) {
+        const int pj = p[j];
+        auto& tr = trow[j - j0];
+        for (size_t a = 0; a < tr.size(); a++) {
+          const int k = tr[a].first;
+          for (size_t b = a; b < tr.size(); b++) {
+            const int l = tr[b].first;
+            GemmDesc g{S.p + tr[a].second, p[k], S.p + tr[b].second, p[l], S.p + remap[o], p[l], p[k], p[l], pj, 0};
+            g.trans_a = 1;
+            g2.push_back(g);
+            o += (int64_t)p[k] * p[l];
+          }
+          GemmDesc gz{S.p + tr[a].second, p[k], y.p + basis->row_off[j], 1, S.p + remap[o], 1, p[k], 1, pj, 0};
+          gz.trans_a = 1;
+          g2.push_back(gz);
+          o += p[k];
+        }
       }
-      GemmDesc gz{T.p + trow[a].second, p[k], yj, 1, zh.p + basis->row_off[k], 1, p[k], 1, pj, 0};
-      gz.sub = 1;
-      gz.trans_a = 1;
-      g2.push_back(gz);
     }
     gemm_batched(c, g2, "loglik_update");
+    // 4. subtract the partials from their targets in row order
+    std::vector<RedJob> rj;
+    for (auto& kv : tpart) {
+      const int k = kv.first.first, l = kv.first.second;
+      double* dst = k == l ? Ah.p + diag_off[k] : Ah.p + boff[k][l];
+      rj.push_back({dst, remap[kv.second.front()], (int64_t)p[k] * p[l], (int32_t)kv.second.size()});
+    }
+    for (auto& kv : zpart)
+      rj.push_back({zh.p + basis->row_off[kv.first], remap[kv.second.front()], (int64_t)p[kv.first],
+                    (int32_t)kv.second.size()});
+    if (!rj.empty()) {
+      DevBuf<RedJob> rjd(rj.size(), st);
+      rjd.upload(rj);
+      TimedLaunch tl(c, "loglik_reduce");
+      k_ll_reduce<<<(unsigned)rj.size(), 256, 0, st>>>(rjd.p, S.p);
+      check_launch("k_ll_reduce");
+    }
   }
   k_ll_finish<<<1, 32, 0, st>>>(logd.p, K, y.p, nt, res.p);
   check_launch("k_ll_finish");
