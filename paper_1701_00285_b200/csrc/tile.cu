@@ -211,8 +211,13 @@ struct TileCfg {
   // occupancy, >= 2): the one-group class (C a, tiny cells) has short stages, so it wants a
   // deeper ring to cover the TMA latency
   static constexpr int NST = RQ == 1 ? 6 : (RQ >= 16 ? 2 : 3);
+#ifdef MLK_K5A_OCC5  // experiment: 5 CTAs per SM for the 6-9 group classes, fewer held W fragments
+  static constexpr int MIN_CTAS = RQ >= 20 ? 3 : ((RQ >= 6 && RQ <= 9) ? 5 : 4);
+  static constexpr int G = RQ <= 12 ? ((RQ >= 6 && RQ <= 9) ? 4 : RQ) : 8;
+#else
   static constexpr int MIN_CTAS = RQ >= 20 ? 3 : 4;  // __launch_bounds__ minimum
   static constexpr int G = RQ <= 12 ? RQ : 8;    // W_b fragments held per DMMA group
+#endif
   static constexpr int NACC = 1;                 // accumulator sets (2 measured no faster)
 };
 
@@ -432,7 +437,41 @@ __global__ void __launch_bounds__(128, TileCfg<RQ>::MIN_CTAS)
             accv[l] = fma(cv[t][1], wv.y, accv[l]);
           }
         }
-        if constexpr (SYM) {
+        if constexpr (SYM && NV == 1) {
+          // column part, one vector: the 2T values of a lane (its two columns per sub-tile) are
+          // summed over the warp's 8 rows (the lanes with equal lane & 3) by a reduce-scatter
+          // (recursive halving over the row bits: 2T - 2 adds per lane instead of 3 x 2T for an
+          // all-reduce, and each lane stores its own 2T/8 sums -- the kernel was issue-bound);
+          // lane row r ends with the values r Q .. r Q + Q - 1
+          constexpr int NVAL = 2 * T, P8 = (NVAL + 7) / 8 * 8, Q = P8 / 8;
+          double v[P8];
+#pragma unroll
+          for (int t = 0; t < T; t++) {
+            v[2 * t] = cvc[t][0] * arow[0];
+            v[2 * t + 1] = cvc[t][1] * arow[0];
+          }
+#pragma unroll
+          for (int i = NVAL; i < P8; i++) v[i] = 0.0;
+          const int r = lane >> 2;
+#pragma unroll
+          for (int step = 0; step < 3; step++) {
+            const int half = P8 >> (step + 1);
+            const int mask = 16 >> step;       // lane bits 4, 3, 2 = row bits 2, 1, 0
+            const bool up = (r & (4 >> step)) != 0;
+#pragma unroll
+            for (int i = 0; i < half; i++) {
+              const double keep = up ? v[i + half] : v[i];
+              const double send = up ? v[i] : v[i + half];
+              v[i] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < Q; q++) {
+            const int idx = r * Q + q;
+            const int y = yb + 8 * (idx >> 1) + 2 * (lane & 3) + (idx & 1);
+            if (idx < NVAL && y < u.s_b && u.qc > 0) colpart[u.cp_off + (int64_t)warp * u.s_b + y] = v[q];
+          }
+        } else if constexpr (SYM) {
           // column part: sum over the warp's 8 rows (lanes with equal lane & 3), lanes 0..3
           // keep the sums of their columns
 #pragma unroll

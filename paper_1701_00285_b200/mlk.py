@@ -12,7 +12,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmlk.so")
+# MLK_LIB_VARIANT=name loads the in-tree libmlk_<name>.so (A/B experiments, tools/build_variant.py)
+LIB_PATH = os.path.join(_HERE, "libmlk%s.so" % ("_" + os.environ["MLK_LIB_VARIANT"]
+                                               if os.environ.get("MLK_LIB_VARIANT") else ""))
 if not os.path.exists(LIB_PATH):
     raise ImportError("libmlk.so is not built (run `python -m paper_1701_00285_b200.build` or "
                       "__graft_entry__.build()); there is no CPU fallback")
