@@ -211,13 +211,9 @@ struct TileCfg {
   // occupancy, >= 2): the one-group class (C a, tiny cells) has short stages, so it wants a
   // deeper ring to cover the TMA latency
   static constexpr int NST = RQ == 1 ? 6 : (RQ >= 16 ? 2 : 3);
-#ifdef MLK_K5A_OCC5  // experiment: 5 CTAs per SM for the 6-9 group classes, fewer held W fragments
-  static constexpr int MIN_CTAS = RQ >= 20 ? 3 : ((RQ >= 6 && RQ <= 9) ? 5 : 4);
-  static constexpr int G = RQ <= 12 ? ((RQ >= 6 && RQ <= 9) ? 4 : RQ) : 8;
-#else
-  static constexpr int MIN_CTAS = RQ >= 20 ? 3 : 4;  // __launch_bounds__ minimum
+  static constexpr int MIN_CTAS = RQ >= 20 ? 3 : 4;  // __launch_bounds__ minimum (5 CTAs with 4
+                                                     // held W fragments measured 1.7 % slower)
   static constexpr int G = RQ <= 12 ? RQ : 8;    // W_b fragments held per DMMA group
-#endif
   static constexpr int NACC = 1;                 // accumulator sets (2 measured no faster)
 };
 
@@ -323,8 +319,11 @@ __global__ void __launch_bounds__(128, TileCfg<RQ>::MIN_CTAS)
     const int nst = (u.s_b + BN - 1) / BN;
 
     // fill the ring slot of stage s (called by one whole warp)
-    auto issue = [&](int s) {
-      const int slot = (gs + s) % nring;
+    // ring position of this task's first stage (one division per task; per stage the slot and
+    // the mbarrier parity advance incrementally)
+    const int slot0 = gs % nring;
+    const unsigned par0 = (unsigned)((gs / nring) & 1);
+    auto issue = [&](int s, int slot) {
       double* Xs = St + slot * sd;
       double* Ws = Xs + BN * sdp;
       const int b0 = s * BN, nb = min(BN, u.s_b - b0);
@@ -353,7 +352,7 @@ __global__ void __launch_bounds__(128, TileCfg<RQ>::MIN_CTAS)
     };
 
     if (warp == 0)
-      for (int s = 0; s < min(nring, nst); s++) issue(s);
+      for (int s = 0, sl = slot0; s < min(nring, nst); s++, sl = sl + 1 == nring ? 0 : sl + 1) issue(s, sl);
     cp_async_wait<0>();
     __syncthreads();  // As visible
 
@@ -382,9 +381,10 @@ __global__ void __launch_bounds__(128, TileCfg<RQ>::MIN_CTAS)
       for (int l = 0; l < NV; l++)  // sigma2 folded in here (the row part gets it in the epilogue)
         arow[l] = (ar < rows && l < u.qc) ? kp.sigma2 * u.Wb[(int64_t)l * u.ldw + ga] : 0.0;
     }
+    int slot = slot0;
+    unsigned par = par0;
     for (int s = 0; s < nst; s++) {
-      const int g = gs + s, slot = g % nring;
-      mbar_wait(&full[slot], (unsigned)((g / nring) & 1));
+      mbar_wait(&full[slot], par);
       const double* Xs = St + slot * sd;
       const double* Ws = Xs + BN * sdp;
       const int yb = s * BN;                       // first b point of the stage (local index)
@@ -535,7 +535,11 @@ __global__ void __launch_bounds__(128, TileCfg<RQ>::MIN_CTAS)
       last = __shfl_sync(0xffffffffu, last, 0);
       if (last) {
         if (lane == 0) cnt[slot] = 0;
-        if (s + nring < nst) issue(s + nring);
+        if (s + nring < nst) issue(s + nring, slot);  // stage s + nring reuses this slot
+      }
+      if (++slot == nring) {
+        slot = 0;
+        par ^= 1u;
       }
     }
     gs += nst;
