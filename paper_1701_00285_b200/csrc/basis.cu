@@ -163,9 +163,10 @@ __global__ void __launch_bounds__(kQrThreads) k_qr_wy(const QrJob* __restrict__ 
   // triangular), x has nonzeros only in rows nc..nc+k and the structure is preserved, so
   // rows nc..nc+k (exactly the entries LAPACK's dense sweep would change).
   const bool stk = jb.stacked != 0;
-  // Thread j owns column j: its dot x . a_j is a serial sum (four partial sums, no shuffles)
-  // and its update touches only its column; the odd column stride keeps the column-strided
-  // accesses of a half-warp in distinct banks.  Two barriers per step.
+  const int lane = tid & 31, sub = tid & 3, cq = tid >> 2, ncq = nt >> 2;
+  const unsigned qmask = 0xFu << (lane & ~3);
+  // A quad of threads owns column j (below); the odd column stride keeps the column-strided
+  // accesses of different quads in distinct banks.  Two barriers per step.
   for (int k = 0; k < nc; k++) {
     const double* ak = A + (int64_t)k * lda;
     const int lo = stk ? nc : k + 1, hi = stk ? nc + k + 1 : m;
@@ -176,62 +177,66 @@ __global__ void __launch_bounds__(kQrThreads) k_qr_wy(const QrJob* __restrict__ 
       for (int i = plo + tid; i < phi; i += nt) ap[i] *= pv[1];
       if (tid == 0) ap[k - 1] = pv[2];
     }
-    // (1) dots for the columns j >= k; the owner of column k forms the reflector
-    for (int j = k + tid; j < nc; j += nt) {
+    // (1) dots for the columns j >= k, a quad of threads per column: lane `sub` of the quad
+    // sums the rows lo + sub + 4 m (the tail rows go to sub 0), then two in-quad shuffles add
+    // (s0 + s1) + (s2 + s3) -- the same partial sums and order as one thread with four
+    // accumulators, so the factors are unchanged, at a quarter of the per-thread row work.
+    // The owner quad of column k forms the reflector.
+    const int nfull = (hi - lo) & ~3;
+    for (int j = k + cq; j < nc; j += ncq) {
       const double* aj = A + (int64_t)j * lda;
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      int i = lo;
-#pragma unroll 2
-      for (; i + 3 < hi; i += 4) {
-        s0 = fma(ak[i], aj[i], s0);
-        s1 = fma(ak[i + 1], aj[i + 1], s1);
-        s2 = fma(ak[i + 2], aj[i + 2], s2);
-        s3 = fma(ak[i + 3], aj[i + 3], s3);
-      }
-      for (; i < hi; i++) s0 = fma(ak[i], aj[i], s0);
-      const double sum = (s0 + s1) + (s2 + s3);
-      if (j == k) {
-        const double alpha = ak[k];
-        double tau = 0.0, scal = 1.0, beta = alpha;
-        if (sum > 0.0) {
-          beta = -copysign(sqrt(fma(alpha, alpha, sum)), alpha);
-          tau = (beta - alpha) / beta;
-          scal = 1.0 / (alpha - beta);
+      double sp = 0.0;
+#pragma unroll 4
+      for (int i = lo + sub; i < lo + nfull; i += 4) sp = fma(ak[i], aj[i], sp);
+      if (sub == 0)
+        for (int i = lo + nfull; i < hi; i++) sp = fma(ak[i], aj[i], sp);
+      sp += __shfl_xor_sync(qmask, sp, 1);
+      sp += __shfl_xor_sync(qmask, sp, 2);
+      if (sub == 0) {
+        const double sum = sp;
+        if (j == k) {
+          const double alpha = ak[k];
+          double tau = 0.0, scal = 1.0, beta = alpha;
+          if (sum > 0.0) {
+            beta = -copysign(sqrt(fma(alpha, alpha, sum)), alpha);
+            tau = (beta - alpha) / beta;
+            scal = 1.0 / (alpha - beta);
+          }
+          taus[k] = tau;
+          double* pv = s_piv + 3 * (k & 1);
+          pv[0] = tau;
+          pv[1] = scal;
+          pv[2] = beta;
+        } else {
+          dots[j] = sum;
         }
-        taus[k] = tau;
-        double* pv = s_piv + 3 * (k & 1);
-        pv[0] = tau;
-        pv[1] = scal;
-        pv[2] = beta;
-      } else {
-        dots[j] = sum;
       }
     }
     __syncthreads();
-    // (2) a_j -= f (e_k + scal x), f = tau (a_kj + scal d_j), for the owned columns j > k
+    // (2) a_j -= f (e_k + scal x), f = tau (a_kj + scal d_j), for the columns j > k (a quad per
+    // column, rows strided over its four lanes)
     const double tau = s_piv[3 * (k & 1)];
     if (tau != 0.0) {
       const double scal = s_piv[3 * (k & 1) + 1];
-      for (int j = k + 1 + tid; j < nc; j += nt) {
+      for (int j = k + 1 + cq; j < nc; j += ncq) {
         double* __restrict__ aj = A + (int64_t)j * lda;
         const double* __restrict__ xk = ak;
         const double f = tau * fma(scal, dots[j], aj[k]);
         const double g = f * scal;
-        aj[k] -= f;
-        // columns j and k never alias: stage 8 loads before the 8 stores (the compiler cannot
-        // prove it and would serialise load - fma - store per element)
-        int i = lo;
-        for (; i + 7 < hi; i += 8) {
-          double x[8], y[8];
+        __syncwarp(qmask);  // every lane has read aj[k] before sub 0 changes it
+        if (sub == 0) aj[k] -= f;
+        int i = lo + sub;
+        for (; i + 12 < hi; i += 16) {
+          double x[4], y[4];
 #pragma unroll
-          for (int u = 0; u < 8; u++) {
-            x[u] = xk[i + u];
-            y[u] = aj[i + u];
+          for (int u = 0; u < 4; u++) {
+            x[u] = xk[i + 4 * u];
+            y[u] = aj[i + 4 * u];
           }
 #pragma unroll
-          for (int u = 0; u < 8; u++) aj[i + u] = fma(-g, x[u], y[u]);
+          for (int u = 0; u < 4; u++) aj[i + 4 * u] = fma(-g, x[u], y[u]);
         }
-        for (; i < hi; i++) aj[i] = fma(-g, xk[i], aj[i]);
+        for (; i < hi; i += 4) aj[i] = fma(-g, xk[i], aj[i]);
       }
     }
     __syncthreads();
