@@ -16,6 +16,7 @@
 //   4. accumulates U (8 rows x 8 RQ columns) with 2 RQ DMMAs.
 // A persistent grid pulls units (largest first) from an atomic counter.
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdlib>
 #include <map>
@@ -206,7 +207,7 @@ struct TileCfg {
   // b points per stage.  BN = 8 (mod 16) makes a W row 8 BN doubles = 64 (mod 128) bytes, so
   // the 16-byte B-fragment loads of a quarter-warp (2 rows x 4 chunks) hit distinct banks
   // without any swizzle -- which a 1-D bulk copy could not apply
-  static constexpr int BN = RQ >= 6 ? 24 : (RQ == 1 ? 56 : 40);
+  static constexpr int BN = RQ >= 6 ? 24 : (RQ == 1 ? 56 : 40);  // 40 for RQ 6-9 measured 13 % slower on cfg4
   // maximum stages in the smem ring (the launch uses the deepest ring that keeps the target
   // occupancy, >= 2): the one-group class (C a, tiny cells) has short stages, so it wants a
   // deeper ring to cover the TMA latency
@@ -375,6 +376,11 @@ __global__ void __launch_bounds__(128, TileCfg<RQ>::MIN_CTAS)
 
     const int ar = warp * 8 + (lane >> 2);
     const int64_t ga = a0 + ar;
+    // the lane's row as a local b index (dga) and the CTA's rows' range [dga_lo, dga_hi], clamped
+    // to int: b points are local indices 0 .. s_b - 1, so a far-away row never matches
+    auto clamp_i = [](int64_t x) { return (int)max((int64_t)INT_MIN / 2, min((int64_t)INT_MAX / 2, x)); };
+    const int dga = clamp_i(ga - u.b_begin);
+    const int dga_lo = clamp_i(a0 - u.b_begin), dga_hi = clamp_i(a0 + rows - 1 - u.b_begin);
     double arow[SYM ? NV : 1];  // a_i of the lane's row (column part of the symmetric product)
     if constexpr (SYM) {
 #pragma unroll
@@ -402,26 +408,44 @@ __global__ void __launch_bounds__(128, TileCfg<RQ>::MIN_CTAS)
       }
       // 2. covariances in registers: closed form, same-site entries exactly 1 + nugget/sigma2,
       //    points past the range exactly 0 (their stage rows are stale)
+      // masks only where a stage can need them (warp-uniform tests): the CTA's rows inside the
+      // stage's b range (same-site entries; for SYM the diagonal j vs i), and the range end
+      // (SYM: any stage starting at or before the last row needs the j <= i masks)
+      const bool diag = SYM ? yb <= dga_hi : (dga_lo < yb + BN && yb <= dga_hi);
+      const bool tail = yb + BN > u.s_b;
       double cv[T][2];
 #pragma unroll
       for (int t = 0; t < T; t++) {
-        const int y = yb + 8 * t + 2 * (lane & 3);
 #pragma unroll
-        for (int e = 0; e < 2; e++) {
-          const double v = corr<FAM>(gr[t][e], s_tab, kp);
-          cv[t][e] = (u.b_begin + y + e == ga) ? kp.same_val : v;
-          if (y + e >= u.s_b) cv[t][e] = 0.0;
+        for (int e = 0; e < 2; e++) cv[t][e] = corr<FAM>(gr[t][e], s_tab, kp);
+      }
+      if (diag || tail) {
+#pragma unroll
+        for (int t = 0; t < T; t++) {
+          const int y = yb + 8 * t + 2 * (lane & 3);
+#pragma unroll
+          for (int e = 0; e < 2; e++) {
+            if (y + e == dga) cv[t][e] = kp.same_val;
+            if (y + e >= u.s_b) cv[t][e] = 0.0;
+          }
         }
       }
-      double cvc[SYM ? T : 1][2];  // column-part weights: j > i only
+      double cvc[SYM ? T : 1][2];  // column-part weights: j > i only (arow is 0 past the rows)
       if constexpr (SYM) {
 #pragma unroll
         for (int t = 0; t < T; t++) {
 #pragma unroll
-          for (int e = 0; e < 2; e++) {
-            const int64_t j = u.b_begin + yb + 8 * t + 2 * (lane & 3) + e;
-            cvc[t][e] = (j > ga && ar < rows) ? cv[t][e] : 0.0;
-            if (j < ga) cv[t][e] = 0.0;  // row part: j >= i only
+          for (int e = 0; e < 2; e++) cvc[t][e] = cv[t][e];
+        }
+        if (diag) {
+#pragma unroll
+          for (int t = 0; t < T; t++) {
+            const int y = yb + 8 * t + 2 * (lane & 3);
+#pragma unroll
+            for (int e = 0; e < 2; e++) {
+              if (y + e <= dga) cvc[t][e] = 0.0;
+              if (y + e < dga) cv[t][e] = 0.0;  // row part: j >= i only
+            }
           }
         }
       }
@@ -640,6 +664,10 @@ int class_bn(int rq) {
   switch (rq) {
     case 1: case -1: case -2: case -4: return TileCfg<1>::BN;
     case 2: case 3: case 4: return TileCfg<2>::BN;
+    case 6: return TileCfg<6>::BN;
+    case 7: return TileCfg<7>::BN;
+    case 8: return TileCfg<8>::BN;
+    case 9: return TileCfg<9>::BN;
     default: return TileCfg<24>::BN;
   }
 }
