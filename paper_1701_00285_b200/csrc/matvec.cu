@@ -25,9 +25,19 @@ __global__ void k_apply_wt(const CellJob* __restrict__ jobs, const double* __res
   for (int x = blockIdx.y * blockDim.x + threadIdx.x; x < jb.s; x += gridDim.y * blockDim.x) {
     for (int iv = 0; iv < nvec; iv++) {
       const double* vv = v + (int64_t)iv * dim + jb.row_off;
-      double s = 0.0;
-      for (int r = 0; r < jb.p; r++) s = fma(jb.W[(int64_t)r * jb.s + x], vv[r], s);
-      a[(int64_t)iv * n + jb.pt_begin + x] += s;
+      // four partial sums: four independent W loads in flight per thread (the pass is bound by
+      // memory-level parallelism, one accumulator left it latency-bound at ~0.5 TB/s)
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      const double* w = jb.W + x;
+      int r = 0;
+      for (; r + 3 < jb.p; r += 4) {
+        s0 = fma(w[(int64_t)r * jb.s], vv[r], s0);
+        s1 = fma(w[(int64_t)(r + 1) * jb.s], vv[r + 1], s1);
+        s2 = fma(w[(int64_t)(r + 2) * jb.s], vv[r + 2], s2);
+        s3 = fma(w[(int64_t)(r + 3) * jb.s], vv[r + 3], s3);
+      }
+      for (; r < jb.p; r++) s0 = fma(w[(int64_t)r * jb.s], vv[r], s0);
+      a[(int64_t)iv * n + jb.pt_begin + x] += (s0 + s1) + (s2 + s3);
     }
   }
 }
@@ -43,8 +53,16 @@ __global__ void k_apply_w(const CellJob* __restrict__ jobs, const double* __rest
     const double* w = jb.W + (int64_t)r * jb.s;
     for (int iv = 0; iv < nvec; iv++) {
       const double* bb = b + (int64_t)iv * n + jb.pt_begin;
-      double s = 0.0;
-      for (int x = lane; x < jb.s; x += 32) s = fma(w[x], bb[x], s);
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;  // four loads in flight per lane
+      int x = lane;
+      for (; x + 96 < jb.s; x += 128) {
+        s0 = fma(w[x], bb[x], s0);
+        s1 = fma(w[x + 32], bb[x + 32], s1);
+        s2 = fma(w[x + 64], bb[x + 64], s2);
+        s3 = fma(w[x + 96], bb[x + 96], s3);
+      }
+      for (; x < jb.s; x += 32) s0 = fma(w[x], bb[x], s0);
+      double s = (s0 + s1) + (s2 + s3);
       for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       if (lane == 0) y[(int64_t)iv * dim + jb.row_off + r] = s;
     }
