@@ -53,16 +53,8 @@ __global__ void k_apply_w(const CellJob* __restrict__ jobs, const double* __rest
     const double* w = jb.W + (int64_t)r * jb.s;
     for (int iv = 0; iv < nvec; iv++) {
       const double* bb = b + (int64_t)iv * n + jb.pt_begin;
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;  // four loads in flight per lane
-      int x = lane;
-      for (; x + 96 < jb.s; x += 128) {
-        s0 = fma(w[x], bb[x], s0);
-        s1 = fma(w[x + 32], bb[x + 32], s1);
-        s2 = fma(w[x + 64], bb[x + 64], s2);
-        s3 = fma(w[x + 96], bb[x + 96], s3);
-      }
-      for (; x < jb.s; x += 32) s0 = fma(w[x], bb[x], s0);
-      double s = (s0 + s1) + (s2 + s3);
+      double s = 0.0;
+      for (int x = lane; x < jb.s; x += 32) s = fma(w[x], bb[x], s);
       for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       if (lane == 0) y[(int64_t)iv * dim + jb.row_off + r] = s;
     }
