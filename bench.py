@@ -416,6 +416,8 @@ def main():
                      "pct_of_peak_step": 100.0 * flops / (ms_per_step * 1e-3) / 1e12 / peak,
                      "peak_tflops": peak, "peak_source": "measured, profiles/fp64_peak_r01.json (DMMA loop)"},
             "roofline": {"kernel": "assemble_tile_contract (K5a)", "bound": "tensor",
+                         "peak_source": "of measured: FP64 DMMA loop on this pool's B200 (tools/fp64_peak.cu, "
+                                        "profiles/fp64_peak_r01.json; MEASURED_PEAKS.json holds bf16/HBM only)",
                          "pipe": "FP64 DMMA.8x8x4 (shares the FP64 pipe with DFMA, DESIGN.md section 6)", "achieved": achieved,
                          "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_flops_per_step": k5_flops, "ms_per_step": k5_ms_per_step},
