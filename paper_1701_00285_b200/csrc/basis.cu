@@ -101,6 +101,10 @@ struct QrJob {
   double* qhi;    // rows j >= nc of Q^T at qhi + (j - nc)*ldq
   int64_t ldq;
   int32_t stacked;  // 1: A = [R_L; R_R] (m = 2 nc, both upper triangular), see k_qr_wy
+  // stacked jobs: R_L, R_R (nc x nc row-major); the shared-memory QR reads them directly and
+  // A is formed (k_stack_r) only for the global-memory and blocked paths
+  const double* RL = nullptr;
+  const double* RR = nullptr;
 };
 
 constexpr int kQrSmemLimit = 225 * 1024;
@@ -140,13 +144,37 @@ __global__ void __launch_bounds__(kQrThreads) k_qr_wy(const QrJob* __restrict__ 
   double* G = GS ? A + (int64_t)lda * nc : jb.T;    // G[q][l], q < l, row-major nc x nc
   const int tid = threadIdx.x, nt = blockDim.x;
   QR_STAMP(0);
-  if (SMEM) {
+  if (SMEM && jb.RL) {
+    // [R_L; R_R] straight from the children's R (row-major nc x nc each): coalesced reads in the
+    // source order, transposed into the column-major shared copy
+    const int nn = nc * nc;
+    for (int f0 = tid; f0 < 2 * nn; f0 += 4 * nt) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int f = f0 + u * nt;
+        v[u] = f < nn ? jb.RL[f] : (f < 2 * nn ? jb.RR[f - nn] : 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int f = f0 + u * nt;
+        if (f < 2 * nn) {
+          const int half = f >= nn, r = f - half * nn, il = r / nc, j = r - il * nc;
+          A[(int64_t)j * lda + il + half * nc] = v[u];
+        }
+      }
+    }
+    __syncthreads();
+  } else if (SMEM) {
     // four independent global loads in flight per thread
     const int64_t tot = (int64_t)m * nc;
     for (int64_t e0 = tid; e0 < tot; e0 += 4 * (int64_t)nt) {
       double v[4];
 #pragma unroll
-      for (int u = 0; u < 4; u++) v[u] = e0 + u * nt < tot ? jb.A[e0 + u * nt] : 0.0;
+      for (int u = 0; u < 4; u++) {
+        const int64_t e = e0 + u * nt;
+        v[u] = e < tot ? jb.A[e] : 0.0;
+      }
 #pragma unroll
       for (int u = 0; u < 4; u++) {
         const int64_t e = e0 + u * nt;
@@ -659,6 +687,20 @@ void run_qr_blocked(Ctx& c, const std::vector<QrJob>& all, int nc, int* flag, co
 
 // QR of every job (one CTA each), then Q^T = I - V W1T on the DMMA GEMM, rows < nc to qlo and
 // rows >= nc to qhi.  Matrices beyond shared memory (or MLK_QR_BLOCKED=1) take the blocked path.
+// A = [R_L; R_R] for the stacked jobs, for the paths that factor A in global memory
+void stack_jobs(Ctx& c, std::vector<QrJob>& jobs, int nc) {
+  std::vector<StackJob> sj;
+  for (auto& j : jobs)
+    if (j.RL) sj.push_back({j.RL, j.RR, j.A});
+  if (sj.empty()) return;
+  DevBuf<StackJob> sjd(sj.size(), c.stream);
+  sjd.upload(sj);
+  TimedLaunch tl(c, "basis_stack");
+  k_stack_r<<<(unsigned)sj.size(), 256, 0, c.stream>>>(sjd.p, nc);
+  check_launch("k_stack_r");
+  for (auto& j : jobs) j.RL = j.RR = nullptr;
+}
+
 void run_qr(Ctx& c, std::vector<QrJob>& jobs, int nc, int* flag, const char* name) {
   if (jobs.empty()) return;
   {
@@ -666,6 +708,7 @@ void run_qr(Ctx& c, std::vector<QrJob>& jobs, int nc, int* flag, const char* nam
     for (auto& j : jobs) mm = std::max(mm, j.m);
     const char* eb = std::getenv("MLK_QR_BLOCKED");
     if (qr_smem(mm, nc, true, false) > (size_t)kQrSmemLimit || (eb && eb[0] == '1')) {
+      stack_jobs(c, jobs, nc);
       run_qr_blocked(c, jobs, nc, flag, name);
       return;
     }
@@ -697,6 +740,8 @@ void run_qr(Ctx& c, std::vector<QrJob>& jobs, int nc, int* flag, const char* nam
       CUDA_CHECK(cudaFuncSetAttribute(k_qr_wy<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_a));
       k_qr_wy<true, false><<<(unsigned)jobs.size(), kQrThreads, s_a, c.stream>>>(dj.p, flag);
     } else {
+      stack_jobs(c, jobs, nc);
+      dj.upload(jobs);
       const size_t s0 = qr_smem(m_max, nc, false, false);
       CUDA_CHECK(cudaFuncSetAttribute(k_qr_wy<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s0));
       k_qr_wy<false, false><<<(unsigned)jobs.size(), kQrThreads, s0, c.stream>>>(dj.p, flag);
@@ -954,14 +999,9 @@ mlk_status mlk_build_basis_ex(mlk_ctx ctx, mlk_tree tree, int32_t index_set, int
         jb.qhi = jb.qlo + (size_t)M * 2 * M;
         jb.ldq = 2 * M;
         jb.stacked = 1;
+        jb.RL = sj.back().RL;
+        jb.RR = sj.back().RR;
         qj.push_back(jb);
-      }
-      DevBuf<StackJob> sjd(nc, st);
-      sjd.upload(sj);
-      {
-        TimedLaunch tl(c, "basis_stack");
-        k_stack_r<<<(unsigned)nc, 256, 0, st>>>(sjd.p, M);
-        check_launch("k_stack_r");
       }
       trace.mark("lvl_stack");
       run_qr(c, qj, M, B->merge_flag.p, "basis_merge_qr");
