@@ -604,3 +604,72 @@ def test_loglik_truncation_sizes_and_identity_pin():
         l, ld, q, nt = Ll.loglik(bsr, tr, B, zw, level)
         assert abs(ld) <= 1e-12 * nt and abs(q - zw[:nt] @ zw[:nt]) <= 1e-12 * q
         assert abs(l - (-0.5 * nt * np.log(2 * np.pi) - 0.5 * zw[:nt] @ zw[:nt])) <= 1e-12 * abs(l)
+
+
+# ----------------------------------------------------------------------------- sm_f (NEXT-3)
+def test_smolyak_level_function_pinned_to_table1():
+    """f of Table multivariate:table1: f(0) = 0, f(1) = 1, f(p) = ceil(log2 p) for
+    p >= 2 -- values written out by hand, so a floor/ceil or off-by-one slip fails; and
+    |SM(d = 2, w = 2)| = 13 counted by hand (f-classes {0}, {1, 2}, {3, 4}: 1 + 4 + 4 + 4)."""
+    expect = {0: 0, 1: 1, 2: 1, 3: 2, 4: 2, 5: 3, 6: 3, 7: 3, 8: 3, 9: 4, 15: 4, 16: 4, 17: 5, 32: 5, 33: 6}
+    for p, f in expect.items():
+        assert I.sm_f(p) == f, (p, I.sm_f(p), f)
+    assert len(I.sm_exponents(2, 2)) == 13
+    assert sorted(I.sm_exponents(2, 1)) == sorted([(0, 0), (1, 0), (0, 1), (2, 0), (0, 2)])
+
+
+# ----------------------------------------------------------------------------- plain-C tiles
+from oracle import fastcov as Fc  # noqa: E402
+
+
+@pytest.mark.parametrize("family", [cv.MATERN_12, cv.MATERN_32, cv.MATERN_52, cv.GAUSSIAN])
+def test_fastcov_tile_equals_numpy_cov(family):
+    """The C tile (oracle/csrc/cov_tile.c) is oracle.covariance.cov written out: same entries
+    (to the last bits of the k-sum order), nugget only where the global indices agree, ragged
+    shapes that are not multiples of its 16 x 512 loop blocking."""
+    rng = np.random.default_rng([1, 7])
+    Xa = rng.standard_normal((37, 11))
+    Xb = np.vstack([rng.standard_normal((1000, 11)), Xa[:5]])
+    ia = np.arange(37) + 1000
+    ib = np.concatenate([np.arange(1000), ia[:5]])
+    kern = dict(family=family, rho=1.7, sigma2=1.3, nugget=1e-3)
+    got = Fc.cov_c(Xa, Xb, ia, ib, kern)
+    ref = cv.cov(Xa, Xb, ia, ib, family, 1.7, 1.3, 1e-3)
+    assert np.max(np.abs(got - ref)) <= 4e-16 * 1.3
+    assert np.all(np.abs(got[np.arange(5), 1000 + np.arange(5)] - (1.3 + 1e-3)) <= 1e-15)
+
+
+def test_fastcov_block_streamed_brute_force_and_panels(monkeypatch):
+    """block_streamed = W_a C W_b^T: against oracle.assemble.block on every admitted block
+    (with one-row panels forced, so the panel sum is exercised), against explicit scalar
+    double sums with math.exp, and the identity pin (Gaussian rho = 1e-5: C = I, so the self
+    block is W_a W_a^T = I)."""
+    X, tr, B, pairs = small_setup(n=96, d=3, w=1, leaf=12, kind=T.RP, points="normal")
+    kern = dict(family=cv.MATERN_12, rho=0.9, sigma2=1.1)
+    monkeypatch.setattr(Fc, "_panel_rows", lambda nb, budget=0: 7)
+    for a, b in pairs:
+        ref = As.block(X, tr, B, kern, a, b)
+        got = Fc.block_streamed(X, tr, B, kern, a, b)
+        assert np.linalg.norm(got - ref) <= 1e-13 * np.linalg.norm(ref)
+    a, b = pairs[len(pairs) // 2]
+    blk = Fc.block_streamed(X, tr, B, kern, a, b)
+    ia = tr.perm[tr.begin[a]:tr.end[a]]
+    ib = tr.perm[tr.begin[b]:tr.end[b]]
+    s = 0.0
+    for x in range(len(ia)):
+        for y in range(len(ib)):
+            r = math.sqrt(sum((X[ia[x], m] - X[ib[y], m]) ** 2 for m in range(3)))
+            s += B.W[a][0, x] * 1.1 * math.exp(-r / 0.9) * B.W[b][0, y]
+    assert abs(s - blk[0, 0]) <= 1e-12 * max(1.0, abs(s))
+    eye = Fc.block_streamed(X, tr, B, dict(family=cv.GAUSSIAN, rho=1e-5), a, a)
+    assert np.max(np.abs(eye - np.eye(B.p(a)))) < 1e-14
+
+
+def test_fastcov_rows_equal_panel_matvec():
+    X, tr, B, pairs = small_setup(n=300, d=4, w=1, leaf=20, kind=T.RP, points="uniform")
+    kern = dict(family=cv.MATERN_52, rho=0.6, nugget=1e-4)
+    a = np.random.default_rng(2).standard_normal((2, 300))
+    rows = np.array([0, 5, 150, 299])
+    ref = Mv.cov_matvec(X, tr, kern, a, rows=rows)
+    got = Fc.cov_rows(X, tr, kern, a, rows)
+    assert np.max(np.abs(got - ref)) <= 1e-13 * np.max(np.abs(ref))
