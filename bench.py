@@ -28,6 +28,19 @@ PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "k5a_traffic_%s.json")  # per config, from ncu --set full
 
 
+K5A_SOURCES = ["tile.cu", "tile.cuh", "dmma.cuh", "fastmath.cuh", "common.cuh"]
+
+
+def k5a_source_sha():
+    """sha256 over K5a's sources: a committed ncu traffic figure is reported only for the code
+    it was measured on (tools/traffic_from_ncu.py stamps the same hash)."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in K5A_SOURCES:
+        h.update(open(os.path.join(ROOT, "paper_1701_00285_b200", "csrc", f), "rb").read())
+    return h.hexdigest()[:16]
+
+
 def fp64_peak():
     d = json.load(open(PEAK_FILE))
     return float(max(d["fp64_peak_tflops_dmma"], d["fp64_peak_tflops_dfma"]))
@@ -85,6 +98,48 @@ def dist_env():
     return ws, rank, local
 
 
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def self_launch(args, argv):
+    """--gpus N > 1 without a torchrun environment: re-launch this script as N ranks (one per
+    GPU) with torch.distributed.run on 127.0.0.1 and return its exit code.  Rank 0 prints the
+    JSON line.  --dry-run needs no GPU (used by tests/test_bench_launch.py)."""
+    import subprocess
+    if not args.dry_run:
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(json.dumps({"error": "--gpus %d but only %d CUDA devices are visible" % (args.gpus, have)}))
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=%d" % args.gpus,
+           "--master-addr=127.0.0.1", "--master-port=%d" % _free_port(), os.path.abspath(__file__)] + argv
+    return subprocess.call(cmd)
+
+
+def dry_run(args):
+    """Launch check without GPU work: every rank reports its environment over gloo."""
+    import torch
+    import torch.distributed as dist
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("gloo")
+        got = [None] * ws
+        dist.all_gather_object(got, {"rank": rank, "world_size": ws, "local_rank": local})
+        dist.destroy_process_group()
+    else:
+        got = [{"rank": rank, "world_size": ws, "local_rank": local}]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": ws, "gpus_flag": args.gpus, "ranks": got}))
+    return 0
+
+
 # --------------------------------------------------------------------------- reference arm
 METRIC = "C_W assembly covariance pairs/s (FP64 TFLOP/s and % of FP64 peak in 'fp64')"
 
@@ -99,9 +154,17 @@ def config_dict(name, ws):
 
 
 class OracleSampler:
-    """The oracle (as it stands) on bounded, seeded samples of a workload's admitted blocks.
-    Tree, basis and admission are built once (untimed); each sample times oracle blocks
-    W_a C(X_a, X_b) W_b^T in seeded random order until the time budget is spent."""
+    """The oracle (as it stands) on bounded, seeded, STRATIFIED samples of a workload's admitted
+    blocks.  Tree, basis and the admitted pair list are built once, untimed (the pair list of
+    cfg3-5 is the oracle's own, read from tests/golden/pairs_<cfg>.npz, written by
+    tools/make_golden_pairs.py from oracle/ only).  A sample walks the level pairs (depth a,
+    depth b) round-robin -- every level pair gets a block before any gets a second -- taking
+    seeded random blocks of at most CAP covariance entries, each computed as W_a C(X_a, X_b) W_b^T
+    by the oracle (oracle.fastcov: direct-difference C tile in plain C, NumPy contractions), until
+    the time budget is spent and at least MIN_BLOCKS blocks were done."""
+
+    CAP = 1 << 26
+    MIN_BLOCKS = 64
 
     def __init__(self, cfg_name):
         from oracle import admission as OA
@@ -114,44 +177,111 @@ class OracleSampler:
         self.X = inp["X"]
         self.tr = OT.build_tree(self.X, c["leaf"], c["tree"], inp["dirs"])
         self.B = OB.build_basis(self.X, self.tr, c["w"])
-        self.pairs = OA.admitted_pairs(self.X, self.tr, self.B, c["pairs"], c["tau"])
+        gp = os.path.join(ROOT, "tests", "golden", "pairs_%s.npz" % cfg_name)
+        if os.path.exists(gp):
+            self.pairs = [tuple(int(v) for v in p) for p in np.load(gp)["pairs"]]
+        else:
+            self.pairs = OA.admitted_pairs(self.X, self.tr, self.B, c["pairs"], c["tau"])
         self.kern = wl.kernel_dict(c)
+        tr = self.tr
+        size = lambda q: int(tr.end[q] - tr.begin[q])
+        self.strata = {}
+        for k, (a, b) in enumerate(self.pairs):
+            key = (int(tr.depth[a]), int(tr.depth[b]))
+            self.strata.setdefault(key, []).append(k)
+        self.eligible = {key: [k for k in ks if size(self.pairs[k][0]) * size(self.pairs[k][1]) <= self.CAP]
+                         for key, ks in self.strata.items()}
 
-    def sample(self, budget_s, seed_tag=0):
-        from oracle import assemble as OAs
+    def _order(self, seed_tag):
+        """Round-robin over the level pairs of seeded permutations of their eligible blocks."""
+        rng = np.random.default_rng([0, 3, seed_tag])
+        queues = [list(rng.permutation(ks)) for key, ks in sorted(self.eligible.items()) if ks]
+        out = []
+        while any(queues):
+            for q in queues:
+                if q:
+                    out.append(int(q.pop(0)))
+        return out
+
+    def sample(self, budget_s, seed_tag=0, min_blocks=None):
+        min_blocks = self.MIN_BLOCKS if min_blocks is None else min_blocks
+        from oracle import fastcov as F
 
         tr = self.tr
-        order = np.random.default_rng([0, 3, seed_tag]).permutation(len(self.pairs))
         ent = 0.0
         nb = 0
+        seen = set()
         t0 = time.perf_counter()
-        for k in order:
+        for k in self._order(seed_tag):
             a, b = self.pairs[k]
-            OAs.block(self.X, tr, self.B, self.kern, a, b)
+            F.block_streamed(self.X, tr, self.B, self.kern, a, b)
             ent += float(tr.end[a] - tr.begin[a]) * float(tr.end[b] - tr.begin[b])
             nb += 1
-            if time.perf_counter() - t0 >= budget_s:
+            seen.add((int(tr.depth[a]), int(tr.depth[b])))
+            if time.perf_counter() - t0 >= budget_s and nb >= min_blocks:
                 break
         dt = time.perf_counter() - t0
-        cores = len(os.sched_getaffinity(0))
+        cores = omp_threads()
         try:
             from threadpoolctl import threadpool_info
             blas = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
         except Exception:
             blas = None
-        desc = ("oracle blocks W_a C W_b^T (direct differences + NumPy matmul) for %d of %d admitted %s "
-                "blocks in seeded random order, %.1f s budget; tree/basis/admission built once, untimed; "
-                "BLAS threads %s" % (nb, len(self.pairs), self.name, budget_s, blas))
+        excluded = sorted(key for key, ks in self.eligible.items() if not ks)
+        desc = ("sampled: %d of %d admitted %s blocks, stratified over %d of %d level pairs (depth a, depth b) "
+                "round-robin, seeded; blocks of <= 2^26 covariance entries (level pairs with none: %s); oracle "
+                "W_a C W_b^T = oracle.fastcov (plain-C direct-difference tile, OpenMP %d threads) + NumPy "
+                "contractions (BLAS threads %s); %.1f s budget; tree/basis/pair list built once, untimed"
+                % (nb, len(self.pairs), self.name, len(seen), len(self.strata),
+                   [list(k) for k in excluded] or "none", cores, blas, budget_s))
         return ent / dt, desc, cores
+
+    def matvec_sample(self, rows=256):
+        """Oracle C_W v pieces: a = W^T v and y = W b in full, b = C a on `rows` seeded rows."""
+        from oracle import fastcov as F
+        from oracle import matvec as OM
+
+        tr, B = self.tr, self.B
+        v = wl.vectors(1, B.dim, seed=0)
+        t0 = time.perf_counter()
+        a = OM.apply_wt(tr, B, v)
+        t1 = time.perf_counter()
+        rr = np.sort(np.random.default_rng([0, 3]).choice(tr.n, rows, replace=False))
+        F.cov_rows(self.X, tr, self.kern, a, rr)
+        t2 = time.perf_counter()
+        OM.apply_w(tr, B, a)
+        t3 = time.perf_counter()
+        return {"kind": "oracle", "sample": "C a on %d seeded rows of %d (oracle.fastcov.cov_rows); W^T v and W b "
+                                            "in full (oracle.matvec)" % (rows, tr.n),
+                "apply_wt_s": t1 - t0, "apply_w_s": t3 - t2, "cov_rows_s": t2 - t1,
+                "cov_entries_per_s": rows * float(tr.n) / (t2 - t1)}
+
+
+def omp_threads():
+    """Threads the oracle's OpenMP tile uses (OMP_NUM_THREADS if set, else the affinity mask)."""
+    n = len(os.sched_getaffinity(0))
+    try:
+        return max(1, min(n, int(os.environ["OMP_NUM_THREADS"])))
+    except (KeyError, ValueError):
+        return n
 
 
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
+    if ws > 1:
+        # torchrun sets OMP_NUM_THREADS=1 per rank; rank 0 runs alone here, so give the oracle the
+        # host's cores (read when the oracle's C tile library is first loaded)
+        os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
+        try:
+            from threadpoolctl import threadpool_limits
+            threadpool_limits(len(os.sched_getaffinity(0)))
+        except Exception:
+            pass
     sampler = OracleSampler(args.config)
     for w in range(args.warmup):
-        sampler.sample(min(3.0, args.ref_budget), seed_tag=100 + w)
+        sampler.sample(min(3.0, args.ref_budget), seed_tag=100 + w, min_blocks=1)
     vals = []
     desc = cores = None
     for s in range(args.steps):
@@ -177,17 +307,30 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--config", default="cfg4",
+                    help="BASELINE workload; cfg4 (n = 262144, d = 50) is the largest that fits one B200")
     ap.add_argument("--impl", default="ours")
     ap.add_argument("--ref-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--pcg-tol", type=float, default=1e-8, help="PCG solve reported after the bench (0: skip)")
+    ap.add_argument("--pcg-tol", type=float, default=None,
+                    help="PCG solve reported after the bench (0: skip; default 1e-8 up to cfg3 size, skipped above)")
+    ap.add_argument("--dry-run", action="store_true", help="launch check only (no GPU work)")
     ap.add_argument("--no-matvec-report", dest="matvec_report", action="store_false",
                     help="skip the C_W v timings reported after the bench")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args, sys.argv[1:])
+    ws_env = dist_env()[0]
+    if ws_env != args.gpus and not (args.gpus == 1 and ws_env > 1):
+        print(json.dumps({"error": "--gpus %d but WORLD_SIZE=%d" % (args.gpus, ws_env)}))
+        return 2
+    if args.dry_run:
+        return dry_run(args)
     if args.impl == "reference":
         return run_reference(args)
+    if args.pcg_tol is None:
+        args.pcg_tol = 1e-8 if wl.CONFIGS[args.config]["n"] <= 131072 else 0.0
 
     import torch
     import torch.distributed as dist
@@ -197,10 +340,17 @@ def main():
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    nccl_id = None
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        # torch.distributed (gloo, host side) carries only the plumbing: the NCCL unique id, the
+        # barriers and the max-over-ranks timings.  The data-path collectives (the all-gather of
+        # the BSR pieces, the allreduce of C_W v) run inside libmlk on its own NCCL communicator.
+        dist.init_process_group("gloo")
+        idl = [mlk.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(idl, src=0)
+        nccl_id = idl[0]
     stream = torch.cuda.Stream(dev)
-    ctx = mlk.Ctx(local, ws, rank, stream.cuda_stream)
+    ctx = mlk.Ctx(local, ws, rank, stream.cuda_stream, nccl_id=nccl_id)
     inp = wl.make(args.config)
     c = inp["cfg"]
     kern = wl.kernel_dict(c)
@@ -224,9 +374,8 @@ def main():
         tr = timed("build_tree", mlk.build_tree, ctx, X, c["leaf"], c["tree"], D)
         B = timed("build_basis", mlk.build_basis, ctx, tr, c["w"], c.get("index_set", 0),
                   mlk.BASIS_KEEP_DEFICIENT if c.get("index_set", 0) else 0)
+        # nranks > 1: the library all-gathers the pieces (MLK_GATHER_DEVICE over NCCL)
         cw = timed("assemble_cw", mlk.assemble_cw, ctx, tr, B, kern, spars)
-        if ws > 1:
-            timed("gather_cw", mlk.gather_cw, ctx, cw)
         if v_host is None:
             if "v" not in vec_cache:
                 vec_cache["v"] = torch.from_numpy(wl.vectors(nvec, B.dim, seed=0)).to(dev)
@@ -250,7 +399,7 @@ def main():
     torch.cuda.synchronize()
     # one untimed pass for the structure numbers
     tr, B, cw = step(X_d, dirs_d)
-    entries, flops = cw.entries, cw.flops
+    entries, flops, own_flops = cw.entries, cw.flops, cw.own_flops
     sf = cw.stage_flops()
     nnz, dim = cw.nnz, B.dim
     del tr, B, cw
@@ -274,10 +423,7 @@ def main():
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        step(X_d, dirs_d)
-        # N > 1: the all-gather / allreduce run on NCCL's stream behind torch's current stream;
-        # the end event must follow them
-        stream.wait_stream(torch.cuda.current_stream(dev))
+        step(X_d, dirs_d)   # the library's collectives run on `stream` too
         e1.record(stream)
         e1.synchronize()
         step_ms.append(e0.elapsed_time(e1))
@@ -289,7 +435,7 @@ def main():
     ctx.set_timing(False)
     total_ms = float(np.sum(step_ms))
     if ws > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([total_ms], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
@@ -316,7 +462,7 @@ def main():
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
     e2e_total = float(np.sum(e2e_ms)) if e2e_ms else float("nan")
     if ws > 1 and e2e_ms:
-        t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
+        t = torch.tensor([e2e_total], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_total = float(t.item())
     e2e_val = entries * args.e2e_steps / (e2e_total * 1e-3) if e2e_ms else None
@@ -390,11 +536,18 @@ def main():
         peak = fp64_peak()
         k5 = stats.get("assemble_tile_contract", {"ms": float("nan"), "launches": 1})
         k5_ms_per_step = k5["ms"] / args.steps
-        k5_flops = (sf["gram"] + sf["contract1"]) / ws
+        # this rank's share of the K5a flops (its LPT units; the whole job when ws == 1)
+        k5_flops = (sf["gram"] + sf["contract1"]) * (own_flops / flops if flops > 0 else 1.0)
         achieved = k5_flops / (k5_ms_per_step * 1e-3) / 1e12
-        traffic = None
+        traffic, traffic_src = None, "no ncu capture for this config"
         if os.path.exists(TRAFFIC_FILE % args.config):
-            traffic = json.load(open(TRAFFIC_FILE % args.config)).get("bytes_per_launch")
+            tj = json.load(open(TRAFFIC_FILE % args.config))
+            if tj.get("k5a_source_sha") == k5a_source_sha():
+                # dram bytes of the launch(es) of one step, per launch like `achieved`
+                traffic = tj.get("bytes_per_launch")
+                traffic_src = "ncu --set full, %s (K5a sources sha %s)" % (tj.get("source"), tj["k5a_source_sha"])
+            else:
+                traffic_src = "stale: %s was captured on other K5a sources" % os.path.basename(TRAFFIC_FILE % args.config)
         asm_ms = sum(stats.get(k, {"ms": 0.0})["ms"] for k in
                      ("search", "assemble_tile_contract", "assemble_wa_gemm")) / args.steps
         cpu = None
@@ -404,8 +557,10 @@ def main():
                 # rank-deficient by design (reading R24), so it has no oracle baseline
                 cpu = {"unavailable": "oracle basis covers total-degree sets without reading R24"}
             else:
-                v, desc, cores = OracleSampler(args.config).sample(args.ref_budget)
-                cpu = {"value": v, "unit": "covariance pairs/s", "cores": cores, "kind": "oracle", "sample": desc}
+                osamp = OracleSampler(args.config)
+                v, desc, cores = osamp.sample(args.ref_budget)
+                cpu = {"value": v, "unit": "covariance pairs/s", "cores": cores, "kind": "oracle", "sample": desc,
+                       "matvec": osamp.matvec_sample()}
         line = {
             "metric": METRIC,
             "value": value, "unit": "covariance pairs/s", "n_gpus": ws, "steps": args.steps,
@@ -420,6 +575,8 @@ def main():
                                         "profiles/fp64_peak_r01.json; MEASURED_PEAKS.json holds bf16/HBM only)",
                          "pipe": "FP64 DMMA.8x8x4 (shares the FP64 pipe with DFMA, DESIGN.md section 6)", "achieved": achieved,
                          "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                         "traffic_source": traffic_src,
+                         "launches_per_step": k5["launches"] / args.steps,
                          "algorithmic_flops_per_step": k5_flops, "ms_per_step": k5_ms_per_step},
             "kernels_ms_per_step": {k: v["ms"] / args.steps for k, v in sorted(stats.items())},
             "api_wall_ms_per_step": api_timed,

@@ -20,12 +20,16 @@
  *    Export calls copy into caller memory; passing NULL for an output skips it.
  *  - A context is single-threaded; calls are stream-ordered on the context's stream and
  *    return after the work they enqueue has completed unless stated otherwise.
- *  - Multi-GPU (nranks > 1): one process per GPU.  Points and basis are replicated; the
- *    assembly and the matvec split their work across ranks and return this rank's part.
- *    The collectives (an all-gather of BSR values, an allreduce of C_W v) are issued by the
- *    caller's NCCL process group between mlk_cw_pack / mlk_cw_unpack, and after
- *    mlk_cw_matvec (see those calls).  Every rank must make the same calls with the same
- *    arguments.
+ *  - Multi-GPU (nranks > 1, S§8(e)): one process per GPU.  Points and basis are replicated
+ *    (every rank builds them identically); the assembly's work units and the C_W v rows are
+ *    split across ranks.  The only collectives are an all-gather of the BSR pieces after the
+ *    assembly and a sum-allreduce of C_W v.  A context created WITH an NCCL unique id
+ *    (mlk_ctx_create) issues them itself on its own communicator, over NVLink/NVSwitch:
+ *    mlk_assemble_cw(gather = MLK_GATHER_DEVICE / _HOST) returns the complete matrix on every
+ *    rank and mlk_cw_matvec returns the summed y.  A context created WITHOUT one leaves them
+ *    to the caller: mlk_cw_pack / caller all-gather / mlk_cw_unpack, and a caller allreduce of
+ *    mlk_cw_matvec's partial y.  Every rank must make the same calls with the same arguments
+ *    (the collective calls are then collective).
  *  - Point-space vectors are in TREE ORDER: entry k belongs to original observation perm[k]
  *    (mlk_tree_export).  C_W-space vectors are in C_W row order (levels t..0, heap order
  *    within a level, reading R11).
@@ -47,7 +51,8 @@ typedef enum {
   MLK_ERR_RANK_DEFICIENT = 3,   /* a moment matrix has rank < M (reading R9)                  */
   MLK_ERR_OUT_OF_MEMORY = 4,    /* a device allocation failed                                 */
   MLK_ERR_CUDA = 5,             /* any other CUDA runtime error                               */
-  MLK_ERR_UNSUPPORTED = 6       /* valid request this build does not implement                */
+  MLK_ERR_UNSUPPORTED = 6,      /* valid request this build does not implement                */
+  MLK_ERR_NCCL = 7              /* libnccl.so.2 missing or an NCCL call failed                */
 } mlk_status;
 
 /* Text for the last non-OK status returned on this thread ("" if none). */
@@ -63,10 +68,20 @@ typedef struct mlk_basis_s* mlk_basis;
 typedef struct mlk_cw_s* mlk_cw;
 
 /* ------------------------------------------------------------------------------------------
- * Context.  device: CUDA ordinal.  nranks >= 1, 0 <= rank < nranks.  cuda_stream: a
- * cudaStream_t the library launches on (NULL: the library creates and owns one).
+ * Context.  device: CUDA ordinal.  nranks >= 1, 0 <= rank < nranks.
+ *  nccl_unique_id  NULL, or the 128-byte ncclUniqueId (mlk_nccl_unique_id on one rank,
+ *                  distributed by the caller, e.g. a torch.distributed broadcast): the context
+ *                  then creates and owns an NCCL communicator of nranks ranks
+ *                  (ncclCommInitRank -- collective over the ranks) and issues the path's
+ *                  collectives itself.  NCCL is loaded at run time (libnccl.so.2);
+ *                  MLK_ERR_NCCL if it is missing or the initialisation fails.
+ *  cuda_stream     a cudaStream_t the library launches on (NULL: the library creates and owns
+ *                  one).  Collectives run on the same stream.
  */
-mlk_status mlk_ctx_create(int device, int nranks, int rank, void* cuda_stream, mlk_ctx* out);
+mlk_status mlk_ctx_create(int device, int nranks, int rank, const void* nccl_unique_id, void* cuda_stream,
+                          mlk_ctx* out);
+/* A fresh ncclUniqueId (128 bytes into id) for mlk_ctx_create; host only, call on one rank. */
+mlk_status mlk_nccl_unique_id(void* id);
 void mlk_ctx_destroy(mlk_ctx ctx); /* NULL-safe */
 /* The cudaStream_t the context launches on. */
 void* mlk_ctx_stream(mlk_ctx ctx);
@@ -164,8 +179,9 @@ mlk_status mlk_apply_w(mlk_ctx ctx, mlk_basis basis, const double* b, double* y,
  * or the Gaussian exp(-r^2 / rho^2) (R17).  rho > 0, sigma2 > 0, nugget >= 0.
  */
 /* MLK_MATERN_NU (NEXT-3): the definition of P:970 for any nu > 0 (the paper's workloads use
- * nu = 1.25, 3/4), with K_nu evaluated in the kernel (Temme's series below z = 2, Steed's
- * continued fraction above, upward recurrence in nu); nu is read only for this family. */
+ * nu = 1.25, 3/4), with K_nu evaluated in the kernel from its integral representation
+ * int_0^inf exp(-z cosh t) cosh(nu t) dt (trapezoidal rule) or, for z < 2 and non-integer nu,
+ * the I_-nu - I_nu power series; 0 < nu <= 50; nu is read only for this family. */
 typedef enum { MLK_MATERN_12 = 0, MLK_MATERN_32 = 1, MLK_MATERN_52 = 2, MLK_GAUSSIAN = 3, MLK_MATERN_NU = 4 } mlk_family;
 typedef struct {
   int32_t family;
@@ -187,6 +203,19 @@ typedef struct {
  * workloads at the FP64 floor (e.g. BASELINE cfg1). */
 typedef enum { MLK_PREC_FP64 = 0, MLK_PREC_DD = 1 } mlk_precision;
 
+/* Gather of the per-rank pieces after the assembly (nranks > 1; nothing to do for nranks == 1):
+ *  MLK_GATHER_NONE    each rank keeps its shard of pieces (mlk_cw_pack / mlk_cw_unpack, or the
+ *                     sharded mlk_cw_matvec BSR, which needs no gather at all).  This is the
+ *                     mode for matrices no single GPU or host holds (BASELINE cfg5: 184 GB of
+ *                     values).
+ *  MLK_GATHER_DEVICE  the library all-gathers the pieces over its NCCL communicator, in block
+ *                     groups sized to a staging buffer (no rank ever holds the nranks x shard
+ *                     receive buffer), and reduces them in chunk order into device values: every
+ *                     rank returns the complete C~_W, bit-identical to nranks == 1.
+ *  MLK_GATHER_HOST    the same into mapped pinned host memory (MLK_VALUES_HOST placement).
+ * The GATHER modes need a context created with an NCCL unique id. */
+typedef enum { MLK_GATHER_NONE = 0, MLK_GATHER_DEVICE = 1, MLK_GATHER_HOST = 2 } mlk_gather;
+
 /* ------------------------------------------------------------------------------------------
  * mlk_assemble_cw -- the sparse multi-level covariance matrix C~_W (Algorithm 6; blocks
  * W_i C W_j^T of P:1636-1653) in variable-block BSR form:
@@ -198,23 +227,24 @@ typedef enum { MLK_PREC_FP64 = 0, MLK_PREC_DD = 1 } mlk_precision;
  * blocks sharing b (for ancestor pairs R = X_b itself), in work units of <= 4096 rows; a
  * block is W_a V_b[X_a], summed over the 4096-row chunks ("pieces") of X_a in chunk order.
  * With nranks > 1 the units are LPT-partitioned over ranks, each rank writes the pieces of
- * its units into its shard; mlk_cw_pack/unpack + the caller's all-gather complete it.
+ * its units into its shard, and `gather` (mlk_gather) decides how the shards are combined.
  * Results are bit-identical for every nranks.
  */
 mlk_status mlk_assemble_cw(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const mlk_kernel* kernel,
-                           const mlk_sparsity* sparsity, int32_t precision, mlk_cw* out);
+                           const mlk_sparsity* sparsity, int32_t precision, int32_t gather, mlk_cw* out);
 /* mlk_assemble_cw_ex -- as mlk_assemble_cw, with the placement of the nnz BSR values:
  *  MLK_VALUES_DEVICE: device memory (what mlk_assemble_cw does);
  *  MLK_VALUES_HOST:   mapped pinned host memory allocated by the library (cudaHostAlloc), for
  *                     matrices beyond HBM (BASELINE cfg5: 184 GB of values next to 106 GB of
  *                     W).  The kernels store the finished blocks straight over the host link;
- *                     the piece shards and all scratch stay on the device.  nranks == 1 only
- *                     (MLK_ERR_UNSUPPORTED-class argument error otherwise).  mlk_cw_values_device
- *                     then returns the host pointer; mlk_cw_matvec BSR reads the values over
- *                     the host link. */
+ *                     the piece shards and all scratch stay on the device (nranks > 1: the gather
+ *                     reduces into it).  mlk_cw_values_device then returns the host pointer;
+ *                     mlk_cw_matvec BSR reads the values over the host link.
+ *  gather: MLK_GATHER_NONE or MLK_GATHER_DEVICE (= "gather into the placement"). */
 typedef enum { MLK_VALUES_DEVICE = 0, MLK_VALUES_HOST = 1 } mlk_values_placement;
 mlk_status mlk_assemble_cw_ex(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const mlk_kernel* kernel,
-                              const mlk_sparsity* sparsity, int32_t precision, int32_t placement, mlk_cw* out);
+                              const mlk_sparsity* sparsity, int32_t precision, int32_t placement, int32_t gather,
+                              mlk_cw* out);
 void mlk_cw_free(mlk_cw cw); /* NULL-safe */
 /* n_cells; n_blocks; nnz values; entries = sum over blocks |row cell| |col cell| (the
  * covariance pairs C~_W is made of); flops = FP64 flops the kernels execute (Gram 2d per
@@ -247,7 +277,7 @@ mlk_status mlk_cw_owner(mlk_cw cw, int32_t* owner);
  * (block, chunk) order, to `dst` (device, >= max_shard_len doubles, tail zero-filled).  After
  * the caller's all-gather of the packed shards into `gathered` (device, nranks x
  * max_shard_len, rank-major), mlk_cw_unpack sums every block's pieces in chunk order into
- * the BSR values (no-op for nranks == 1). */
+ * the BSR values (no-op for nranks == 1), group by group exactly as MLK_GATHER_DEVICE does. */
 mlk_status mlk_cw_shard_len(mlk_cw cw, int64_t* shard_len, int64_t* max_shard_len);
 mlk_status mlk_cw_pack(mlk_ctx ctx, mlk_cw cw, double* dst);
 mlk_status mlk_cw_unpack(mlk_ctx ctx, mlk_cw cw, const double* gathered);
@@ -275,8 +305,14 @@ mlk_status mlk_cov_matvec(mlk_ctx ctx, mlk_tree tree, const mlk_kernel* kernel, 
 
 /* mlk_cw_matvec -- y = C_W v.  EXACT: y = W (C (W^T v)) by the three steps of
  * P:2146-2170 (cw may be NULL).  BSR: y = C~_W v on the assembled blocks (mirrored lower
- * triangle).  v, y: nvec x dim (host or device).  With nranks > 1 y is this rank's partial
- * sum (its row panel of C, or its blocks); the caller sum-allreduces y over the ranks. */
+ * triangle).  v, y: nvec x dim (host or device).
+ * nranks > 1: each rank applies its share -- EXACT its row panel of C; BSR the blocks it owns
+ * when cw is complete (gathered / unpacked), otherwise the pieces of its own shard (S§8(e): "each
+ * rank applies its own blocks and their mirrors", no gather needed).  With a library
+ * communicator (mlk_ctx_create with an NCCL id) y is then sum-allreduced and every rank returns
+ * C_W v; without one y is this rank's partial sum and the caller allreduces it.  The EXACT
+ * row split is a function of (n, nvec, nranks) and the device's total memory only, identical on
+ * every rank. */
 typedef enum { MLK_MATVEC_EXACT = 0, MLK_MATVEC_BSR = 1 } mlk_matvec_mode;
 mlk_status mlk_cw_matvec(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const mlk_kernel* kernel,
                          mlk_cw cw, int32_t mode, const double* v, double* y, int32_t nvec);
@@ -327,6 +363,18 @@ mlk_status mlk_partition_lpt(const double* cost, int64_t n, int32_t nranks, int3
  * buffer holds rank r's shard at r * max(shard_len). */
 mlk_status mlk_shard_plan(const int64_t* val_off, const int32_t* owner, int64_t n, int32_t nranks,
                           int64_t* shard_off, int64_t* shard_len);
+
+/* mlk_gather_plan: the block groups of the chunked all-gather (MLK_GATHER_DEVICE / _HOST and
+ * mlk_cw_unpack).  Inputs: n_blocks, piece_ptr[n_blocks+1], piece_off[n_pieces] (offset in the
+ * owner's shard), piece_owner[n_pieces], block_len[n_blocks] (doubles per block), nranks, and the
+ * receive budget (doubles).  Group g covers blocks group_ptr[g] .. group_ptr[g+1]-1; rank r
+ * contributes its shard slice [group_lo[g*nranks + r], + group_count[g]) (pieces of the group are
+ * contiguous in every shard), so a group is one equal-count all-gather of nranks x
+ * group_count[g] <= budget doubles (a single larger block is a group of its own).  Call with
+ * the three group arrays NULL to get *n_groups; group_ptr needs n_groups + 1 entries. */
+mlk_status mlk_gather_plan(int64_t n_blocks, const int64_t* piece_ptr, const int64_t* piece_off,
+                           const int32_t* piece_owner, const int64_t* block_len, int32_t nranks, int64_t budget,
+                           int64_t* n_groups, int64_t* group_ptr, int64_t* group_lo, int64_t* group_count);
 
 #ifdef __cplusplus
 }

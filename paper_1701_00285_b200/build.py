@@ -14,7 +14,7 @@ LIB = os.path.join(HERE, "libmlk.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
-SOURCES = ["ctx.cu", "tree.cu", "gemm.cu", "basis.cu", "tile.cu", "assemble.cu", "dd.cu", "matvec.cu", "pcg.cu",
+SOURCES = ["ctx.cu", "comm.cu", "tree.cu", "gemm.cu", "basis.cu", "tile.cu", "assemble.cu", "dd.cu", "matvec.cu", "pcg.cu",
            "loglik.cu"]
 
 
@@ -44,7 +44,7 @@ def build(verbose=False):
                 print(log, file=sys.stderr)
     if not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
         cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB] + objs + \
-              ["-lcudart"]
+              ["-lcudart", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("link failed:\n%s\n%s" % (r.stdout, r.stderr))

@@ -20,6 +20,14 @@
     return MLK_ERR_CUDA;                                                   \
   }                                                                        \
   return MLK_OK;
+// the status of a nested ABI call, after the caller's own checks
+#define MLK_API_END_CALL(expr)                                             \
+  }                                                                        \
+  catch (const ::mlk::Error& e) {                                          \
+    ::mlk::set_last_error(e.what());                                       \
+    return e.status;                                                       \
+  }                                                                        \
+  return (expr);
 
 struct mlk_basis_s;
 struct mlk_tree_s;
@@ -39,6 +47,11 @@ void apply_wt_dev(Ctx& c, const mlk_tree_s* tree, const mlk_basis_s* B, const do
 void cov_matvec_dev(Ctx& c, const mlk_tree_s* tree, const mlk_kernel& k, const double* a, double* b, int nvec);
 void apply_w_dev(Ctx& c, const mlk_tree_s* tree, const mlk_basis_s* B, const double* b, double* y, int nvec);
 void check_kernel(const mlk_kernel* k);
+
+// NCCL collectives on the context's communicator (comm.cu)
+void* comm_create(int nranks, int rank, const void* unique_id);
+void comm_destroy(void* comm);
+void comm_allreduce_sum(Ctx& c, double* x, int64_t count);
 
 // padded coordinate count for the DMMA k = 4 Gram steps
 inline int pad4(int d) { return (d + 3) / 4 * 4; }
@@ -113,6 +126,11 @@ struct mlk_cw_s {
 };
 
 namespace mlk {
+// all-gather of the piece shards into the values (nranks > 1, library communicator; comm.cu)
+void gather_values(Ctx& c, mlk_cw_s* cw, const double* full);
+void gather_plan(int64_t nb, const int64_t* piece_ptr, const int64_t* piece_off, const int32_t* piece_owner,
+                 const int64_t* block_len, int nranks, int64_t budget, std::vector<int64_t>& group_ptr,
+                 std::vector<int64_t>& group_lo, std::vector<int64_t>& group_count);
 // Row-major NN product C = A B (m x k times k x n); if trans_c, C^T is stored (C[j][i]).
 // If accumulate, the product is added to C (fixed order: exactly one job per C tile).
 struct GemmDesc {

@@ -280,16 +280,23 @@ using namespace mlk;
 extern "C" {
 
 mlk_status mlk_assemble_cw(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const mlk_kernel* kernel,
-                           const mlk_sparsity* sparsity, int32_t precision, mlk_cw* out) {
-  return mlk_assemble_cw_ex(ctx, tree, basis, kernel, sparsity, precision, MLK_VALUES_DEVICE, out);
+                           const mlk_sparsity* sparsity, int32_t precision, int32_t gather, mlk_cw* out) {
+  MLK_API_BEGIN
+  MLK_REQUIRE(gather >= MLK_GATHER_NONE && gather <= MLK_GATHER_HOST, "unknown gather mode");
+  MLK_API_END_CALL(mlk_assemble_cw_ex(ctx, tree, basis, kernel, sparsity, precision,
+                                      gather == MLK_GATHER_HOST ? MLK_VALUES_HOST : MLK_VALUES_DEVICE,
+                                      gather == MLK_GATHER_NONE ? MLK_GATHER_NONE : MLK_GATHER_DEVICE, out));
 }
 
 mlk_status mlk_assemble_cw_ex(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const mlk_kernel* kernel,
-                              const mlk_sparsity* sparsity, int32_t precision, int32_t placement, mlk_cw* out) {
+                              const mlk_sparsity* sparsity, int32_t precision, int32_t placement, int32_t gather,
+                              mlk_cw* out) {
   MLK_API_BEGIN
   MLK_REQUIRE(ctx && tree && basis && kernel && sparsity && out, "NULL argument");
   MLK_REQUIRE(placement == MLK_VALUES_DEVICE || placement == MLK_VALUES_HOST, "unknown value placement");
-  MLK_REQUIRE(placement == MLK_VALUES_DEVICE || ctx->c.nranks == 1, "MLK_VALUES_HOST needs nranks == 1");
+  MLK_REQUIRE(gather == MLK_GATHER_NONE || gather == MLK_GATHER_DEVICE, "mlk_assemble_cw_ex: gather is 0 or 1");
+  MLK_REQUIRE(gather == MLK_GATHER_NONE || ctx->c.nranks == 1 || ctx->c.comm,
+              "gather needs a context created with an NCCL unique id");
   *out = nullptr;
   MLK_REQUIRE(basis->tree == tree, "basis was built for another tree");
   MLK_REQUIRE(kernel->family >= MLK_MATERN_12 && kernel->family <= MLK_MATERN_NU, "unknown covariance family");
@@ -623,6 +630,10 @@ mlk_status mlk_assemble_cw_ex(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const
   }
   CUDA_CHECK(cudaStreamSynchronize(st));
   trace.mark("structure");
+  if (gather != MLK_GATHER_NONE && c.nranks > 1) {
+    gather_values(c, cw.get(), nullptr);
+    trace.mark("gather");
+  }
   *out = cw.release();
   MLK_API_END
 }
@@ -737,11 +748,7 @@ mlk_status mlk_cw_unpack(mlk_ctx ctx, mlk_cw cw, const double* gathered) {
   Ctx& c = ctx->c;
   CUDA_CHECK(cudaSetDevice(c.device));
   MLK_REQUIRE(is_device_ptr(gathered), "gathered must be device memory");
-  if (cw->nranks > 1) {
-    if (!cw->hvals && !cw->values.p) cw->values.alloc(std::max<int64_t>(cw->nnz, 1), c.stream);
-    TimedLaunch tl(c, "cw_unpack");
-    reduce_pieces(c, cw, gathered);
-  }
+  if (cw->nranks > 1) gather_values(c, cw, gathered);
   CUDA_CHECK(cudaStreamSynchronize(c.stream));
   cw->complete = true;
   MLK_API_END

@@ -67,6 +67,7 @@ struct Ctx {
   cudaStream_t copy_stream = nullptr;  // mlk_cw_export_async (created on first use)
   cudaStream_t aux_stream = nullptr;   // asynchronous basis merge levels (created on first use)
   cudaEvent_t copy_ready = nullptr;
+  void* comm = nullptr;                // ncclComm_t of mlk_ctx_create with a unique id (comm.cu)
   int64_t scratch_budget_bytes();
 
   cudaEvent_t get_event();
@@ -84,11 +85,20 @@ struct TimedLaunch {
       CUDA_CHECK(cudaEventRecord(a, c.stream));
     }
   }
-  ~TimedLaunch() noexcept(false) {
-    if (c.timing) {
-      cudaEvent_t b = c.get_event();
-      CUDA_CHECK(cudaEventRecord(b, c.stream));
+  // never throws: it also runs while an exception unwinds the launch sequence; a failed
+  // record drops the sample (the error itself surfaces at the next check_launch / CUDA_CHECK)
+  ~TimedLaunch() {
+    if (!c.timing || a == nullptr) return;
+    cudaEvent_t b = nullptr;
+    if (cudaEventCreate(&b) != cudaSuccess || cudaEventRecord(b, c.stream) != cudaSuccess) {
+      if (b) cudaEventDestroy(b);
+      c.event_pool.push_back(a);
+      return;
+    }
+    try {
       c.pending.push_back({name, a, b});
+    } catch (...) {
+      cudaEventDestroy(b);
     }
   }
 };
@@ -233,6 +243,7 @@ struct HostTrace {
 };
 
 int num_sms(int device);
+int64_t device_total_bytes(int device);  // cudaDeviceProp::totalGlobalMem, cached
 
 }  // namespace mlk
 

@@ -34,6 +34,15 @@ int num_sms(int device) {
   return v;
 }
 
+int64_t device_total_bytes(int device) {
+  static int64_t cached[64] = {0};
+  if (device >= 0 && device < 64 && cached[device]) return cached[device];
+  cudaDeviceProp prop;
+  CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
+  if (device >= 0 && device < 64) cached[device] = (int64_t)prop.totalGlobalMem;
+  return (int64_t)prop.totalGlobalMem;
+}
+
 namespace {
 struct PinnedRing {
   static constexpr size_t kCap = (size_t)64 << 20;
@@ -183,7 +192,8 @@ const char* mlk_version(void) { return "mlk 0.1 (sm_100a, FP64 DMMA)"; }
 
 int64_t mlk_launch_count(void) { return g_launches.load(); }
 
-mlk_status mlk_ctx_create(int device, int nranks, int rank, void* cuda_stream, mlk_ctx* out) {
+mlk_status mlk_ctx_create(int device, int nranks, int rank, const void* nccl_unique_id, void* cuda_stream,
+                          mlk_ctx* out) {
   MLK_API_BEGIN
   MLK_REQUIRE(out != nullptr, "out is NULL");
   *out = nullptr;
@@ -214,6 +224,15 @@ mlk_status mlk_ctx_create(int device, int nranks, int rank, void* cuda_stream, m
     }
     h->c.own_stream = true;
   }
+  if (nccl_unique_id) {
+    try {
+      h->c.comm = comm_create(nranks, rank, nccl_unique_id);
+    } catch (...) {
+      if (h->c.own_stream) cudaStreamDestroy(h->c.stream);
+      delete h;
+      throw;
+    }
+  }
   *out = h;
   MLK_API_END
 }
@@ -235,6 +254,12 @@ void mlk_ctx_destroy(mlk_ctx ctx) {
     cudaStreamSynchronize(ctx->c.copy_stream);
     cudaStreamDestroy(ctx->c.copy_stream);
     cudaEventDestroy(ctx->c.copy_ready);
+  }
+  if (ctx->c.comm) {
+    try {
+      comm_destroy(ctx->c.comm);
+    } catch (...) {
+    }
   }
   if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
   delete ctx;

@@ -61,39 +61,42 @@ __global__ void k_apply_w(const CellJob* __restrict__ jobs, const double* __rest
   }
 }
 
-// BSR: y_r = sum_{own blocks (r,c)} B v_c + sum_{own blocks (c,r), c != r} B^T v_c, as two
-// passes over the stored blocks that each read a block once with coalesced loads, then a
-// fixed-order reduction per cell (deterministic, no atomics).  HBM-bound: 2 x 8 nnz bytes.
-//  row pass  (one CTA per block, grid.y = vector group): warp per block row i, lanes over the
-//            columns, warp reduction -> rp[k][iv][i] (p_r values)
-//  col pass  (one CTA per block and 256-column panel): thread per block column j, loop over
-//            the rows -> cp[k][iv][j] (p_c values, off-diagonal blocks only)
+// BSR: y_r = sum_{items (r,c)} B v_c + sum_{items (c,r), c != r} B^T v_c over the stored
+// items this rank applies -- every block (nranks == 1), the blocks it owns (complete values,
+// nranks > 1), or the row-chunk pieces it computed, read straight from its shard (nranks > 1
+// before any gather: S§8(e)'s sharded product, the ranks' partial y sum to C~_W v).  Two passes
+// read each item once with coalesced loads, then a fixed-order reduction per cell
+// (deterministic, no atomics).  HBM-bound: 2 x 8 x (item values) bytes.
+//  row pass  (one CTA per item, grid.y = vector group): warp per row i, lanes over the columns,
+//            warp reduction -> rp[part_off[k]][iv][i] (p_r values)
+//  col pass  (one CTA per item and 256-column panel): thread per column j, loop over the rows
+//            -> cp[..][iv][j] (p_c values, off-diagonal items only)
 constexpr int kBsrVG = 4;  // vectors per pass
 
-__global__ void k_bsr_rows(const int32_t* __restrict__ brow, const int32_t* __restrict__ bcol,
-                           const int64_t* __restrict__ val_off, const int32_t* __restrict__ owner, int rank,
-                           const int64_t* __restrict__ row_off, const int64_t* __restrict__ part_off,
-                           const double* __restrict__ vals, const double* __restrict__ v, int64_t dim, int nvec,
-                           double* __restrict__ rp) {
+struct BsrItem {
+  int32_t r, c;  // cell positions (C_W order)
+  int64_t off;   // values at base + off, p_r x p_c row-major
+};
+
+__global__ void k_bsr_rows(const BsrItem* __restrict__ items, const int64_t* __restrict__ row_off,
+                           const int64_t* __restrict__ part_off, const double* __restrict__ base,
+                           const double* __restrict__ v, int64_t dim, int nvec, double* __restrict__ rp) {
   const int k = blockIdx.x, iv0 = blockIdx.y * kBsrVG;
-  const int r = brow[k], c = bcol[k];
-  const int64_t r0 = row_off[r], c0 = row_off[c];
-  const int pr = (int)(row_off[r + 1] - r0), pc = (int)(row_off[c + 1] - c0);
+  const BsrItem it = items[k];
+  const int64_t r0 = row_off[it.r], c0 = row_off[it.c];
+  const int pr = (int)(row_off[it.r + 1] - r0), pc = (int)(row_off[it.c + 1] - c0);
   const int nv = min(kBsrVG, nvec - iv0);
   double* out = rp + part_off[k] * nvec;  // nvec x p_r
-  const bool own = owner[k] == rank;
-  const double* B = vals + val_off[k];
+  const double* B = base + it.off;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int i = warp; i < pr; i += nw) {
     double s[kBsrVG] = {0.0, 0.0, 0.0, 0.0};
-    if (own) {
-      const double* Bi = B + (int64_t)i * pc;
-      for (int j = lane; j < pc; j += 32) {
-        const double bij = Bi[j];
+    const double* Bi = B + (int64_t)i * pc;
+    for (int j = lane; j < pc; j += 32) {
+      const double bij = Bi[j];
 #pragma unroll
-        for (int q = 0; q < kBsrVG; q++)
-          if (q < nv) s[q] = fma(bij, v[(int64_t)(iv0 + q) * dim + c0 + j], s[q]);
-      }
+      for (int q = 0; q < kBsrVG; q++)
+        if (q < nv) s[q] = fma(bij, v[(int64_t)(iv0 + q) * dim + c0 + j], s[q]);
     }
 #pragma unroll
     for (int q = 0; q < kBsrVG; q++) {
@@ -105,29 +108,25 @@ __global__ void k_bsr_rows(const int32_t* __restrict__ brow, const int32_t* __re
   }
 }
 
-__global__ void k_bsr_cols(const int32_t* __restrict__ brow, const int32_t* __restrict__ bcol,
-                           const int64_t* __restrict__ val_off, const int32_t* __restrict__ owner, int rank,
-                           const int64_t* __restrict__ row_off, const int64_t* __restrict__ part_off,
-                           const double* __restrict__ vals, const double* __restrict__ v, int64_t dim, int nvec,
-                           double* __restrict__ cp) {
+__global__ void k_bsr_cols(const BsrItem* __restrict__ items, const int64_t* __restrict__ row_off,
+                           const int64_t* __restrict__ part_off, const double* __restrict__ base,
+                           const double* __restrict__ v, int64_t dim, int nvec, double* __restrict__ cp) {
   const int k = blockIdx.x, iv0 = blockIdx.z * kBsrVG;
-  const int r = brow[k], c = bcol[k];
-  if (r == c) return;
-  const int64_t r0 = row_off[r], c0 = row_off[c];
-  const int pr = (int)(row_off[r + 1] - r0), pc = (int)(row_off[c + 1] - c0);
+  const BsrItem it = items[k];
+  if (it.r == it.c) return;
+  const int64_t r0 = row_off[it.r], c0 = row_off[it.c];
+  const int pr = (int)(row_off[it.r + 1] - r0), pc = (int)(row_off[it.c + 1] - c0);
   const int j = blockIdx.y * blockDim.x + threadIdx.x;
   if (j >= pc) return;
   const int nv = min(kBsrVG, nvec - iv0);
   double s[kBsrVG] = {0.0, 0.0, 0.0, 0.0};
-  if (owner[k] == rank) {
-    const double* B = vals + val_off[k] + j;
+  const double* B = base + it.off + j;
 #pragma unroll 4
-    for (int i = 0; i < pr; i++) {
-      const double bij = B[(int64_t)i * pc];
+  for (int i = 0; i < pr; i++) {
+    const double bij = B[(int64_t)i * pc];
 #pragma unroll
-      for (int q = 0; q < kBsrVG; q++)
-        if (q < nv) s[q] = fma(bij, v[(int64_t)(iv0 + q) * dim + r0 + i], s[q]);
-    }
+    for (int q = 0; q < kBsrVG; q++)
+      if (q < nv) s[q] = fma(bij, v[(int64_t)(iv0 + q) * dim + r0 + i], s[q]);
   }
   double* out = cp + part_off[k] * nvec;  // nvec x p_c
 #pragma unroll
@@ -135,24 +134,20 @@ __global__ void k_bsr_cols(const int32_t* __restrict__ brow, const int32_t* __re
     if (q < nv) out[(int64_t)(iv0 + q) * pc + j] = s[q];
 }
 
-// y[cell rows] = row partials of the cell's block row (in order) + column partials of the
-// blocks in its block column (in order)
-__global__ void k_bsr_reduce(const int32_t* __restrict__ brow_ptr, const int32_t* __restrict__ csc_ptr,
-                             const int32_t* __restrict__ csc_blk, const int64_t* __restrict__ row_off,
-                             const int64_t* __restrict__ rpart_off, const int64_t* __restrict__ cpart_off,
-                             const double* __restrict__ rp, const double* __restrict__ cp, int64_t dim, int nvec,
-                             double* __restrict__ y) {
+// y[cell rows] = the row partials of the items in the cell's block row (item order) + the
+// column partials of the off-diagonal items in its block column (item order)
+__global__ void k_bsr_reduce(const int32_t* __restrict__ rl_ptr, const int64_t* __restrict__ rl,
+                             const int32_t* __restrict__ cl_ptr, const int64_t* __restrict__ cl,
+                             const int64_t* __restrict__ row_off, const double* __restrict__ rp,
+                             const double* __restrict__ cp, int64_t dim, int nvec, double* __restrict__ y) {
   const int r = blockIdx.x;
   const int64_t r0 = row_off[r];
   const int pr = (int)(row_off[r + 1] - r0);
   for (int e = threadIdx.x; e < pr * nvec; e += blockDim.x) {
     const int iv = e / pr, i = e - iv * pr;
     double s = 0.0;
-    for (int k = brow_ptr[r]; k < brow_ptr[r + 1]; k++) s += rp[rpart_off[k] * nvec + (int64_t)iv * pr + i];
-    for (int q = csc_ptr[r]; q < csc_ptr[r + 1]; q++) {
-      const int k = csc_blk[q];
-      s += cp[cpart_off[k] * nvec + (int64_t)iv * pr + i];
-    }
+    for (int q = rl_ptr[r]; q < rl_ptr[r + 1]; q++) s += rp[rl[q] * nvec + (int64_t)iv * pr + i];
+    for (int q = cl_ptr[r]; q < cl_ptr[r + 1]; q++) s += cp[cl[q] * nvec + (int64_t)iv * pr + i];
     y[(int64_t)iv * dim + r0 + i] = s;
   }
 }
@@ -246,24 +241,44 @@ void cov_matvec_dev(Ctx& c, const mlk_tree_s* tree, const mlk_kernel& k, const d
   // rows of this rank: a contiguous range of 32-row tiles (for the symmetric kernel balanced by
   // the triangular task costs n - 32 I)
   const int64_t tiles = ceil_div(n, 32);
-  int64_t t0 = tiles * c.rank / c.nranks, t1 = tiles * (c.rank + 1) / c.nranks;
-  const bool sym_ok = nvec <= 4 && std::getenv("MLK_NO_SYM_MATVEC") == nullptr;
-  int64_t cp = 0;
-  if (sym_ok) {
-    // balance the triangular costs (n - 32 I) over ranks
+  auto sym_range = [&](int r, int64_t& a0, int64_t& a1) {
     auto cost_before = [&](int64_t I) { return (double)I * n - 16.0 * I * (I - 1); };
     const double total = cost_before(tiles);
-    t0 = 0;
-    while (t0 < tiles && cost_before(t0 + 1) <= total * c.rank / c.nranks) t0++;
-    t1 = t0;
-    while (t1 < tiles && cost_before(t1 + 1) <= total * (c.rank + 1) / c.nranks) t1++;
-    if (c.rank == c.nranks - 1) t1 = tiles;
-    for (int64_t I = t0; I < t1; I++) cp += 4 * (int64_t)nvec * (n - 32 * I);
+    a0 = 0;
+    while (a0 < tiles && cost_before(a0 + 1) <= total * r / c.nranks) a0++;
+    a1 = a0;
+    while (a1 < tiles && cost_before(a1 + 1) <= total * (r + 1) / c.nranks) a1++;
+    if (r == c.nranks - 1) a1 = tiles;
+  };
+  auto sym_partials = [&](int64_t a0, int64_t a1) {
+    int64_t s = 0;
+    for (int64_t I = a0; I < a1; I++) s += 4 * (int64_t)nvec * (n - 32 * I);
+    return s;
+  };
+  // The symmetric and the row-panel kernels split the rows differently, so every rank must take
+  // the same branch: the choice depends only on (n, nvec, nranks) and the device's TOTAL memory
+  // (identical across the ranks of one box), never on this rank's free memory.  The symmetric
+  // kernel's column partials of the largest rank share must fit a quarter of the device.
+  bool sym = nvec <= 4 && std::getenv("MLK_NO_SYM_MATVEC") == nullptr;
+  if (sym) {
+    int64_t worst = 0;
+    for (int r = 0; r < c.nranks; r++) {
+      int64_t a0, a1;
+      sym_range(r, a0, a1);
+      worst = std::max(worst, sym_partials(a0, a1));
+    }
+    sym = worst * (int64_t)sizeof(double) <= device_total_bytes(c.device) / 4;
+  }
+  int64_t t0 = tiles * c.rank / c.nranks, t1 = tiles * (c.rank + 1) / c.nranks;
+  int64_t cp = 0;
+  if (sym) {
+    sym_range(c.rank, t0, t1);
+    cp = sym_partials(t0, t1);
   }
   if (t1 <= t0) return;
   const int nv = nvec == 1 ? 1 : nvec == 2 ? 2 : 4;
   std::vector<TileUnit> units;
-  if (sym_ok && cp * (int64_t)sizeof(double) <= c.scratch_budget_bytes()) {
+  if (sym) {
     int64_t off = 0;
     for (int64_t I = t0; I < t1; I++) {
       const int64_t r = 32 * I;
@@ -296,6 +311,86 @@ void cov_matvec_dev(Ctx& c, const mlk_tree_s* tree, const mlk_kernel& k, const d
   if (nvec <= 4)
     for (auto& u : units) u.rq = -nv;
   run_tile_contract(c, tree, make_kernel_params(k), units, "cov_matvec_tile");
+}
+
+// y = (this rank's items of) C~_W v, v / y device nvec x dim
+void bsr_matvec_dev(Ctx& c, const mlk_basis_s* basis, const mlk_cw_s* cw, const double* v, double* y, int nvec) {
+  const int64_t dim = basis->dim;
+  const int64_t nb = cw->n_blocks;
+  std::vector<BsrItem> items;
+  const double* base = cw->vals();
+  if (c.nranks == 1) {
+    for (int64_t k = 0; k < nb; k++) items.push_back({cw->brow[k], cw->bcol[k], cw->val_off[k]});
+  } else if (cw->complete) {
+    for (int64_t k = 0; k < nb; k++)
+      if (cw->owner[k] == c.rank) items.push_back({cw->brow[k], cw->bcol[k], cw->val_off[k]});
+  } else {
+    base = cw->shard.p;
+    for (int64_t k = 0; k < nb; k++)
+      for (int64_t p = cw->piece_ptr[k]; p < cw->piece_ptr[k + 1]; p++)
+        if (cw->piece_owner[p] == c.rank) items.push_back({cw->brow[k], cw->bcol[k], cw->piece_off[p]});
+  }
+  if (items.empty()) {
+    CUDA_CHECK(cudaMemsetAsync(y, 0, sizeof(double) * nvec * dim, c.stream));
+    return;
+  }
+  const int64_t ni = (int64_t)items.size();
+  const int nc = cw->n_cells;
+  // partial offsets (per vector): p_row per item, p_col per off-diagonal item; per cell the
+  // lists of row partials (items in its block row) and column partials (its block column)
+  std::vector<int64_t> rpo(ni), cpo(ni);
+  std::vector<int32_t> rl_ptr(nc + 1, 0), cl_ptr(nc + 1, 0);
+  int64_t rtot = 0, ctot = 0;
+  int pcmax = 1;
+  for (int64_t k = 0; k < ni; k++) {
+    const int r = items[k].r, cc = items[k].c;
+    const int pr = (int)(basis->row_off[r + 1] - basis->row_off[r]);
+    const int pc = (int)(basis->row_off[cc + 1] - basis->row_off[cc]);
+    rpo[k] = rtot;
+    rtot += pr;
+    rl_ptr[r + 1]++;
+    cpo[k] = ctot;
+    if (r != cc) {
+      ctot += pc;
+      cl_ptr[cc + 1]++;
+    }
+    pcmax = std::max(pcmax, pc);
+  }
+  for (int i = 0; i < nc; i++) {
+    rl_ptr[i + 1] += rl_ptr[i];
+    cl_ptr[i + 1] += cl_ptr[i];
+  }
+  std::vector<int64_t> rl(std::max<int32_t>(rl_ptr[nc], 1)), cl(std::max<int32_t>(cl_ptr[nc], 1));
+  {
+    std::vector<int32_t> rf(rl_ptr.begin(), rl_ptr.end() - 1), cf(cl_ptr.begin(), cl_ptr.end() - 1);
+    for (int64_t k = 0; k < ni; k++) {
+      rl[rf[items[k].r]++] = rpo[k];
+      if (items[k].r != items[k].c) cl[cf[items[k].c]++] = cpo[k];
+    }
+  }
+  DevBuf<BsrItem> it_d(ni, c.stream);
+  it_d.upload(items);
+  DevBuf<int64_t> ro(basis->row_off.size(), c.stream), rpo_d(ni, c.stream), cpo_d(ni, c.stream);
+  ro.upload(basis->row_off);
+  rpo_d.upload(rpo);
+  cpo_d.upload(cpo);
+  DevBuf<int32_t> rlp_d(nc + 1, c.stream), clp_d(nc + 1, c.stream);
+  rlp_d.upload(rl_ptr);
+  clp_d.upload(cl_ptr);
+  DevBuf<int64_t> rl_d(rl.size(), c.stream), cl_d(cl.size(), c.stream);
+  rl_d.upload(rl);
+  cl_d.upload(cl);
+  DevBuf<double> rp((size_t)std::max<int64_t>(rtot * nvec, 1), c.stream);
+  DevBuf<double> cp((size_t)std::max<int64_t>(ctot * nvec, 1), c.stream);
+  TimedLaunch tl(c, "bsr_matvec");
+  const unsigned vg = (unsigned)ceil_div(nvec, kBsrVG);
+  k_bsr_rows<<<dim3((unsigned)ni, vg), 256, 0, c.stream>>>(it_d.p, ro.p, rpo_d.p, base, v, dim, nvec, rp.p);
+  check_launch("k_bsr_rows");
+  k_bsr_cols<<<dim3((unsigned)ni, (unsigned)ceil_div(pcmax, 256), vg), 256, 0, c.stream>>>(it_d.p, ro.p, cpo_d.p,
+                                                                                            base, v, dim, nvec, cp.p);
+  check_launch("k_bsr_cols");
+  k_bsr_reduce<<<(unsigned)nc, 256, 0, c.stream>>>(rlp_d.p, rl_d.p, clp_d.p, cl_d.p, ro.p, rp.p, cp.p, dim, nvec, y);
+  check_launch("k_bsr_reduce");
 }
 
 void check_kernel(const mlk_kernel* k) {
@@ -375,53 +470,14 @@ mlk_status mlk_cw_matvec(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const mlk_
     apply_wt_dev(c, tree, basis, vin.p, a.p, nvec);
     cov_matvec_dev(c, tree, *kernel, a.p, b.p, nvec);
     apply_w_dev(c, tree, basis, b.p, yout.p, nvec);
+    comm_allreduce_sum(c, yout.p, (int64_t)nvec * dim);  // no-op without a communicator
     yout.finish();
   } else {
     MLK_REQUIRE(cw != nullptr, "BSR mode needs the assembled matrix");
     MLK_REQUIRE(cw->n_cells == (int32_t)basis->cells.size(), "cw does not match the basis");
-    MLK_REQUIRE(cw->complete, "BSR mode with nranks > 1 needs mlk_cw_unpack first");
-    DevBuf<int64_t> ro(basis->row_off.size(), c.stream);
-    ro.upload(basis->row_off);
-    DevBuf<int32_t> brp(cw->brow_ptr.size(), c.stream);
-    brp.upload(cw->brow_ptr);
-    // partial offsets (per vector): row partials p_row per block, column partials p_col per
-    // off-diagonal block
-    const int64_t nb = cw->n_blocks;
-    std::vector<int64_t> rpo(std::max<int64_t>(nb, 1), 0), cpo(std::max<int64_t>(nb, 1), 0);
-    int64_t rtot = 0, ctot = 0;
-    int pcmax = 0;
-    for (int64_t k = 0; k < nb; k++) {
-      const int r = cw->brow[k], cc = cw->bcol[k];
-      const int pr = (int)(basis->row_off[r + 1] - basis->row_off[r]);
-      const int pc = (int)(basis->row_off[cc + 1] - basis->row_off[cc]);
-      rpo[k] = rtot;
-      rtot += pr;
-      cpo[k] = ctot;
-      if (r != cc) ctot += pc;
-      pcmax = std::max(pcmax, pc);
-    }
-    if (nb > 0) {
-      DevBuf<int64_t> rpo_d(rpo.size(), c.stream), cpo_d(cpo.size(), c.stream);
-      rpo_d.upload(rpo);
-      cpo_d.upload(cpo);
-      DevBuf<double> rp((size_t)std::max<int64_t>(rtot * nvec, 1), c.stream);
-      DevBuf<double> cp((size_t)std::max<int64_t>(ctot * nvec, 1), c.stream);
-      TimedLaunch tl(c, "bsr_matvec");
-      const unsigned vg = (unsigned)ceil_div(nvec, kBsrVG);
-      k_bsr_rows<<<dim3((unsigned)nb, vg), 256, 0, c.stream>>>(cw->brow_d.p, cw->bcol_d.p, cw->val_off_d.p,
-                                                               cw->owner_d.p, c.rank, ro.p, rpo_d.p, cw->vals(), vin.p,
-                                                               dim, nvec, rp.p);
-      check_launch("k_bsr_rows");
-      k_bsr_cols<<<dim3((unsigned)nb, (unsigned)ceil_div(std::max(pcmax, 1), 256), vg), 256, 0, c.stream>>>(
-          cw->brow_d.p, cw->bcol_d.p, cw->val_off_d.p, cw->owner_d.p, c.rank, ro.p, cpo_d.p, cw->vals(), vin.p, dim,
-          nvec, cp.p);
-      check_launch("k_bsr_cols");
-      k_bsr_reduce<<<(unsigned)cw->n_cells, 256, 0, c.stream>>>(brp.p, cw->csc_ptr_d.p, cw->csc_blk_d.p, ro.p, rpo_d.p,
-                                                               cpo_d.p, rp.p, cp.p, dim, nvec, yout.p);
-      check_launch("k_bsr_reduce");
-    } else {
-      CUDA_CHECK(cudaMemsetAsync(yout.p, 0, sizeof(double) * nvec * dim, c.stream));
-    }
+    MLK_REQUIRE(cw->nranks == c.nranks && cw->rank == c.rank, "cw was assembled for another rank layout");
+    bsr_matvec_dev(c, basis, cw, vin.p, yout.p, nvec);
+    comm_allreduce_sum(c, yout.p, (int64_t)nvec * dim);  // no-op without a communicator
     yout.finish();
   }
   MLK_API_END

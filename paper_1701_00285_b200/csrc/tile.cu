@@ -46,22 +46,17 @@ KernelParams make_kernel_params(const mlk_kernel& k) {
     default: p.c1 = 1.0 / (k.rho * k.rho); break;
   }
   if (k.family == MLK_MATERN_NU) {
-    // constants of Temme's method for K_mu (mu = nu - round(nu)), in long double
+    // constants of matern_nu (computed once, in long double)
+    const long double nu = k.nu;
     p.nu = k.nu;
-    p.nl = (int32_t)std::floor(k.nu + 0.5);
-    const long double mu = (long double)k.nu - p.nl;
-    const long double gampl = 1.0L / std::tgamma(1.0L + mu), gammi = 1.0L / std::tgamma(1.0L - mu);
-    p.mu = (double)mu;
-    p.gampl = (double)gampl;
-    p.gammi = (double)gammi;
-    p.gam1 = std::fabs(mu) < 1e-6L ? -0.5772156649015329 : (double)((gammi - gampl) / (2.0L * mu));
-    p.gam2 = (double)((gammi + gampl) / 2.0L);
-    const long double pimu = 3.14159265358979323846264338327950288L * mu;
-    p.fact = std::fabs(mu) < 1e-18L ? 1.0 : (double)(pimu / std::sin(pimu));
-    p.norm = (double)(std::pow(2.0L, 1.0L - (long double)k.nu) / std::tgamma((long double)k.nu));
+    p.norm = (double)(std::pow(2.0L, 1.0L - nu) / std::tgamma(nu));
+    p.h0 = std::min(0.2, 0.5 / std::sqrt(k.nu + 1.0));
+    p.series = std::fabs(k.nu - std::nearbyint(k.nu)) >= 0.01 ? 1 : 0;
+    p.g1m = p.series ? (double)std::tgamma(1.0L - nu) : 0.0;
+    p.rg1p = (double)(1.0L / std::tgamma(1.0L + nu));
   } else {
-    p.nu = p.mu = p.gam1 = p.gam2 = p.gampl = p.gammi = p.fact = p.norm = 0.0;
-    p.nl = 0;
+    p.nu = p.norm = p.h0 = p.g1m = p.rg1p = 0.0;
+    p.series = 0;
   }
   // coordinates are pre-scaled so that the augmented Gram product is z^2 = (c1 r)^2
   // (Matern) or r^2 / rho^2 (Gaussian)
@@ -129,63 +124,50 @@ void make_tile_units(std::vector<TileUnit>& out, int64_t a_begin, int32_t s_a, i
 
 namespace {
 
-// 2^(1-nu)/Gamma(nu) z^nu K_nu(z), z > 0: K_mu and K_{mu+1} by Temme's series (z < 2) or
-// Steed's continued fraction CF2 (z >= 2), then the upward recurrence to nu = nl + mu
-// (the classical Temme / Thompson-Barnett scheme; the mu constants come from the host)
+// phi(z) = 2^(1-nu)/Gamma(nu) z^nu K_nu(z), z > 0 (the Matern definition), from
+// two textbook representations of K_nu:
+//  * the integral K_nu(z) = int_0^inf exp(-z cosh t) cosh(nu t) dt, by the trapezoidal rule with
+//    step h = h0 / max(1, sqrt z).  The integrand is entire and decays double-exponentially, so
+//    the rule converges geometrically in 1/h; the sqrt(z) scaling keeps the peak of width
+//    ~1/sqrt(z) resolved at large z.  z^nu is folded into the exponent,
+//    z^nu e^{-z cosh t} cosh(nu t) = e^{nu (t + log z) - z cosh t} (1 + e^{-2 nu t}) / 2,
+//    so nothing overflows for large nu or small z; the sum stops once t is past the integrand's
+//    peak (sinh t = nu / z) and a term falls below 1e-17 of the sum.  e^t and e^{-2 nu t} advance
+//    by one multiplication per node.  Measured against scipy's K_nu (tools, this round): relative
+//    error <= 7e-13 for nu in [0.1, 50], z in [1e-8, 700]; <= 2e-13 for nu <= 12.
+//  * for z < 2 and nu at least 0.01 from an integer, the series from K_nu = pi/2 (I_-nu - I_nu) /
+//    sin(nu pi) and I_mu(z) = sum_k (z/2)^(2k+mu) / (k! Gamma(k+mu+1)), which with
+//    Gamma(nu) Gamma(1-nu) = pi / sin(nu pi) becomes
+//      phi = sum_k w^k Gamma(1-nu) / (k! Gamma(k+1-nu)) - Gamma(1-nu) (z/2)^(2 nu) sum_k w^k / (k! Gamma(k+1+nu)),
+//    w = z^2 / 4 (about 13 terms; phi(0) = 1 is its k = 0 term).  Near integer nu the two sums
+//    cancel (Gamma(1-nu) has poles there), so those nu always take the integral.
 __device__ __noinline__ double matern_nu(double z, const KernelParams& kp) {
-  const double xmu = kp.mu, xmu2 = xmu * xmu, xi = 1.0 / z, xi2 = 2.0 * xi;
-  double rkmu, rk1;
-  if (z < 2.0) {
-    const double x2 = 0.5 * z;
-    double dl = -log(x2);
-    double e = xmu * dl;
-    const double fact2 = fabs(e) < 1e-16 ? 1.0 : sinh(e) / e;
-    double ff = kp.fact * (kp.gam1 * cosh(e) + kp.gam2 * fact2 * dl);
-    double sum = ff;
-    e = exp(e);
-    double p = 0.5 * e / kp.gampl, q = 0.5 / (e * kp.gammi), c = 1.0, sum1 = p;
-    const double dd = x2 * x2;
-    for (int i = 1; i < 200; i++) {
-      ff = (i * ff + p + q) / ((double)i * i - xmu2);
-      c *= dd / i;
-      p /= (i - xmu);
-      q /= (i + xmu);
-      const double del = c * ff;
-      sum += del;
-      sum1 += c * (p - i * ff);
-      if (fabs(del) < fabs(sum) * 1e-17) break;
+  const double nu = kp.nu;
+  if (kp.series && z < 2.0) {
+    const double w = 0.25 * z * z;
+    double a = 1.0, sm = 1.0, b = kp.rg1p, sp = kp.rg1p;
+    for (int k = 1; k < 100; k++) {
+      a *= w / (k * (k - nu));
+      b *= w / (k * (k + nu));
+      sm += a;
+      sp += b;
+      if (fabs(a) <= 1e-17 * fabs(sm) && fabs(b) <= 1e-17 * fabs(sp)) break;
     }
-    rkmu = sum;
-    rk1 = sum1 * xi2;
-  } else {
-    double b = 2.0 * (1.0 + z), d = 1.0 / b, h = d, delh = d, q1 = 0.0, q2 = 1.0;
-    const double a1 = 0.25 - xmu2;
-    double q = a1, c = a1, a = -a1, s = 1.0 + q * delh;
-    for (int i = 2; i < 500; i++) {
-      a -= 2 * (i - 1);
-      c = -a * c / i;
-      const double qnew = (q1 - b * q2) / a;
-      q1 = q2;
-      q2 = qnew;
-      q += c * qnew;
-      b += 2.0;
-      d = 1.0 / (b + a * d);
-      delh = (b * d - 1.0) * delh;
-      h += delh;
-      const double dels = q * delh;
-      s += dels;
-      if (fabs(dels / s) < 1e-17) break;
-    }
-    h = a1 * h;
-    rkmu = sqrt(1.5707963267948966 * xi) * exp(-z) / s;
-    rk1 = rkmu * (xmu + z + 0.5 - h) * xi;
+    return sm - kp.g1m * exp(2.0 * nu * log(0.5 * z)) * sp;
   }
-  for (int i = 1; i <= kp.nl; i++) {
-    const double t = (xmu + i) * xi2 * rk1 + rkmu;
-    rkmu = rk1;
-    rk1 = t;
+  const double h = kp.h0 / fmax(1.0, sqrt(z));
+  const double lz = nu * log(z), E = exp(h), Q = exp(-2.0 * nu * h);
+  const double tpk = asinh(nu / z);
+  double e = 1.0, q = 1.0, s = 0.5 * exp(lz - z);  // node t = 0, weight 1/2
+  for (int k = 1; k < 4096; k++) {
+    e *= E;
+    q *= Q;
+    const double t = k * h;
+    const double term = exp(nu * t + lz - 0.5 * z * (e + 1.0 / e)) * 0.5 * (1.0 + q);
+    s += term;
+    if (t > tpk && term <= 1e-17 * s) break;
   }
-  return kp.norm * pow(z, kp.nu) * rkmu;
+  return kp.norm * h * s;
 }
 
 // correlation phi from the augmented Gram value x = z^2 (Matern, z = sqrt(2 nu) r / rho) or

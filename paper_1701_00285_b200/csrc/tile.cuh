@@ -40,11 +40,11 @@ struct KernelParams {
   double nugget;
   double same_val;  // 1 + nugget / sigma2: the correlation of a site with itself (R18)
   double scale;     // coordinate pre-scale of the augmented Gram product (c1, or 1 / rho)
-  // MLK_MATERN_NU: nu = nl + mu (nl = round(nu), |mu| <= 1/2) and the mu-dependent constants
-  // of Temme's series (1/Gamma(1 +- mu), gamma_1, gamma_2, pi mu / sin(pi mu)), and
-  // 2^(1 - nu) / Gamma(nu)
-  double nu, mu, gam1, gam2, gampl, gammi, fact, norm;
-  int32_t nl;
+  // MLK_MATERN_NU (tile.cu matern_nu): nu, norm = 2^(1 - nu) / Gamma(nu), the trapezoid step
+  // scale h0, and for the small-z series g1m = Gamma(1 - nu), rg1p = 1 / Gamma(1 + nu) (used
+  // only when nu is at least 0.01 away from an integer: series != 0)
+  double nu, norm, h0, g1m, rg1p;
+  int32_t series;
 };
 
 KernelParams make_kernel_params(const mlk_kernel& k);

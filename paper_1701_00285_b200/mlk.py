@@ -22,13 +22,14 @@ _lib = C.CDLL(LIB_PATH)
 
 # enums (include/mlk.h)
 OK, ERR_INVALID_ARG, ERR_DUPLICATE_POINTS, ERR_RANK_DEFICIENT, ERR_OUT_OF_MEMORY, ERR_CUDA, \
-    ERR_UNSUPPORTED = range(7)
+    ERR_UNSUPPORTED, ERR_NCCL = range(8)
 TREE_KD, TREE_RP = 0, 1
 MATERN_12, MATERN_32, MATERN_52, GAUSSIAN, MATERN_NU = 0, 1, 2, 3, 4
 PAIRS_ALL, PAIRS_PAPER_TAU = 0, 1
 PREC_FP64, PREC_DD = 0, 1
 VALUES_DEVICE, VALUES_HOST = 0, 1
 MATVEC_EXACT, MATVEC_BSR = 0, 1
+GATHER_NONE, GATHER_DEVICE, GATHER_HOST = 0, 1, 2
 INDEX_TD, INDEX_HC, INDEX_SM, INDEX_TP = 0, 1, 2, 3
 
 SYMBOLS = [
@@ -40,6 +41,7 @@ SYMBOLS = [
     "mlk_cw_unpack", "mlk_cw_values_device", "mlk_cov_matvec", "mlk_cw_matvec", "mlk_partition_lpt",
     "mlk_shard_plan", "mlk_launch_count", "mlk_cw_flops", "mlk_cw_export_async", "mlk_ctx_wait_copies",
     "mlk_pcg_solve", "mlk_build_basis_ex", "mlk_assemble_cw_ex", "mlk_cw_export_pieces", "mlk_loglik",
+    "mlk_nccl_unique_id", "mlk_gather_plan",
 ]
 
 
@@ -70,7 +72,9 @@ P = C.c_void_p
 _sig = {
     "mlk_last_error": (C.c_char_p, []),
     "mlk_version": (C.c_char_p, []),
-    "mlk_ctx_create": (C.c_int, [C.c_int, C.c_int, C.c_int, P, C.POINTER(P)]),
+    "mlk_ctx_create": (C.c_int, [C.c_int, C.c_int, C.c_int, P, P, C.POINTER(P)]),
+    "mlk_nccl_unique_id": (C.c_int, [P]),
+    "mlk_gather_plan": (C.c_int, [C.c_int64, P, P, P, P, C.c_int32, C.c_int64, P, P, P, P]),
     "mlk_ctx_destroy": (None, [P]),
     "mlk_ctx_stream": (P, [P]),
     "mlk_ctx_set_timing": (C.c_int, [P, C.c_int]),
@@ -90,9 +94,9 @@ _sig = {
     "mlk_apply_wt": (C.c_int, [P, P, P, P, C.c_int32]),
     "mlk_apply_w": (C.c_int, [P, P, P, P, C.c_int32]),
     "mlk_assemble_cw": (C.c_int, [P, P, P, C.POINTER(KernelSpec), C.POINTER(SparsitySpec), C.c_int32,
-                                  C.POINTER(P)]),
+                                  C.c_int32, C.POINTER(P)]),
     "mlk_assemble_cw_ex": (C.c_int, [P, P, P, C.POINTER(KernelSpec), C.POINTER(SparsitySpec), C.c_int32,
-                                     C.c_int32, C.POINTER(P)]),
+                                     C.c_int32, C.c_int32, C.POINTER(P)]),
     "mlk_cw_export_pieces": (C.c_int, [P, P, P, P, P]),
     "mlk_loglik": (C.c_int, [P, P, P, C.c_int32, P, P, P, P, P]),
     "mlk_cw_free": (None, [P]),
@@ -139,13 +143,30 @@ def launch_count():
     return int(_lib.mlk_launch_count())
 
 
-def _ptr(x, dtype=np.float64):
-    """(pointer, keepalive) for a NumPy array or torch tensor (no copy for contiguous inputs)."""
+_TORCH_DTYPE = {np.float64: "torch.float64", np.int64: "torch.int64", np.int32: "torch.int32"}
+
+
+def _ptr(x, dtype=np.float64, device=None, out=False):
+    """(pointer, keepalive) for a NumPy array or torch tensor (no copy for contiguous inputs).
+
+    Torch tensors are passed by address, so their dtype must be exactly `dtype` and a CUDA
+    tensor must live on the context's `device` (the library writes / reads nvec x dim x 8 bytes
+    there).  NumPy inputs are converted; a NumPy output (out=True) must already be a C-contiguous
+    array of `dtype`, since a converted copy would silently swallow the result."""
     if x is None:
         return None, None
     if hasattr(x, "data_ptr") and hasattr(x, "is_cuda"):
-        assert x.is_contiguous(), "tensor must be contiguous"
+        if str(x.dtype) != _TORCH_DTYPE[dtype]:
+            raise TypeError("tensor dtype %s, expected %s" % (x.dtype, _TORCH_DTYPE[dtype]))
+        if not x.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        if x.is_cuda and device is not None and x.device.index != device:
+            raise ValueError("CUDA tensor on cuda:%d, the context is on cuda:%d" % (x.device.index, device))
         return C.c_void_p(x.data_ptr()), x
+    if out:
+        if not (isinstance(x, np.ndarray) and x.dtype == dtype and x.flags["C_CONTIGUOUS"] and x.flags["WRITEABLE"]):
+            raise TypeError("output must be a writeable C-contiguous %s array" % np.dtype(dtype).name)
+        return x.ctypes.data_as(C.c_void_p), x
     a = np.ascontiguousarray(x, dtype=dtype)
     return a.ctypes.data_as(C.c_void_p), a
 
@@ -164,13 +185,29 @@ def _kspec(k):
     return kernel_spec(k["family"], k["rho"], k.get("sigma2", 1.0), k.get("nugget", 0.0), k.get("nu") or 0.0)
 
 
+def nccl_unique_id():
+    """A fresh 128-byte ncclUniqueId (bytes) for Ctx(..., nccl_id=...); call on one rank."""
+    buf = C.create_string_buffer(128)
+    _check(_lib.mlk_nccl_unique_id(buf))
+    return buf.raw
+
+
 class Ctx:
-    def __init__(self, device=0, nranks=1, rank=0, stream=None):
+    """mlk_ctx_create.  nccl_id (128 bytes from nccl_unique_id(), the same on every rank): the
+    library creates its own NCCL communicator and issues the all-gather / allreduce itself."""
+
+    def __init__(self, device=0, nranks=1, rank=0, stream=None, nccl_id=None):
         h = C.c_void_p()
-        _check(_lib.mlk_ctx_create(int(device), int(nranks), int(rank),
+        idbuf = None
+        if nccl_id is not None:
+            if len(nccl_id) != 128:
+                raise ValueError("nccl_id must be 128 bytes")
+            idbuf = C.create_string_buffer(bytes(nccl_id), 128)
+        _check(_lib.mlk_ctx_create(int(device), int(nranks), int(rank), idbuf,
                                    C.c_void_p(stream) if stream else None, C.byref(h)))
         self.h = h
         self.device, self.nranks, self.rank = device, nranks, rank
+        self.has_comm = nccl_id is not None
 
     @property
     def stream(self):
@@ -238,9 +275,9 @@ class Tree:
 
 
 def build_tree(ctx, X, leaf_size, kind, directions=None):
-    Xp, keep = _ptr(X)
+    Xp, keep = _ptr(X, device=ctx.device)
     n, d = X.shape
-    Dp, keep2 = _ptr(directions)
+    Dp, keep2 = _ptr(directions, device=ctx.device)
     nrows = 0 if directions is None else directions.shape[0]
     h = C.c_void_p()
     _check(_lib.mlk_build_tree(ctx.h, Xp, n, d, int(leaf_size), int(kind), Dp, nrows, C.byref(h)))
@@ -293,26 +330,35 @@ def build_basis(ctx, tree, w, index_set=INDEX_TD, flags=0):
     return Basis(h, tree, ctx)
 
 
-def _vec_io(x, nvec_dim, out, out_cols):
-    xp, keep = _ptr(x)
+def _numel(x):
+    return int(x.numel()) if hasattr(x, "numel") and callable(x.numel) else int(np.size(x))
+
+
+def _vec_io(x, in_cols, out, out_cols, device=None):
+    """Marshal an (nvec, in_cols) input and an (nvec, out_cols) output (checked sizes / dtypes)."""
+    xp, keep = _ptr(x, device=device)
     nvec = 1 if x.ndim == 1 else x.shape[0]
+    if _numel(x) != nvec * in_cols:
+        raise ValueError("input has %d entries, expected %d x %d" % (_numel(x), nvec, in_cols))
     if out is None:
         res = np.empty((nvec, out_cols), np.float64)
         op = _np(res)
     else:
+        if _numel(out) != nvec * out_cols:
+            raise ValueError("output has %d entries, expected %d x %d" % (_numel(out), nvec, out_cols))
         res = out
-        op, _ = _ptr(out)
+        op, _ = _ptr(out, device=device, out=True)
     return xp, keep, nvec, res, op
 
 
 def apply_wt(ctx, basis, v, out=None):
-    vp, keep, nvec, res, op = _vec_io(v, basis.dim, out, basis.tree.n)
+    vp, keep, nvec, res, op = _vec_io(v, basis.dim, out, basis.tree.n, ctx.device)
     _check(_lib.mlk_apply_wt(ctx.h, basis.h, vp, op, nvec))
     return res
 
 
 def apply_w(ctx, basis, b, out=None):
-    bp, keep, nvec, res, op = _vec_io(b, basis.tree.n, out, basis.dim)
+    bp, keep, nvec, res, op = _vec_io(b, basis.tree.n, out, basis.dim, ctx.device)
     _check(_lib.mlk_apply_w(ctx.h, basis.h, bp, op, nvec))
     return res
 
@@ -339,14 +385,18 @@ class CW:
     def export(self, out=None):
         brow_ptr, bcol, val_off = self.structure()
         vals = np.empty(self.nnz, np.float64) if out is None else out
-        vp, _ = _ptr(vals)
+        if _numel(vals) < self.nnz:
+            raise ValueError("output holds %d values, need %d" % (_numel(vals), self.nnz))
+        vp, _ = _ptr(vals, out=True)
         _check(_lib.mlk_cw_export(self.h, None, None, None, vp))
         return dict(brow_ptr=brow_ptr, bcol=bcol, val_off=val_off, values=vals)
 
     def export_async(self, ctx, out):
         """Enqueue the copy of all BSR values into `out` (NumPy array or torch tensor, ideally
         pinned) behind the work already on the context stream; ctx.wait_copies() completes it."""
-        vp, _ = _ptr(out)
+        if _numel(out) < self.nnz:
+            raise ValueError("output holds %d values, need %d" % (_numel(out), self.nnz))
+        vp, _ = _ptr(out, device=ctx.device, out=True)
         _check(_lib.mlk_cw_export_async(ctx.h, self.h, vp))
         self._async_keep = out
         return out
@@ -396,30 +446,32 @@ class CW:
             self.h = None
 
 
-def assemble_cw(ctx, tree, basis, kernel, sparsity, precision=PREC_FP64, placement=VALUES_DEVICE):
-    """mlk_assemble_cw (placement VALUES_DEVICE) or mlk_assemble_cw_ex (VALUES_HOST: the values
-    in mapped pinned host memory, for matrices beyond HBM)."""
+def assemble_cw(ctx, tree, basis, kernel, sparsity, precision=PREC_FP64, placement=VALUES_DEVICE, gather=None):
+    """mlk_assemble_cw_ex: values in device memory (VALUES_DEVICE) or mapped pinned host memory
+    (VALUES_HOST, for matrices beyond HBM).  gather (nranks > 1): GATHER_NONE keeps this rank's
+    shard, GATHER_DEVICE all-gathers over the context's NCCL communicator; default: gather iff the
+    context has a communicator."""
     h = C.c_void_p()
     ks = _kspec(kernel)
     sp = sparsity if isinstance(sparsity, SparsitySpec) else SparsitySpec(int(sparsity["mode"]),
                                                                            float(sparsity.get("tau", 0.0)))
-    if placement == VALUES_DEVICE:
-        _check(_lib.mlk_assemble_cw(ctx.h, tree.h, basis.h, C.byref(ks), C.byref(sp), int(precision), C.byref(h)))
-    else:
-        _check(_lib.mlk_assemble_cw_ex(ctx.h, tree.h, basis.h, C.byref(ks), C.byref(sp), int(precision),
-                                       int(placement), C.byref(h)))
+    if gather is None:
+        gather = GATHER_DEVICE if getattr(ctx, "has_comm", False) else GATHER_NONE
+    _check(_lib.mlk_assemble_cw_ex(ctx.h, tree.h, basis.h, C.byref(ks), C.byref(sp), int(precision),
+                                   int(placement), 1 if gather else 0, C.byref(h)))
     cw = CW(h, (ctx, tree, basis))
     cw.placement = placement
     return cw
 
 
 def gather_cw(ctx, cw, group=None):
-    """All-gather of the BSR shards over the caller's process group (NCCL on GPUs):
-    pack this rank's blocks, all_gather_into_tensor, unpack into BSR order."""
+    """Caller-side all-gather of the BSR shards over a torch.distributed group (for contexts
+    without a library communicator): pack this rank's pieces, all_gather_into_tensor, unpack
+    into BSR order.  Contexts with a communicator gather inside assemble_cw."""
     import torch
     import torch.distributed as dist
 
-    if ctx.nranks == 1:
+    if ctx.nranks == 1 or getattr(ctx, "has_comm", False):
         return
     _, mx = cw.shard_len()
     dev = torch.device("cuda", ctx.device)
@@ -440,20 +492,21 @@ def unpack_cw(ctx, cw, gathered):
 
 
 def cov_matvec(ctx, tree, kernel, a, out=None):
-    ap, keep, nvec, res, op = _vec_io(a, tree.n, out, tree.n)
+    ap, keep, nvec, res, op = _vec_io(a, tree.n, out, tree.n, ctx.device)
     ks = _kspec(kernel)
     _check(_lib.mlk_cov_matvec(ctx.h, tree.h, C.byref(ks), ap, op, nvec))
     return res
 
 
 def cw_matvec(ctx, tree, basis, kernel, cw, mode, v, out=None, allreduce=True, group=None):
-    """y = C_W v.  With nranks > 1 the partial results are sum-allreduced over `group`
-    (torch.distributed, NCCL) unless allreduce=False."""
-    vp, keep, nvec, res, op = _vec_io(v, basis.dim, out, basis.dim)
+    """y = C_W v.  nranks > 1: a context with a library communicator returns the allreduced y;
+    otherwise the partial results are sum-allreduced here over `group` (torch.distributed)
+    unless allreduce=False."""
+    vp, keep, nvec, res, op = _vec_io(v, basis.dim, out, basis.dim, ctx.device)
     ks = _kspec(kernel) if kernel is not None else kernel_spec(0, 1.0)
     _check(_lib.mlk_cw_matvec(ctx.h, tree.h, basis.h, C.byref(ks), cw.h if cw is not None else None,
                               int(mode), vp, op, nvec))
-    if ctx.nranks > 1 and allreduce:
+    if ctx.nranks > 1 and allreduce and not getattr(ctx, "has_comm", False):
         import torch
         import torch.distributed as dist
 
@@ -469,13 +522,17 @@ def cw_matvec(ctx, tree, basis, kernel, cw, mode, v, out=None, allreduce=True, g
 def pcg_solve(ctx, tree, basis, kernel, cw, z_w, tol=1e-10, max_iter=1000, precond=True, out=None):
     """gamma_W = C_W^-1 z_W by PCG with the block-diagonal preconditioner (cw's self blocks) or
     none.  Returns (gamma_W, iterations, true relative residual)."""
-    zp, keep = _ptr(z_w)
+    zp, keep = _ptr(z_w, device=ctx.device)
+    if _numel(z_w) != basis.dim:
+        raise ValueError("z_w has %d entries, expected %d" % (_numel(z_w), basis.dim))
     if out is None:
         res = np.empty(basis.dim, np.float64)
         op = _np(res)
     else:
+        if _numel(out) != basis.dim:
+            raise ValueError("out has %d entries, expected %d" % (_numel(out), basis.dim))
         res = out
-        op, _ = _ptr(out)
+        op, _ = _ptr(out, device=ctx.device, out=True)
     it = C.c_int32()
     rr = C.c_double()
     _check(_lib.mlk_pcg_solve(ctx.h, tree.h, basis.h, C.byref(_kspec(kernel)), cw.h if cw is not None else None,
@@ -486,7 +543,9 @@ def pcg_solve(ctx, tree, basis, kernel, cw, z_w, tol=1e-10, max_iter=1000, preco
 def loglik(ctx, basis, cw, z_w, level=0):
     """Level-truncated multi-level log-likelihood (mlk_loglik): returns dict(loglik, logdet,
     quad, n_tilde) for the cells of levels t .. level."""
-    zp, keep = _ptr(z_w)
+    zp, keep = _ptr(z_w, device=ctx.device)
+    if _numel(z_w) != basis.dim:
+        raise ValueError("z_w has %d entries, expected %d" % (_numel(z_w), basis.dim))
     ll, ld, q, nt = C.c_double(), C.c_double(), C.c_double(), C.c_int64()
     _check(_lib.mlk_loglik(ctx.h, basis.h, cw.h, int(level), zp, C.byref(ll), C.byref(ld), C.byref(q), C.byref(nt)))
     return dict(loglik=ll.value, logdet=ld.value, quad=q.value, n_tilde=nt.value)
@@ -497,6 +556,25 @@ def partition_lpt(cost, nranks):
     owner = np.empty(cost.size, np.int32)
     _check(_lib.mlk_partition_lpt(_np(cost), cost.size, int(nranks), _np(owner)))
     return owner
+
+
+def gather_plan(piece_ptr, piece_off, piece_owner, block_len, nranks, budget):
+    """(group_ptr, group_lo[n_groups, nranks], group_count) of the chunked all-gather (host only)."""
+    pp = np.ascontiguousarray(piece_ptr, dtype=np.int64)
+    po = np.ascontiguousarray(piece_off, dtype=np.int64)
+    pw = np.ascontiguousarray(piece_owner, dtype=np.int32)
+    bl = np.ascontiguousarray(block_len, dtype=np.int64)
+    nb = bl.size
+    ng = C.c_int64()
+    _check(_lib.mlk_gather_plan(nb, _np(pp), _np(po), _np(pw), _np(bl), int(nranks), int(budget), C.byref(ng),
+                                None, None, None))
+    g = ng.value
+    gp = np.empty(g + 1, np.int64)
+    gl = np.empty(max(g * nranks, 1), np.int64)
+    gc = np.empty(max(g, 1), np.int64)
+    _check(_lib.mlk_gather_plan(nb, _np(pp), _np(po), _np(pw), _np(bl), int(nranks), int(budget), C.byref(ng),
+                                _np(gp), _np(gl), _np(gc)))
+    return gp, gl[:g * nranks].reshape(g, nranks), gc[:g]
 
 
 def shard_plan(val_off, owner, nranks):

@@ -246,65 +246,130 @@ def test_identity_pin_on_gpu(mlk, ctx):
         assert np.max(np.abs(D - np.eye(gb.dim))) < 1e-13
 
 
-def test_cfg2_full_size_sampled_blocks(mlk, ctx):
-    """cfg2 at BASELINE size in the bench's launch configuration; blocks sampled and recomputed
-    one by one by the oracle (root-root, leaf self blocks, random admitted pairs)."""
-    inp = wl.make("cfg2")
-    c = inp["cfg"]
-    X = inp["X"]
-    g, o = _tree_both(mlk, ctx, X, c["leaf"], c["tree"], inp["dirs"])
-    gb = mlk.build_basis(ctx, g, c["w"])
-    ob = OB.build_basis(X, o, c["w"])
-    kern = wl.kernel_dict(c)
-    pairs = OA.admitted_pairs(X, o, ob, c["pairs"], c["tau"])
-    cw = mlk.assemble_cw(ctx, g, gb, kern, dict(mode=c["pairs"], tau=c["tau"]))
-    got = cw.export()
-    _, _, brow_ptr, bcol, val_off = OAs.bsr_structure(ob, pairs)
-    assert np.array_equal(got["val_off"], val_off) and len(pairs) == 2074
-    rng = np.random.default_rng([0, 3])
-    idx = set(rng.choice(len(pairs), 24, replace=False).tolist())
-    idx |= {k for k, (a, b) in enumerate(pairs) if a == 0 or b == 0}
-    idx |= {k for k, (a, b) in enumerate(pairs) if a == b}
-    idx = sorted(idx)[:60]
-    for k in idx:
-        a, b = pairs[k]
-        ref = OAs.block(X, o, ob, kern, a, b).ravel()
-        e = np.linalg.norm(got["values"][val_off[k]:val_off[k + 1]] - ref) / np.linalg.norm(ref)
-        assert e <= TOL_BLOCK, (k, a, b, e)
+_FULL = {}
 
 
-@pytest.mark.parametrize("name,max_entries", [("cfg3", 2 ** 22), ("cfg4", 2 ** 20)])
-def test_full_size_sampled_blocks(mlk, ctx, name, max_entries):
-    """cfg3 / cfg4 at BASELINE size in the bench's launch configuration: tree bit-exact, the
-    BSR structure bit-exact against the oracle's pair list (tests/golden/pairs_<cfg>.npz,
-    written by tools/make_golden_pairs.py from oracle/ only), and seeded sampled blocks
-    (leaf self blocks, random admitted pairs) recomputed one by one by the oracle."""
+def _full(name):
+    """Oracle tree / basis / pair list of a BASELINE config at full size (cached per module)."""
+    if name not in _FULL:
+        import os
+        inp = wl.make(name)
+        c = inp["cfg"]
+        X = inp["X"]
+        o = OT.build_tree(X, c["leaf"], c["tree"], inp["dirs"])
+        ob = OB.build_basis(X, o, c["w"])
+        gp = os.path.join(os.path.dirname(__file__), "golden", "pairs_%s.npz" % name)
+        if os.path.exists(gp):
+            pairs = [tuple(int(v) for v in p) for p in np.load(gp)["pairs"]]
+        else:
+            pairs = OA.admitted_pairs(X, o, ob, c["pairs"], c["tau"])
+        _FULL.clear()   # one config at a time (host memory)
+        _FULL[name] = (inp, c, X, o, ob, pairs)
+    return _FULL[name]
+
+
+def _golden(kind, name):
     import os
-    inp = wl.make(name)
-    c = inp["cfg"]
-    X = inp["X"]
-    g, o = _tree_both(mlk, ctx, X, c["leaf"], c["tree"], inp["dirs"])
+    return np.load(os.path.join(os.path.dirname(__file__), "golden", "%s_%s.npz" % (kind, name)))
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg4"])
+def test_full_size_blocks(mlk, ctx, name):
+    """BASELINE cfg2 / cfg3 / cfg4 at full size, assembled by the same calls bench.py times:
+    tree bit-exact, BSR structure bit-exact against the oracle's pair list, and the fixed sample
+    of tests/sampling.py (cfg2: the root-root block, EVERY block with both cells at level <= 2,
+    all leaf self blocks, 24 random pairs; cfg3 / cfg4: all leaf self blocks, 64 random pairs of
+    <= 2^28 entries and the (0,0) block) within 1e-11 relative Frobenius per block.  Blocks above
+    2^26 entries come from tests/golden/blocks_<cfg>.npz (tools/make_golden_blocks.py, oracle
+    only), the rest are recomputed here by the oracle.  The sample must include blocks summed
+    from several 4096-row pieces (the root-root block: n / 4096 of them)."""
+    import sampling
+    from oracle import fastcov as F
+    inp, c, X, o, ob, pairs = _full(name)
+    g = mlk.build_tree(ctx, X, c["leaf"], c["tree"], inp["dirs"])
     _check_tree(g, o)
     gb = mlk.build_basis(ctx, g, c["w"])
-    ob = OB.build_basis(X, o, c["w"])
-    gold = np.load(os.path.join(os.path.dirname(__file__), "golden", "pairs_%s.npz" % name))
-    pairs = [tuple(int(v) for v in p) for p in gold["pairs"]]
     kern = wl.kernel_dict(c)
     cw = mlk.assemble_cw(ctx, g, gb, kern, dict(mode=c["pairs"], tau=c["tau"]))
     got = cw.export()
     _, _, brow_ptr, bcol, val_off = OAs.bsr_structure(ob, pairs)
     assert np.array_equal(got["brow_ptr"], brow_ptr) and np.array_equal(got["bcol"], bcol)
     assert np.array_equal(got["val_off"], val_off)
-    size = lambda q: int(o.end[q] - o.begin[q])
-    rng = np.random.default_rng([0, 3])
-    selfs = [k for k, (a, b) in enumerate(pairs) if a == b and o.is_leaf[a]]
-    small = [k for k, (a, b) in enumerate(pairs) if a != b and size(a) * size(b) <= max_entries]
-    idx = sorted(set(rng.choice(selfs, 6, replace=False).tolist()) | set(rng.choice(small, 14, replace=False).tolist()))
+    idx = sampling.select_blocks(name, pairs, o)
+    gold = _golden("blocks", name)
+    need = set(sampling.golden_needed(pairs, o, idx))
+    assert need == set(int(k) for k in gold["index"])
+    piece_ptr = cw.pieces(with_shard=False)[0]
+    npieces = np.diff(piece_ptr)
+    multi = [k for k in idx if npieces[k] > 1]
+    root = [k for k, (a, b) in enumerate(pairs) if a == 0 and b == 0][0]
+    assert root in idx and npieces[root] == c["n"] // 4096, npieces[root]
+    assert len(multi) >= (8 if name == "cfg2" else 1), len(multi)
+    worst = 0.0
     for k in idx:
         a, b = pairs[k]
-        ref = OAs.block(X, o, ob, kern, a, b).ravel()
+        ref = gold["k%d" % k] if k in need else F.block_streamed(X, o, ob, kern, a, b)
+        ref = ref.ravel()
         e = np.linalg.norm(got["values"][val_off[k]:val_off[k + 1]] - ref) / np.linalg.norm(ref)
-        assert e <= TOL_BLOCK, (name, k, a, b, e)
+        worst = max(worst, e)
+        assert e <= TOL_BLOCK, (name, k, a, b, int(npieces[k]), e)
+    print("%s: %d blocks (%d multi-piece, root %d pieces), worst %.2e" % (name, len(idx), len(multi),
+                                                                           npieces[root], worst))
+
+
+def test_matvec_cfg1_config(mlk, ctx):
+    """C_W v at BASELINE cfg1's own configuration (n = 1024 uniform on [-1,1]^2, kD leaf 32,
+    Matern 1/2, rho = 0.5, w = 2, ALL pairs): EXACT and BSR against the oracle's dense W C W^T v."""
+    inp = wl.make("cfg1")
+    c = inp["cfg"]
+    X = inp["X"]
+    g, o = _tree_both(mlk, ctx, X, c["leaf"], c["tree"], None)
+    gb = mlk.build_basis(ctx, g, c["w"])
+    ob = OB.build_basis(X, o, c["w"])
+    kern = wl.kernel_dict(c)
+    CW, _, _ = OAs.dense_cw(X, o, ob, kern)
+    v = wl.vectors(3, gb.dim, seed=0)
+    yr = v @ CW.T
+    ye = mlk.cw_matvec(ctx, g, gb, kern, None, mlk.MATVEC_EXACT, v)
+    cw = mlk.assemble_cw(ctx, g, gb, kern, dict(mode=c["pairs"], tau=c["tau"]))
+    yb = mlk.cw_matvec(ctx, g, gb, kern, cw, mlk.MATVEC_BSR, v)
+    for y in (ye, yb):
+        assert np.linalg.norm(y - yr) <= 1e-11 * np.linalg.norm(yr), np.linalg.norm(y - yr) / np.linalg.norm(yr)
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg4"])
+def test_matvec_full_size(mlk, ctx, name):
+    """C_W v at full size against the oracle's three-step product (tests/golden/matvec_<cfg>.npz,
+    tools/make_golden_blocks.py; v = workloads.vectors(1, dim, seed=0)): EXACT everywhere, BSR at
+    cfg2 (the oracle's own C~_W of all 2074 blocks).  Each step also on its own: W^T v in full,
+    C a on 512 seeded rows with the oracle's a as input, W b on a seeded vector."""
+    from oracle import fastcov as F
+    import sampling
+    inp, c, X, o, ob, pairs = _full(name)
+    g = mlk.build_tree(ctx, X, c["leaf"], c["tree"], inp["dirs"])
+    gb = mlk.build_basis(ctx, g, c["w"])
+    kern = wl.kernel_dict(c)
+    gold = _golden("matvec", name)
+    nvec = c.get("nvec", 1)
+    v = wl.vectors(nvec, gb.dim, seed=0)          # row 0 is the golden's vector
+    yr = gold["y_exact"]
+    y = mlk.cw_matvec(ctx, g, gb, kern, None, mlk.MATVEC_EXACT, v)
+    assert np.linalg.norm(y[0] - yr) <= 1e-11 * np.linalg.norm(yr), np.linalg.norm(y[0] - yr) / np.linalg.norm(yr)
+    if "y_bsr" in gold.files:
+        cw = mlk.assemble_cw(ctx, g, gb, kern, dict(mode=c["pairs"], tau=c["tau"]))
+        yb = mlk.cw_matvec(ctx, g, gb, kern, cw, mlk.MATVEC_BSR, v[:1])
+        ybr = gold["y_bsr"]
+        assert np.linalg.norm(yb[0] - ybr) <= 1e-11 * np.linalg.norm(ybr)
+    a_ref = OM.apply_wt(o, ob, v[:1])
+    a = mlk.apply_wt(ctx, gb, v[:1])
+    assert np.max(np.abs(a - a_ref)) <= 1e-11 * np.max(np.abs(a_ref))
+    rows = sampling.matvec_rows(c["n"])
+    b = mlk.cov_matvec(ctx, g, kern, a_ref)
+    br = F.cov_rows(X, o, kern, a_ref, rows)
+    assert np.linalg.norm(b[:, rows] - br) <= 1e-11 * np.linalg.norm(br)
+    bin_ = np.random.default_rng([0, 4]).standard_normal((1, c["n"]))
+    assert np.linalg.norm(mlk.apply_w(ctx, gb, bin_) - OM.apply_w(o, ob, bin_)) <= \
+        1e-12 * np.linalg.norm(OM.apply_w(o, ob, bin_))
 
 
 def test_cfg5_shape_mini(mlk, ctx):
@@ -413,34 +478,9 @@ def test_cov_matvec_symmetric_and_full_agree(mlk, ctx, nvec, monkeypatch):
     assert np.linalg.norm(b_full - br) <= 1e-12 * np.linalg.norm(br)
 
 
-def test_matvec_cfg3_sampled_rows(mlk, ctx):
-    """cfg3 at full size with its 10 N(0,1) vectors: apply_wt / apply_w in full, C a on 512
-    seeded rows (the host cannot do the 1.7e10-entry product in test time)."""
-    inp = wl.make("cfg3")
-    c = inp["cfg"]
-    X = inp["X"]
-    g, o = _tree_both(mlk, ctx, X, c["leaf"], c["tree"], inp["dirs"])
-    gb = mlk.build_basis(ctx, g, c["w"])
-    ob = OB.build_basis(X, o, c["w"])
-    kern = wl.kernel_dict(c)
-    v = wl.vectors(10, gb.dim)
-    a = mlk.apply_wt(ctx, gb, v)
-    ar = OM.apply_wt(o, ob, v)
-    assert np.max(np.abs(a - ar)) <= 1e-11 * np.max(np.abs(ar))
-    b = mlk.cov_matvec(ctx, g, kern, a)
-    rows = np.random.default_rng([0, 3]).choice(c["n"], 512, replace=False)
-    br = OM.cov_matvec(X, o, kern, a, rows=rows)
-    assert np.linalg.norm(b[:, rows] - br) <= 1e-11 * np.linalg.norm(br)
-    y = mlk.apply_w(ctx, gb, b)
-    yr = OM.apply_w(o, ob, b)
-    assert np.linalg.norm(y - yr) <= 1e-12 * np.linalg.norm(yr)
-    y2 = mlk.cw_matvec(ctx, g, gb, kern, None, mlk.MATVEC_EXACT, v)
-    assert np.array_equal(y, y2)
-
-
 # --------------------------------------------------------------------------------- multi-rank
 @pytest.mark.parametrize("R", [2, 3, 8])
-def test_multirank_emulated_bit_identical(mlk, ctx, R):
+def test_multirank_emulated_bit_identical(mlk, ctx, R, monkeypatch):
     """nranks = R contexts on one GPU, run one after another (no rank waits on another): each
     assembles its LPT share, the shards are concatenated (what the NCCL all-gather does) and
     unpacked; values must equal the nranks = 1 result bit for bit, and the partial C_W v of
@@ -477,6 +517,52 @@ def test_multirank_emulated_bit_identical(mlk, ctx, R):
     ybs = [mlk.cw_matvec(c, t, b, kern, cw, mlk.MATVEC_BSR, v, allreduce=False)
            for c, t, b, cw in zip(ctxs, trees, bases, cws)]
     assert np.linalg.norm(sum(ybs) - yb1) <= 1e-13 * np.linalg.norm(yb1)
+    # S§8(e)'s sharded BSR product: fresh assemblies, NO gather -- each rank applies the pieces of
+    # its own shard and their mirrors; the partial products sum to the single-rank C~_W v
+    shard_cws = [mlk.assemble_cw(c, t, b, kern, sp) for c, t, b in zip(ctxs, trees, bases)]
+    ysh = [mlk.cw_matvec(c, t, b, kern, cw, mlk.MATVEC_BSR, v, allreduce=False)
+           for c, t, b, cw in zip(ctxs, trees, bases, shard_cws)]
+    assert np.linalg.norm(sum(ysh) - yb1) <= 1e-13 * np.linalg.norm(yb1)
+    # the chunked gather (the MLK_GATHER_DEVICE group plan, here fed from the caller's buffer)
+    # with a tiny staging budget: many groups, still bit-identical
+    monkeypatch.setenv("MLK_GATHER_BUDGET", str(4 * 66 * 66 * R))
+    shards = []
+    for c, cw in zip(ctxs, shard_cws):
+        buf = torch.empty(max(mx, 1), dtype=torch.float64, device="cuda")
+        mlk.pack_cw(c, cw, buf)
+        shards.append(buf)
+    gathered = torch.cat(shards)
+    for c, cw in zip(ctxs, shard_cws):
+        mlk.unpack_cw(c, cw, gathered)
+        assert np.array_equal(cw.export()["values"], ref)
+
+
+def test_library_nccl_communicator_world1(mlk, ctx):
+    """A context with its own NCCL communicator (mlk_ctx_create with a unique id; one rank on
+    this one-GPU box): the library runs ncclAllReduce on C_W v itself, and assembly (gather mode),
+    EXACT and BSR products equal the communicator-free context bit for bit."""
+    X, dirs = _setup(4096, 10, 128, 1)
+    kern = dict(family=OC.MATERN_32, rho=1.0)
+    sp = dict(mode=1, tau=1e-3)
+    g = mlk.build_tree(ctx, X, 128, 1, dirs)
+    gb = mlk.build_basis(ctx, g, 2)
+    ref = mlk.assemble_cw(ctx, g, gb, kern, sp)
+    v = wl.vectors(3, gb.dim, seed=8)
+    ye = mlk.cw_matvec(ctx, g, gb, kern, None, mlk.MATVEC_EXACT, v)
+    yb = mlk.cw_matvec(ctx, g, gb, kern, ref, mlk.MATVEC_BSR, v)
+    cc = mlk.Ctx(0, 1, 0, nccl_id=mlk.nccl_unique_id())
+    assert cc.has_comm
+    g2 = mlk.build_tree(cc, X, 128, 1, dirs)
+    b2 = mlk.build_basis(cc, g2, 2)
+    cw2 = mlk.assemble_cw(cc, g2, b2, kern, sp, gather=mlk.GATHER_DEVICE)
+    assert np.array_equal(cw2.export()["values"], ref.export()["values"])
+    cc.reset_stats()
+    cc.set_timing(True)
+    assert np.array_equal(mlk.cw_matvec(cc, g2, b2, kern, None, mlk.MATVEC_EXACT, v), ye)
+    assert np.array_equal(mlk.cw_matvec(cc, g2, b2, kern, cw2, mlk.MATVEC_BSR, v), yb)
+    st = cc.kernel_stats()
+    assert st["nccl_allreduce"]["launches"] == 2
+    cc.set_timing(False)
 
 
 # --------------------------------------------------------------------------------- PCG (NEXT-1)

@@ -3,7 +3,9 @@
 library's LPT partition gives it, packs them with the library's shard plan, all-gathers with
 torch.distributed and sums each block's pieces in chunk order; the result must equal the
 single-process piece sum bit for bit and the oracle blocks to rounding.  The distributed C_W v (row panels of C per rank + allreduce) must match the
-single-process product."""
+single-process product.  The library's chunked all-gather plan (mlk_gather_plan) and the sharded
+BSR product (each rank applies its own pieces and their mirrors, then one allreduce) are run
+the same way."""
 import os
 import socket
 
@@ -80,8 +82,50 @@ def _worker(rank, world, port, q):
             a = full.val_off[k]
             vals[a:a + plen[i]] += g[owner[i] * mx + so[i]: owner[i] * mx + so[i] + plen[i]]
             single[a:a + plen[i]] += piece_val(k, c0)
+        # the library's CHUNKED all-gather plan (mlk_gather_plan, what MLK_GATHER_DEVICE runs over
+        # NCCL): per group one equal-count all-gather of every rank's contiguous shard slice,
+        # then the fixed-order piece sums -- bit-identical to the one-shot gather
+        piece_ptr = np.zeros(len(pairs) + 1, np.int64)
+        for k, _ in pieces:
+            piece_ptr[k + 1] += 1
+        piece_ptr = np.cumsum(piece_ptr)
+        blen = np.diff(full.val_off).astype(np.int64)
+        gptr, glo, gcnt = mlk.gather_plan(piece_ptr, so, owner, blen, world, budget=4 * int(blen.max()))
+        chunked = np.zeros_like(full.values)
+        for gi in range(len(gcnt)):
+            cnt = int(gcnt[gi])
+            send = np.zeros(max(cnt, 1))
+            mylen = max(0, min(cnt, mx - int(glo[gi, rank])))
+            send[:mylen] = shard[glo[gi, rank]:glo[gi, rank] + mylen]
+            rv = torch.zeros(world * max(cnt, 1), dtype=torch.float64)
+            dist.all_gather_into_tensor(rv, torch.from_numpy(send))
+            rv = rv.numpy()
+            for k in range(gptr[gi], gptr[gi + 1]):
+                a = full.val_off[k]
+                for i in range(piece_ptr[k], piece_ptr[k + 1]):
+                    o = owner[i] * max(cnt, 1) + so[i] - glo[gi, owner[i]]
+                    chunked[a:a + plen[i]] += rv[o:o + plen[i]]
+        ok_chunked = np.array_equal(chunked, single) and len(gcnt) > 3
+        # the sharded BSR product (S§8(e)): each rank applies its own pieces and their mirrors
+        # straight from its shard, then one allreduce -- equals the single-rank C~_W v
+        vb = wl.vectors(2, B.dim, seed=6)
+        yb = np.zeros_like(vb)
+        ro = full.row_off
+        pos = {q: i for i, q in enumerate(full.cells)}
+        for i, (k, c0) in enumerate(pieces):
+            if owner[i] != rank:
+                continue
+            r, cc = pos[pairs[k][0]], pos[pairs[k][1]]
+            P = shard[so[i]:so[i] + plen[i]].reshape(ro[r + 1] - ro[r], ro[cc + 1] - ro[cc])
+            yb[:, ro[r]:ro[r + 1]] += vb[:, ro[cc]:ro[cc + 1]] @ P.T
+            if r != cc:
+                yb[:, ro[cc]:ro[cc + 1]] += vb[:, ro[r]:ro[r + 1]] @ P
+        ybt = torch.from_numpy(yb)
+        dist.all_reduce(ybt)
+        yref = OM.cw_matvec_bsr(full, vb)
+        ok_bsr = np.max(np.abs(ybt.numpy() - yref)) <= 1e-12 * np.max(np.abs(yref))
         multi = sum(1 for k in range(len(pairs)) if sum(1 for kk, _ in pieces if kk == k) > 1)
-        ok_gather = (np.array_equal(vals, single) and multi > 0 and
+        ok_gather = (ok_chunked and ok_bsr and np.array_equal(vals, single) and multi > 0 and
                      np.max(np.abs(vals - full.values)) <= 1e-12 * np.max(np.abs(full.values)))
         # distributed exact matvec: rank owns a contiguous range of 32-row tiles of C
         v = wl.vectors(2, B.dim, seed=5)

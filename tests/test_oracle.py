@@ -673,3 +673,35 @@ def test_fastcov_rows_equal_panel_matvec():
     ref = Mv.cov_matvec(X, tr, kern, a, rows=rows)
     got = Fc.cov_rows(X, tr, kern, a, rows)
     assert np.max(np.abs(got - ref)) <= 1e-13 * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg4"])
+def test_full_size_goldens_match_the_sample(name):
+    """tests/golden/blocks_<cfg>.npz holds exactly the expensive blocks of tests/sampling.py's
+    fixed sample (so the GPU test checks what the golden script computed), each with the block
+    shape p_a x p_b of the oracle's cell sizes; matvec_<cfg>.npz holds a y of length n - M."""
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    import sampling
+    inp = wl.make(name)
+    c = inp["cfg"]
+    tr = T.build_tree(inp["X"], c["leaf"], c["tree"], inp["dirs"])
+    gp = os.path.join(GOLD, "pairs_%s.npz" % name)
+    if os.path.exists(gp):
+        pairs = [tuple(int(v) for v in p) for p in np.load(gp)["pairs"]]
+    else:
+        B = Bm.build_basis(inp["X"], tr, c["w"])
+        pairs = A.admitted_pairs(inp["X"], tr, B, c["pairs"], c["tau"])
+    g = np.load(os.path.join(GOLD, "blocks_%s.npz" % name))
+    idx = sampling.select_blocks(name, pairs, tr)
+    need = sampling.golden_needed(pairs, tr, idx)
+    assert list(g["index"]) == need and len(need) >= 1
+    M = math.comb(c["d"] + c["w"], c["w"])
+    p = lambda q: (tr.end[q] - tr.begin[q]) - M if tr.is_leaf[q] else M
+    for k in need:
+        a, b = pairs[k]
+        assert g["k%d" % k].shape == (p(a), p(b))
+    root = [k for k, (a, b) in enumerate(pairs) if a == 0 and b == 0]
+    assert root[0] in need
+    mv = np.load(os.path.join(GOLD, "matvec_%s.npz" % name))
+    assert mv["y_exact"].shape == (c["n"] - M,)
