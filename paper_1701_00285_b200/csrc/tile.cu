@@ -20,6 +20,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <map>
+#include <mutex>
 #include <array>
 #include <string>
 
@@ -184,17 +185,24 @@ __device__ __forceinline__ double corr(double x, const double* tab, const Kernel
   return fma(e, fma(x, 1.0 / 3.0, z), e);                         // (1 + z + z^2/3) e^{-z}
 }
 
+// A/B switches (tools/build_variant.py): occupancy target and stage width of the 2-4 group classes
+#ifndef MLK_MINCTAS_SMALL
+#define MLK_MINCTAS_SMALL 5  // 5 CTAs: cfg3 K5a 250.6 -> 246.3 ms (r02d)
+#endif
+#ifndef MLK_BN_SMALL
+#define MLK_BN_SMALL 40
+#endif
 template <int RQ>
 struct TileCfg {
   // b points per stage.  BN = 8 (mod 16) makes a W row 8 BN doubles = 64 (mod 128) bytes, so
   // the 16-byte B-fragment loads of a quarter-warp (2 rows x 4 chunks) hit distinct banks
   // without any swizzle -- which a 1-D bulk copy could not apply
-  static constexpr int BN = RQ >= 6 ? 24 : (RQ == 1 ? 56 : 40);  // 40 for RQ 6-9 measured 13 % slower on cfg4
+  static constexpr int BN = RQ >= 6 ? 24 : (RQ == 1 ? 56 : MLK_BN_SMALL);  // 40 for RQ 6-9 measured 13 % slower on cfg4
   // maximum stages in the smem ring (the launch uses the deepest ring that keeps the target
   // occupancy, >= 2): the one-group class (C a, tiny cells) has short stages, so it wants a
   // deeper ring to cover the TMA latency
   static constexpr int NST = RQ == 1 ? 6 : (RQ >= 16 ? 2 : 3);
-  static constexpr int MIN_CTAS = RQ >= 20 ? 3 : 4;  // __launch_bounds__ minimum (5 CTAs with 4
+  static constexpr int MIN_CTAS = RQ >= 20 ? 3 : ((RQ == 2 || RQ == 3) ? MLK_MINCTAS_SMALL : 4);  // (5 CTAs with 4
                                                      // held W fragments measured 1.7 % slower)
   static constexpr int G = RQ <= 12 ? RQ : 8;    // W_b fragments held per DMMA group
   static constexpr int NACC = 1;                 // accumulator sets (2 measured no faster)
@@ -206,11 +214,15 @@ __host__ __device__ constexpr int stage_doubles(int rq, int bn, int sdp) {
   return (bn * sdp + (8 * rq + tile_max_nr(rq)) * bn + 15) / 16 * 16;
 }
 
-// Augmented, pre-scaled coordinates (x in tree order, s = kp.scale, u = s x):
+// Augmented, pre-scaled coordinates (x in tree order, s = kp.scale, u = s x), dpa doubles per row.
+// Augmented mode (dk == dpa = pad4(d + 2)):
 //   Pa[i] = [u_i, |u_i|^2, 1, 0...],  Pb[i] = [-2 u_i, 1, |u_i|^2, 0...]
 // so that one DMMA dot product gives Pa[i].Pb[j] = |u_i - u_j|^2 (the Gram identity) directly.
+// Norm mode (dk = pad4(d) < pad4(d + 2), e.g. d = 20: 5 instead of 6 DMMA k-steps; dpa = dk + 4):
+//   Pa[i] = [u_i, 0.., |u_i|^2 at column dk, 0..],  Pb[i] = [-2 u_i, 0.., |u_i|^2 at column dk, 0..]
+// and the kernel starts the Gram accumulator at |u_i|^2 + |u_j|^2 (the DMMA adds -2 u_i.u_j).
 __global__ void k_tile_aug(const double* __restrict__ Xt, int dpt, int d, int64_t n, double s,
-                           double* __restrict__ Pa, double* __restrict__ Pb, int dpa) {
+                           double* __restrict__ Pa, double* __restrict__ Pb, int dpa, int dk) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double* x = Xt + i * dpt;
@@ -223,11 +235,16 @@ __global__ void k_tile_aug(const double* __restrict__ Xt, int dpt, int d, int64_
     pa[k] = u;
     pb[k] = -2.0 * u;
   }
-  pa[d] = nn;
-  pa[d + 1] = 1.0;
-  pb[d] = 1.0;
-  pb[d + 1] = nn;
-  for (int k = d + 2; k < dpa; k++) pa[k] = pb[k] = 0.0;
+  for (int k = d; k < dpa; k++) pa[k] = pb[k] = 0.0;
+  if (dk < dpa) {
+    pa[dk] = nn;
+    pb[dk] = nn;
+  } else {
+    pa[d] = nn;
+    pa[d + 1] = 1.0;
+    pb[d] = 1.0;
+    pb[d + 1] = nn;
+  }
 }
 
 // NV > 0 (with RQ = 1): the contraction has NV <= 4 columns (C a for a few vectors) and is done
@@ -249,7 +266,7 @@ template <int RQ, int FAM, int NV, bool SYM = false>
 __global__ void __launch_bounds__(128, TileCfg<RQ>::MIN_CTAS)
     k_tile_contract(const TileUnit* __restrict__ units, const int32_t* __restrict__ task_range,
                     const int32_t* __restrict__ task_first, int n_units, int* __restrict__ counter,
-                    const double* __restrict__ Pa, const double* __restrict__ Pb, int dpa, int sdp, int nring,
+                    const double* __restrict__ Pa, const double* __restrict__ Pb, int dpa, int dk, int sdp, int nring,
                     KernelParams kp, const CUtensorMap* __restrict__ maps, double* __restrict__ colpart) {
   constexpr int BN = TileCfg<RQ>::BN;
   constexpr int G = TileCfg<RQ>::G;
@@ -275,7 +292,8 @@ __global__ void __launch_bounds__(128, TileCfg<RQ>::MIN_CTAS)
   // stale stage contents are only ever multiplied by zeroed covariances: keep them finite
   for (int e = tid; e < nring * sd; e += 128) St[e] = 0.0;
   fence_proxy_async_smem();
-  const int ks_n = dpa >> 2;
+  const int ks_n = dk >> 2;
+  const bool nmode = dk < dpa;  // norm mode: Gram accumulators start at |u_a|^2 + |u_b|^2
   int gs = 0;  // stages consumed so far by this CTA (ring position and mbarrier phases)
 
   while (true) {
@@ -358,6 +376,7 @@ __global__ void __launch_bounds__(128, TileCfg<RQ>::MIN_CTAS)
 
     const int ar = warp * 8 + (lane >> 2);
     const int64_t ga = a0 + ar;
+    const double na = nmode ? As[ar * sdp + dk] : 0.0;  // |u_a|^2 of the lane's row (norm mode)
     // the lane's row as a local b index (dga) and the CTA's rows' range [dga_lo, dga_hi], clamped
     // to int: b points are local indices 0 .. s_b - 1, so a far-away row never matches
     auto clamp_i = [](int64_t x) { return (int)max((int64_t)INT_MIN / 2, min((int64_t)INT_MAX / 2, x)); };
@@ -371,23 +390,55 @@ __global__ void __launch_bounds__(128, TileCfg<RQ>::MIN_CTAS)
     }
     int slot = slot0;
     unsigned par = par0;
-    for (int s = 0; s < nst; s++) {
-      mbar_wait(&full[slot], par);
-      const double* Xs = St + slot * sd;
-      const double* Ws = Xs + BN * sdp;
-      const int yb = s * BN;                       // first b point of the stage (local index)
-      // 1. augmented Gram: g = |u_a - u_b|^2 for the T sub-tiles (independent chains)
-      double gr[T][2];
+    // 1. Gram: g = |u_a - u_b|^2 for the T sub-tiles of a stage (independent chains); norm mode
+    //    starts the accumulators at |u_a|^2 + |u_b|^2
+    const double* ap = As + ar * sdp + (lane & 3);
+    auto gram = [&](const double* Xs, double (&g)[T][2]) {
+      if (nmode) {
 #pragma unroll
-      for (int t = 0; t < T; t++) gr[t][0] = gr[t][1] = 0.0;
-      const double* ap = As + ar * sdp + (lane & 3);
+        for (int t = 0; t < T; t++) {
+          const double* nb = Xs + (8 * t + 2 * (lane & 3)) * sdp + dk;
+          g[t][0] = na + nb[0];
+          g[t][1] = na + nb[sdp];
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < T; t++) g[t][0] = g[t][1] = 0.0;
+      }
       const double* bp = Xs + (lane >> 2) * sdp + (lane & 3);
 #pragma unroll 4
       for (int ks = 0; ks < ks_n; ks++) {
         const double a = ap[4 * ks];
 #pragma unroll
-        for (int t = 0; t < T; t++) dmma_8x8x4(gr[t][0], gr[t][1], a, bp[8 * t * sdp + 4 * ks]);
+        for (int t = 0; t < T; t++) dmma_8x8x4(g[t][0], g[t][1], a, bp[8 * t * sdp + 4 * ks]);
       }
+    };
+#ifdef MLK_GRAM_PIPE
+    // software pipeline: the Gram DMMAs of stage s + 1 are issued before the evaluation and
+    // contraction of stage s, so the FP64 pipe has independent work while those wait
+    double grn[T][2];
+    if (nst > 0) {
+      mbar_wait(&full[slot], par);
+      gram(St + slot * sd, grn);
+    }
+#endif
+    for (int s = 0; s < nst; s++) {
+      const double* Xs = St + slot * sd;
+      const double* Ws = Xs + BN * sdp;
+      const int yb = s * BN;                       // first b point of the stage (local index)
+      double gr[T][2];
+#ifdef MLK_GRAM_PIPE
+#pragma unroll
+      for (int t = 0; t < T; t++) gr[t][0] = grn[t][0], gr[t][1] = grn[t][1];
+      if (s + 1 < nst) {
+        const int sl1 = slot + 1 == nring ? 0 : slot + 1;
+        mbar_wait(&full[sl1], slot + 1 == nring ? par ^ 1u : par);
+        gram(St + sl1 * sd, grn);
+      }
+#else
+      mbar_wait(&full[slot], par);
+      gram(Xs, gr);
+#endif
       // 2. covariances in registers: closed form, same-site entries exactly 1 + nugget/sigma2,
       //    points past the range exactly 0 (their stage rows are stale)
       // masks only where a stage can need them (warp-uniform tests): the CTA's rows inside the
@@ -599,7 +650,7 @@ __global__ void __launch_bounds__(128, TileCfg<RQ>::MIN_CTAS)
 struct AugArgs {
   const double* Pa;
   const double* Pb;
-  int dpa, sdp;
+  int dpa, dk, sdp;
   const CUtensorMap* maps;
   const int32_t* task_range;  // task -> range (relative to the class), per class
   const int32_t* task_first;  // range -> first task (relative to the class)
@@ -661,32 +712,44 @@ void launch_class(Ctx& c, const AugArgs& ag, const KernelParams& kp, const TileU
   auto fn = k_tile_contract<RQ, FAM, NV, SYM>;
   // ring depth: the deepest ring (<= NST, >= 2) that keeps MIN_CTAS resident CTAs per SM (the
   // stage size grows with d: a fixed depth cut cfg3 / cfg4 to 1-2 CTAs per SM).  Attribute and
-  // occupancy queries are driver round trips: once per instantiation and row stride.
-  static int sdp_set = -1, nring = 0, occ = 0;
-  static size_t smem = 0;
-  if (ag.sdp != sdp_set) {
-    nring = 0;
+  // occupancy queries are driver round trips: once per instantiation, device and row stride
+  // (the dynamic shared-memory attribute is per device), under a lock.
+  struct Cfg {
+    int nring = 0, occ = 0;
+    size_t smem = 0;
+  };
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, Cfg> cache;
+  static std::map<int, size_t> attr;  // per device: the MaxDynamicSharedMemorySize now set
+  std::lock_guard<std::mutex> lock(mu);
+  Cfg& cf = cache[{c.device, ag.sdp}];
+  if (cf.nring == 0) {
     for (int ns = TileCfg<RQ>::NST; ns >= 2; ns--) {
       const size_t sm_ns = sizeof(double) * (size_t)(32 * ag.sdp + ns * stage_doubles(RQ, BN, ag.sdp));
       if (sm_ns > 227 * 1024) continue;
       CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_ns));
+      attr[c.device] = sm_ns;
       int o = 0;
       CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, 128, sm_ns));
-      if (nring == 0 || o > occ) {  // deepest ring at the best occupancy seen
-        nring = ns;
-        occ = o;
-        smem = sm_ns;
+      if (cf.nring == 0 || o > cf.occ) {  // deepest ring at the best occupancy seen
+        cf.nring = ns;
+        cf.occ = o;
+        cf.smem = sm_ns;
       }
       if (o >= TileCfg<RQ>::MIN_CTAS) break;
     }
-    if (nring == 0) throw Error(MLK_ERR_UNSUPPORTED, "tile stages do not fit shared memory");
-    CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    occ = std::max(occ, 1);
-    sdp_set = ag.sdp;
+    if (cf.nring == 0) throw Error(MLK_ERR_UNSUPPORTED, "tile stages do not fit shared memory");
+    cf.occ = std::max(cf.occ, 1);
   }
-  int grid = std::min<int64_t>(n, (int64_t)num_sms(c.device) * occ);
-  fn<<<grid, 128, smem, c.stream>>>(units, ag.task_range, ag.task_first, n, counter, ag.Pa, ag.Pb, ag.dpa, ag.sdp,
-                                    nring, kp, ag.maps, ag.colpart);
+  // the attribute is an upper bound: raise it when this row stride needs more than the last
+  // configuration set on this device (a smaller launch is always allowed)
+  if (attr[c.device] < cf.smem) {
+    CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cf.smem));
+    attr[c.device] = cf.smem;
+  }
+  int grid = std::min<int64_t>(n, (int64_t)num_sms(c.device) * cf.occ);
+  fn<<<grid, 128, cf.smem, c.stream>>>(units, ag.task_range, ag.task_first, n, counter, ag.Pa, ag.Pb, ag.dpa, ag.dk,
+                                       ag.sdp, cf.nring, kp, ag.maps, ag.colpart);
   check_launch("k_tile_contract");
 }
 
@@ -763,7 +826,19 @@ void run_tile_contract(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, s
   // conflicts of the fragment loads when dpa/4 is even
   AugArgs ag;
   ag.colpart = colpart;
-  ag.dpa = pad4(tree->d + 2);
+  // Gram columns: augmented [u, |u|^2, 1] rows when d + 2 pads to the same multiple of 4 as d,
+  // else (d = 3, 4 mod 4, e.g. cfg3's d = 20) the norm mode: one DMMA k-step fewer per sub-tile
+#ifndef MLK_NO_NORM_MODE  // A/B switch (tools/build_variant.py)
+  const bool norm_mode = pad4(tree->d + 2) > pad4(tree->d);
+#else
+  const bool norm_mode = false;
+#endif
+  if (norm_mode) {
+    ag.dk = pad4(tree->d);
+    ag.dpa = ag.dk + 4;
+  } else {
+    ag.dk = ag.dpa = pad4(tree->d + 2);
+  }
   ag.sdp = ((ag.dpa >> 2) & 1) ? ag.dpa : ag.dpa + 4;
   DevBuf<double> aug((size_t)2 * tree->n * ag.dpa, c.stream);
   ag.Pa = aug.p;
@@ -810,7 +885,7 @@ void run_tile_contract(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, s
   TimedLaunch tl(c, name);
   k_tile_aug<<<(unsigned)ceil_div(tree->n, 256), 256, 0, c.stream>>>(tree->Xt.p, tree->d_pad, tree->d, tree->n,
                                                                      kp.scale, aug.p, aug.p + (size_t)tree->n * ag.dpa,
-                                                                     ag.dpa);
+                                                                     ag.dpa, ag.dk);
   check_launch("k_tile_aug");
   for (size_t g = 0; g + 1 < starts.size(); g++) {
     const int s0 = starts[g], nr_ = starts[g + 1] - starts[g];

@@ -57,6 +57,8 @@ constexpr int kTileMaxRQ = 24;
 // 24 padded (286 vs 274 ms, r01g vs r01f: register pressure and the broadcast W loads), so 3
 constexpr int kTileMaxNR = 3;
 constexpr int kTileMaxNRWide = 3;
+// (5 DFMA columns for the two-group class -- cfg3's p = 21 as 16 + 5 instead of 24 padded --
+// measured 3 % slower than the padding on cfg3's K5a, r02c)
 __host__ __device__ constexpr int tile_max_nr(int rq) { return rq <= 4 ? kTileMaxNR : kTileMaxNRWide; }
 // Run all units (any mix of rq classes) on the context stream.  colpart != nullptr selects the
 // symmetric C a kernel (units with rq = -NV; see tile.cu).

@@ -6,7 +6,9 @@ arithmetic of the method.
   cfg2: the root-root block, every admitted block with both cells at level <= 2 (the blocks
         summed from several 4096-row pieces), all leaf self blocks, 24 random admitted pairs.
   cfg3, cfg4: all leaf self blocks, 64 random admitted pairs with |a| |b| <= 2^28, the (0,0)
-        block.
+        block, every admitted block with both cells at level <= 1, and 8 random ancestor blocks
+        whose row cell spans several 4096-row pieces (row cell at depth 3-4 for cfg3, 5 for cfg4;
+        column cell an ancestor at depth >= 1).
 Random draws use numpy.random.default_rng([0, 3]).
 """
 import numpy as np
@@ -37,6 +39,18 @@ def select_blocks(name, pairs, tree):
                 if not (a == b and tree.is_leaf[a]) and size(tree, a) * size(tree, b) <= (1 << 28)
                 and not (a == 0 and b == 0)]
         idx |= set(rng.choice(cand, 64, replace=False).tolist())
+        idx |= {k for k, (a, b) in enumerate(pairs) if depth[a] <= 1 and depth[b] <= 1}
+        rdep = (3, 4) if name == "cfg3" else (5,)
+
+        def is_anc(b, a):
+            while a > 0:
+                a = (a - 1) // 2
+                if a == b:
+                    return True
+            return False
+        multi = [k for k, (a, b) in enumerate(pairs)
+                 if depth[a] in rdep and depth[b] >= 1 and is_anc(b, a) and k not in idx]
+        idx |= set(rng.choice(multi, 8, replace=False).tolist())
     return sorted(int(k) for k in idx)
 
 

@@ -57,8 +57,17 @@ def main(names):
         idx = sampling.select_blocks(name, pairs, tr)
         need = sampling.golden_needed(pairs, tr, idx)
         out = {}
+        # reuse blocks an earlier run of this script already wrote (same pair index and cells)
+        old_path = os.path.join(GOLD, "blocks_%s.npz" % name)
+        old = {}
+        if os.path.exists(old_path):
+            g = np.load(old_path)
+            old = {int(k): (tuple(int(v) for v in p), g["k%d" % k]) for k, p in zip(g["index"], g["pairs"])}
         for k in need:
             a, b = pairs[k]
+            if k in old and old[k][0] == (a, b):
+                out["k%d" % k] = old[k][1]
+                continue
             t1 = time.time()
             out["k%d" % k] = F.block_streamed(X, tr, B, kern, a, b)
             print("  block %d (%d, %d) |a||b| = %.2e: %.0f s" % (k, a, b, sampling.size(tr, a) * sampling.size(tr, b),
@@ -67,6 +76,8 @@ def main(names):
                             pairs=np.array([pairs[k] for k in need], np.int32),
                             source="oracle.fastcov.block_streamed on workloads.make('%s') (seed 0), "
                                    "tools/make_golden_blocks.py" % name, **out)
+        if os.environ.get("GOLDEN_BLOCKS_ONLY"):
+            continue
         # C_W v, EXACT: y = W (C (W^T v)) with C a by row panels of the C tile
         v = wl.vectors(1, B.dim, seed=0)
         t1 = time.time()

@@ -27,6 +27,8 @@ KEYS = [
     "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem", "launch__grid_size",
     "sm__warps_active.avg.pct_of_peak_sustained_active", "dram__bytes_read.sum", "dram__bytes_write.sum",
     "lts__t_bytes.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smsp__inst_executed.sum",
+    "lts__t_sector_hit_rate.pct", "smsp__inst_executed_pipe_fp64.sum", "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum",
+    "sm__sass_thread_inst_executed_op_dmma_pred_on.sum", "smsp__inst_executed_op_shared_ld.sum",
 ]
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
@@ -56,6 +58,13 @@ def launches(path, tag, note, cfg="cfg2"):
     print("\n".join(out[:12]))
 
 
+def _sha():
+    import sys
+    sys.path.insert(0, ROOT)
+    import bench
+    return bench.k5a_source_sha()
+
+
 def k5a(rep, tag, note, cfg="cfg2"):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -78,7 +87,7 @@ def k5a(rep, tag, note, cfg="cfg2"):
     wr = float(m["dram__bytes_write.sum"][1].replace(",", "")) * SCALE[m["dram__bytes_write.sum"][0]]
     json.dump({"what": "dram__bytes_read.sum + dram__bytes_write.sum of one K5a launch (%s), ncu --set full"
                % m["Kernel Name"][1].split("(")[0], "bytes_per_launch": rd + wr, "read": rd, "write": wr,
-               "source": rep + " (" + tag + ")"},
+               "source": os.path.basename(rep) + " (" + tag + ")", "k5a_source_sha": _sha()},
               open(os.path.join(ROOT, "profiles", "k5a_traffic_%s.json" % cfg), "w"), indent=1)
 
 
