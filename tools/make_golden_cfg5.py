@@ -33,12 +33,13 @@ BLOCKS = ((1, 1), (1, 2))
 OUT = os.path.join(ROOT, "tests", "golden", "entries_cfg5.npz")
 
 
-def streamed_basis(X, tr, w, keep):
-    """W of the cells in `keep`, by the oracle's node step, finest level first, dropping every
-    node's Phi / R as soon as its parent has been formed."""
+def streamed_basis(X, tr, w, keep, top=1):
+    """W of the cells in `keep`, by the oracle's node step, finest level first up to depth
+    `top`, dropping every node's Phi / R as soon as its parent has been formed (the root level,
+    which the level-1 blocks do not need, would take ~50 GB of dense NumPy temporaries)."""
     exps = td_exponents(tr.d, w)
     B = OB.Basis(M=len(exps), exps=exps)
-    for dep in range(tr.t, -1, -1):
+    for dep in range(tr.t, top - 1, -1):
         t0 = time.time()
         nodes = [q for q in range(2 ** dep - 1, 2 ** (dep + 1) - 1) if q < tr.n_nodes and tr.exists[q]]
         for q in nodes:
