@@ -411,6 +411,7 @@ def main():
     # one untimed pass for the structure numbers
     tr, B, cw = step(X_d, dirs_d)
     entries, flops, own_flops = cw.entries, cw.flops, cw.own_flops
+    plan = cw.plan()
     sf = cw.stage_flops()
     nnz, dim = cw.nnz, B.dim
     del tr, B, cw
@@ -592,6 +593,8 @@ def main():
             "kernels_ms_per_step": {k: v["ms"] / args.steps for k, v in sorted(stats.items())},
             "api_wall_ms_per_step": api_timed,
             "entries_per_step": entries, "blocks_nnz": nnz,
+            "assembly_plan": {"nested": plan["nested"], "transfer_flops": plan["transfer_flops"],
+                              "k5a_flops": sf["gram"] + sf["contract1"], "k5b_flops": sf["contract2"]},
             "clocks": clocks, "gpu_launches": launches,
             "e2e": {"value": e2e_val, "unit": "covariance pairs/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),

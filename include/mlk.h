@@ -269,6 +269,11 @@ mlk_status mlk_ctx_wait_copies(mlk_ctx ctx);
  * contract1 = the fused tile products V_b = C W_b^T (2 p_b per entry), contract2 = the
  * products W_a V_b[X_a] (2 p_a |X_a| p_b per block). */
 mlk_status mlk_cw_flops(mlk_cw cw, double* gram, double* contract1, double* contract2);
+/* The assembly plan: *nested = 1 if the internal cells' V_b came from the nested evaluation
+ * (leaves' scaling sums + merge-factor transfers; MLK_ASSEMBLY=direct|nested
+ * overrides the cost model), transfer_flops = the FP64 flops of those transfers (all ranks; not
+ * part of mlk_cw_flops' three stages).  Either may be NULL. */
+mlk_status mlk_cw_plan(mlk_cw cw, int32_t* nested, double* transfer_flops);
 /* Owner rank of every block (n_blocks): the rank of its first piece; mlk_cw_matvec BSR with
  * nranks > 1 applies the blocks a rank owns. */
 mlk_status mlk_cw_owner(mlk_cw cw, int32_t* owner);

@@ -91,6 +91,11 @@ struct mlk_basis_s {
   std::vector<int64_t> phi_off;    // node -> offset of Phi block in Phi
   mlk::DevBuf<double> W;           // all W blocks, C_W order, each p x |node| row-major
   mlk::DevBuf<double> Phi;         // all Phi blocks, M x |node| row-major
+  // merge factors: for every internal node q the complete Q (2M x 2M, row-major) of the QR of
+  // [R_L; R_R] at Qm + q_off[q] (Phi_q = Q[:, :M]^T (Phi_L (+) Phi_R), W_q = Q[:, M:]^T (...));
+  // kept when they total <= 1 GB (not cfg5: 29 GB) -- the nested assembly transfers with them
+  mlk::DevBuf<double> Qm;
+  std::vector<int64_t> q_off;      // node -> offset in Qm, or -1
   // the merge levels run asynchronously on the context's auxiliary stream; `ready` marks
   // their completion and consumers wait on it (mlk::basis_wait), checking merge_flag once
   cudaEvent_t ready = nullptr;
@@ -113,7 +118,8 @@ struct mlk_cw_s {
   int64_t shard_len = 0, max_shard_len = 0;
   bool complete = false;           // values hold every block (nranks == 1 or unpacked)
   double entries = 0, flops = 0, own_entries = 0, own_flops = 0;
-  double f_gram = 0, f_c1 = 0, f_c2 = 0;
+  double f_gram = 0, f_c1 = 0, f_c2 = 0, f_tr = 0;  // f_tr: nested-assembly transfers
+  bool nested = false;             // internal cells' V_b by the nested evaluation
   mlk::DevBuf<double> values;      // nnz on the device (nranks == 1: at assembly; else at unpack)
   double* hvals = nullptr;         // MLK_VALUES_HOST: nnz in mapped pinned host memory instead
   double* vals() const { return hvals ? hvals : values.p; }

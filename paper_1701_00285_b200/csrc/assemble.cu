@@ -18,6 +18,8 @@ namespace mlk {
 // n up to 32768 -- a block's pieces are full p_a x p_b partials, so at cfg5 (n = 2^20, M = 1326)
 // 4096-row pieces would hold 464 GB against 184 GB of final values (16384: 221 GB).  A function
 // of n only, so the pieces (and the results) are the same for every rank count.
+// cost-model weight per transfer flop of the nested assembly (K5a entries cost 2 dp + 16 rq + 60)
+constexpr double kTransferW = 2.6;
 int64_t row_chunk(int64_t n) {
   int64_t ch = 4096;
   while (ch < 32768 && (n >> 18) >= 2 * (ch / 4096)) ch *= 2;
@@ -369,11 +371,11 @@ mlk_status mlk_assemble_cw_ex(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const
   // ---- work units (column cell b, row chunk) and pieces (block, row chunk)
   const int64_t CH = row_chunk(tree->n);
   struct Unit {
-    int b;
+    int b;            // the cell contracted first; -1: a nested unit (every internal b, one chunk)
     int64_t chunk;
     std::vector<std::pair<int64_t, int64_t>> rows;  // tree-position ranges inside the chunk
     int64_t nrows = 0;
-    double cost = 0, flops_gram = 0, flops_c1 = 0, flops_c2 = 0;
+    double cost = 0, flops_gram = 0, flops_c1 = 0, flops_c2 = 0, flops_tr = 0;
     int owner = 0;
     int64_t v_off = 0;  // offset of this unit's V rows in the V buffer (doubles)
   };
@@ -385,9 +387,82 @@ mlk_status mlk_assemble_cw_ex(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const
   };
   std::vector<Piece> pieces;
   std::vector<int64_t> piece_ptr(nb + 1, 0);
+  // ---- nested evaluation (DESIGN.md section 6 "Nested assembly"): for every internal b,
+  // V_b = C(X_R, X_b) W_b^T follows from the leaves' scaling sums S_l = C(X_R, X_l) Phi_l^T by the
+  // merge factors of the basis, [S_c | V_c] = [S_cL S_cR] Q_c (W_c = Q_c[:, M:]^T (Phi_cL (+) Phi_cR),
+  // Phi_c = Q_c[:, :M]^T (...), steps (c)-(e) of P:1427-1515), so each covariance entry is
+  // evaluated once per row chunk instead of once per ancestor (and once per extra pair).  Taken
+  // when its cost model beats the direct units of the internal cells (MLK_ASSEMBLY=direct /
+  // nested forces a mode).
+  const int64_t nn = tree->n_nodes;
+  bool nested = false;
+  if (!dd && B->Qm.p && !B->phi_dropped && tree->t >= 1) {
+    const char* env = std::getenv("MLK_ASSEMBLY");
+    const std::string mode = env ? env : "auto";
+    if (mode == "nested") {
+      nested = true;
+    } else if (mode != "direct") {
+      // per-entry K5a cost ~ (2 dp + 16 rq + 60) as in the unit costs below; transfers 8 M^2
+      // flops per (row, internal cell) on the batched GEMM, weighted kTransferW per flop (it ran
+      // at ~40 % of the FP64 peak against K5a's ~70 %: r02f)
+      std::map<int, double> rows_b;
+      std::map<int, std::vector<std::pair<int64_t, int64_t>>> rs;
+      for (int64_t k = 0; k < nb; k++)
+        if (tree->state[Bc[k]] == 0) rs[Bc[k]].push_back({tree->begin[A[k]], tree->end[A[k]]});
+      double direct = 0.0;
+      for (auto& kv : rs) {
+        auto rg = kv.second;
+        rg.push_back({tree->begin[kv.first], tree->end[kv.first]});
+        std::sort(rg.begin(), rg.end());
+        int64_t tot = 0, cur_lo = -1, cur_hi = -1;
+        for (auto& x : rg) {
+          if (x.first <= cur_hi) {
+            cur_hi = std::max(cur_hi, x.second);
+          } else {
+            tot += cur_hi - cur_lo;
+            cur_lo = x.first;
+            cur_hi = x.second;
+          }
+        }
+        tot += cur_hi - cur_lo;
+        const int rq = tile_rq_class(std::min(B->p[kv.first], 8 * kTileMaxRQ));
+        direct += (double)tot * (double)S(kv.first) * (2.0 * dp + 16.0 * rq + 60.0);
+      }
+      int64_t nint = 0;
+      for (int64_t q = 0; q < nn; q++) nint += tree->state[q] == 0;
+      const int rqm = tile_rq_class(std::min(B->M, 8 * kTileMaxRQ));
+      const double nest = (double)tree->n * (double)tree->n * (2.0 * dp + 16.0 * rqm + 60.0) +
+                          kTransferW * (double)tree->n * (double)nint * 8.0 * B->M * B->M;
+      nested = nest < 0.9 * direct;
+    }
+  }
+  cw->nested = nested;
+  std::vector<int> nested_unit;  // chunk -> unit
   if (!dd) {
+    if (nested) {
+      const double n = (double)tree->n;
+      int64_t nint = 0;
+      for (int64_t q = 0; q < nn; q++) nint += tree->state[q] == 0;
+      const int rqm = tile_rq_class(std::min(B->M, 8 * kTileMaxRQ));
+      for (int64_t c0 = 0; c0 * CH < tree->n; c0++) {
+        Unit u;
+        u.b = -1;
+        u.chunk = c0;
+        const int64_t lo = c0 * CH, hi = std::min<int64_t>(tree->n, (c0 + 1) * CH);
+        u.rows.push_back({lo, hi});
+        u.nrows = hi - lo;
+        u.flops_gram = 2.0 * d * (hi - lo) * n;
+        u.flops_c1 = 2.0 * (hi - lo) * n * B->M;
+        u.flops_tr = 8.0 * (hi - lo) * (double)nint * B->M * B->M;
+        u.cost = (hi - lo) * n * (2.0 * dp + 16.0 * rqm + 60.0) + kTransferW * u.flops_tr;
+        nested_unit.push_back((int)units.size());
+        units.push_back(u);
+      }
+    }
+    auto direct_b = [&](int b) { return !nested || tree->state[b] != 0; };
     std::map<int, std::vector<std::pair<int64_t, int64_t>>> rowsets;
-    for (int64_t k = 0; k < nb; k++) rowsets[Bc[k]].push_back({tree->begin[A[k]], tree->end[A[k]]});
+    for (int64_t k = 0; k < nb; k++)
+      if (direct_b(Bc[k])) rowsets[Bc[k]].push_back({tree->begin[A[k]], tree->end[A[k]]});
     for (auto& kv : rowsets) {
       int b = kv.first;
       auto rg = kv.second;
@@ -428,7 +503,7 @@ mlk_status mlk_assemble_cw_ex(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const
     for (int64_t k = 0; k < nb; k++) {
       int a = A[k], b = Bc[k];
       for (int64_t c0 = tree->begin[a] / CH; c0 * CH < tree->end[a]; c0++) {
-        int ui = unit_of.at({b, c0});
+        int ui = direct_b(b) ? unit_of.at({b, c0}) : nested_unit[c0];
         int64_t lo = std::max(tree->begin[a], c0 * CH), hi = std::min(tree->end[a], (c0 + 1) * CH);
         double f = 2.0 * B->p[a] * (double)(hi - lo) * B->p[b];
         units[ui].flops_c2 += f;
@@ -464,10 +539,11 @@ mlk_status mlk_assemble_cw_ex(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const
     for (size_t i = 0; i < units.size(); i++) units[i].owner = own[i];
   }
   for (auto& u : units) {
-    double f = u.flops_gram + u.flops_c1 + u.flops_c2;
+    double f = u.flops_gram + u.flops_c1 + u.flops_c2 + u.flops_tr;
     cw->flops += f;
     cw->f_gram += u.flops_gram;
     cw->f_c1 += u.flops_c1;
+    cw->f_tr += u.flops_tr;
     cw->f_c2 += u.flops_c2;
     if (u.owner == c.rank) {
       cw->own_flops += f;
@@ -531,7 +607,7 @@ mlk_status mlk_assemble_cw_ex(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const
     // own units in batches that bound the V scratch
     std::vector<int> mine;
     for (size_t i = 0; i < units.size(); i++)
-      if (units[i].owner == c.rank) mine.push_back((int)i);
+      if (units[i].owner == c.rank && units[i].b >= 0) mine.push_back((int)i);
     std::vector<std::vector<int64_t>> unit_pieces(units.size());
     for (int64_t i = 0; i < npc; i++)
       if (powner[i] == c.rank) unit_pieces[pieces[i].unit].push_back(i);
@@ -587,6 +663,57 @@ mlk_status mlk_assemble_cw_ex(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const
       gemm_batched(c, gd, "assemble_wa_gemm");
       trace.mark("k5b_launch");
       pos = end;
+    }
+    // nested units, one row chunk at a time: (1) the leaves' scaling sums S_l = C(X_rows, X_l)
+    // Phi_l^T on the fused tile kernel, (2) bottom-up [S_c | V_c] = [S_cL S_cR] Q_c on the batched
+    // GEMM (level by level), (3) the pieces W_a V_b[rows] of every block with an internal b.
+    // S and V hold one M-column slot per heap node (node q at column q M, ld = n_nodes M).
+    if (nested) {
+      const int M = B->M;
+      const int64_t ld = nn * (int64_t)M;
+      DevBuf<double> Sb, Vb;
+      for (size_t ui = 0; ui < units.size(); ui++) {
+        const Unit& u = units[ui];
+        if (u.b >= 0 || u.owner != c.rank) continue;
+        const int64_t lo = u.rows[0].first, rows = u.nrows;
+        if (Sb.n < (size_t)(rows * ld)) {
+          Sb.alloc((size_t)(rows * ld), st);
+          Vb.alloc((size_t)(rows * ld), st);
+        }
+        std::vector<TileUnit> tu;
+        for (int64_t q = 0; q < nn; q++) {
+          if (tree->state[q] != 1) continue;
+          const int32_t sl = (int32_t)S(q);
+          make_tile_units(tu, lo, (int32_t)rows, tree->begin[q], sl, B->Phi.p + B->phi_off[q], sl, M, Sb.p + q * M, ld,
+                          0, dp);
+        }
+        run_tile_contract(c, tree, kp, tu, "assemble_tile_contract");
+        trace.mark("nested_k5a");
+        for (int dep = tree->t - 1; dep >= 0; dep--) {
+          std::vector<GemmDesc> gd;
+          for (int64_t q = (1 << dep) - 1; q < (2 << dep) - 1 && q < nn; q++) {
+            if (tree->state[q] != 0) continue;
+            const double* Sch = Sb.p + (2 * q + 1) * M;  // [S_cL S_cR]: rows x 2M, adjacent slots
+            const double* Q = B->Qm.p + B->q_off[q];      // 2M x 2M row-major
+            if (q > 0) gd.push_back(GemmDesc{Sch, ld, Q, 2 * M, Sb.p + q * M, ld, (int32_t)rows, M, 2 * M, 0});
+            gd.push_back(GemmDesc{Sch, ld, Q + M, 2 * M, Vb.p + q * M, ld, (int32_t)rows, M, 2 * M, 0});
+          }
+          if (!gd.empty()) gemm_batched(c, gd, "assemble_transfer_gemm");
+        }
+        trace.mark("nested_transfer");
+        std::vector<GemmDesc> gd;
+        for (int64_t i = 0; i < npc; i++) {
+          if (pieces[i].unit != (int)ui) continue;
+          const int64_t k = pieces[i].blk;
+          const int a = A[k], b = Bc[k];
+          const int64_t plo = std::max(tree->begin[a], lo), phi = std::min(tree->end[a], lo + rows);
+          GemmDesc g{B->W.p + B->w_off[a] + (plo - tree->begin[a]), S(a), Vb.p + (plo - lo) * ld + (int64_t)b * M, ld,
+                     piece_dst(i), (int64_t)B->p[pairs[k].second], B->p[a], M, (int32_t)(phi - plo), swap[k] ? 1 : 0};
+          gd.push_back(g);
+        }
+        gemm_batched(c, gd, "assemble_wa_gemm");
+        trace.mark("nested_k5b");
+      }
     }
   }
   // piece structure on the device; nranks == 1: reduce the multi-piece blocks now
@@ -709,6 +836,14 @@ mlk_status mlk_cw_flops(mlk_cw cw, double* gram, double* contract1, double* cont
   if (gram) *gram = cw->f_gram;
   if (contract1) *contract1 = cw->f_c1;
   if (contract2) *contract2 = cw->f_c2;
+  MLK_API_END
+}
+
+mlk_status mlk_cw_plan(mlk_cw cw, int32_t* nested, double* transfer_flops) {
+  MLK_API_BEGIN
+  MLK_REQUIRE(cw, "cw is NULL");
+  if (nested) *nested = cw->nested ? 1 : 0;
+  if (transfer_flops) *transfer_flops = cw->f_tr;
   MLK_API_END
 }
 

@@ -16,6 +16,17 @@
 namespace mlk {
 namespace {
 
+// Q (row-major, 2M x 2M) of each job from Q^T (row-major): dst[c][r] = src[r][c]
+__global__ void k_keep_q(const double* __restrict__ qt, const int64_t* __restrict__ dst_off, int m2,
+                         double* __restrict__ qm) {
+  const double* src = qt + (int64_t)blockIdx.y * m2 * m2;
+  double* dst = qm + dst_off[blockIdx.y];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)m2 * m2; e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e / m2), cc = (int)(e - (int64_t)r * m2);
+    dst[(int64_t)cc * m2 + r] = src[e];
+  }
+}
+
 // Index set Lambda(w) of Table multivariate:table1 as factor lists (coordinate
 // indices, nondecreasing; a monomial is the left-to-right product of its factors), in graded
 // order (R8): total degree, then the factor lists lexicographically -- combinations with
@@ -970,6 +981,23 @@ mlk_status mlk_build_basis_ex(mlk_ctx ctx, mlk_tree tree, int32_t index_set, int
     for (auto& lb : lvlphi) lb.alloc((size_t)std::max<int64_t>(mn, 1), st);
   DevBuf<double> Qt(0, st);
   DevBuf<double> Ast(0, st);
+  // keep the merge Q factors for the nested assembly when they are small (cfg2-4: 7-43 MB)
+  {
+    int64_t nint = 0;
+    for (int q = 0; q < nn; q++)
+      if (tree->state[q] == 0) nint++;
+    const int64_t qbytes = nint * 4 * (int64_t)M * M * (int64_t)sizeof(double);
+    B->q_off.assign(nn, -1);
+    if (nint > 0 && qbytes <= ((int64_t)1 << 30)) {
+      B->Qm.alloc((size_t)nint * 4 * M * M, st);
+      int64_t o = 0;
+      for (int q = 0; q < nn; q++)
+        if (tree->state[q] == 0) {
+          B->q_off[q] = o;
+          o += 4 * (int64_t)M * M;
+        }
+    }
+  }
   // cells of a level in groups whose stacked matrices and Q^T (6 M^2 doubles per cell) fit a
   // quarter of the scratch budget (cfg5: 84 MB per cell; a whole level of 256 took 22 GB)
   const int64_t per_cell = 6 * (int64_t)M * M * (int64_t)sizeof(double);
@@ -1006,6 +1034,14 @@ mlk_status mlk_build_basis_ex(mlk_ctx ctx, mlk_tree tree, int32_t index_set, int
       trace.mark("lvl_stack");
       run_qr(c, qj, M, B->merge_flag.p, "basis_merge_qr");
       trace.mark("lvl_qr");
+      if (B->Qm.p) {
+        std::vector<int64_t> qo(nc);
+        for (size_t i = 0; i < nc; i++) qo[i] = B->q_off[cellsq[i]];
+        DevBuf<int64_t> qo_d(nc, st);
+        qo_d.upload(qo);
+        k_keep_q<<<dim3(8, (unsigned)nc), 256, 0, st>>>(Qt.p, qo_d.p, 2 * M, B->Qm.p);
+        check_launch("k_keep_q");
+      }
       // Phi_q / W_q = (Q^T)[rows, cols of child] x Phi_child
       std::vector<GemmDesc> gd;
       for (size_t i = 0; i < nc; i++) {
@@ -1048,6 +1084,7 @@ void mlk_basis_free(mlk_basis basis) {
   cudaDeviceSynchronize();
   basis->W.s = nullptr;
   basis->Phi.s = nullptr;
+  basis->Qm.s = nullptr;
   basis->merge_flag.s = nullptr;
   if (basis->ready) cudaEventDestroy(basis->ready);
   delete basis;

@@ -413,32 +413,13 @@ __global__ void __launch_bounds__(128, TileCfg<RQ>::MIN_CTAS)
         for (int t = 0; t < T; t++) dmma_8x8x4(g[t][0], g[t][1], a, bp[8 * t * sdp + 4 * ks]);
       }
     };
-#ifdef MLK_GRAM_PIPE
-    // software pipeline: the Gram DMMAs of stage s + 1 are issued before the evaluation and
-    // contraction of stage s, so the FP64 pipe has independent work while those wait
-    double grn[T][2];
-    if (nst > 0) {
-      mbar_wait(&full[slot], par);
-      gram(St + slot * sd, grn);
-    }
-#endif
     for (int s = 0; s < nst; s++) {
       const double* Xs = St + slot * sd;
       const double* Ws = Xs + BN * sdp;
       const int yb = s * BN;                       // first b point of the stage (local index)
       double gr[T][2];
-#ifdef MLK_GRAM_PIPE
-#pragma unroll
-      for (int t = 0; t < T; t++) gr[t][0] = grn[t][0], gr[t][1] = grn[t][1];
-      if (s + 1 < nst) {
-        const int sl1 = slot + 1 == nring ? 0 : slot + 1;
-        mbar_wait(&full[sl1], slot + 1 == nring ? par ^ 1u : par);
-        gram(St + sl1 * sd, grn);
-      }
-#else
       mbar_wait(&full[slot], par);
       gram(Xs, gr);
-#endif
       // 2. covariances in registers: closed form, same-site entries exactly 1 + nugget/sigma2,
       //    points past the range exactly 0 (their stage rows are stale)
       // masks only where a stage can need them (warp-uniform tests): the CTA's rows inside the

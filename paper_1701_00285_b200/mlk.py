@@ -41,7 +41,7 @@ SYMBOLS = [
     "mlk_cw_unpack", "mlk_cw_values_device", "mlk_cov_matvec", "mlk_cw_matvec", "mlk_partition_lpt",
     "mlk_shard_plan", "mlk_launch_count", "mlk_cw_flops", "mlk_cw_export_async", "mlk_ctx_wait_copies",
     "mlk_pcg_solve", "mlk_build_basis_ex", "mlk_assemble_cw_ex", "mlk_cw_export_pieces", "mlk_loglik",
-    "mlk_nccl_unique_id", "mlk_gather_plan",
+    "mlk_nccl_unique_id", "mlk_gather_plan", "mlk_cw_plan",
 ]
 
 
@@ -113,6 +113,7 @@ _sig = {
     "mlk_shard_plan": (C.c_int, [P, P, C.c_int64, C.c_int32, P, P]),
     "mlk_launch_count": (C.c_int64, []),
     "mlk_cw_flops": (C.c_int, [P, P, P, P]),
+    "mlk_cw_plan": (C.c_int, [P, P, P]),
     "mlk_cw_export_async": (C.c_int, [P, P, P]),
     "mlk_ctx_wait_copies": (C.c_int, [P]),
     "mlk_pcg_solve": (C.c_int, [P, P, P, C.POINTER(KernelSpec), P, C.c_int32, P, P, C.c_double, C.c_int32,
@@ -405,6 +406,12 @@ class CW:
         g, a, b = C.c_double(), C.c_double(), C.c_double()
         _check(_lib.mlk_cw_flops(self.h, C.byref(g), C.byref(a), C.byref(b)))
         return dict(gram=g.value, contract1=a.value, contract2=b.value)
+
+    def plan(self):
+        """dict(nested, transfer_flops) of mlk_cw_plan."""
+        nst, tf = C.c_int32(), C.c_double()
+        _check(_lib.mlk_cw_plan(self.h, C.byref(nst), C.byref(tf)))
+        return dict(nested=bool(nst.value), transfer_flops=tf.value)
 
     def owner(self):
         o = np.empty(self.n_blocks, np.int32)

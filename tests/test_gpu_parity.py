@@ -197,6 +197,46 @@ def test_assembly_fp64_parity(mlk, ctx, fam, rho, n, d, w, leaf, kind, mode, tau
     assert errs.max() <= TOL_BLOCK, (errs.max(), int(errs.argmax()))
 
 
+@pytest.mark.parametrize("mode", ["nested", "direct"])
+@pytest.mark.parametrize("n,d,w,leaf,kind,fam,rho,mode_pairs,tau,points", [
+    (4096, 10, 2, 128, 1, OC.MATERN_32, 1.0, 1, 1e-3, "uniform"),   # cfg2 shape, tau pattern
+    (8192, 50, 1, 512, 1, OC.MATERN_12, 3.0, 1, 1e-7, "mixture"),   # cfg4 shape
+    (8192, 20, 1, 256, 1, OC.MATERN_52, 2.0, 0, 0.0, "normal"),     # cfg3 shape, all pairs
+    (1000, 3, 1, 40, 0, OC.GAUSSIAN, 1.5, 1, 0.05, "normal"),       # ragged kD tree
+    (1024, 2, 2, 32, 0, OC.MATERN_12, 0.5, 0, 0.0, "uniform"),      # cfg1 shape (R23 bound)
+])
+def test_nested_and_direct_assembly(mlk, ctx, monkeypatch, mode, n, d, w, leaf, kind, fam, rho, mode_pairs, tau,
+                                    points):
+    """Both assembly plans against the oracle: 'direct' (V_b = C(X_R, X_b) W_b^T on the fused
+    tile kernel for every b) and 'nested' (the internal cells' V_b from the leaves' scaling sums
+    S_l = C(X_R, X_l) Phi_l^T and the merge factors, [S_c | V_c] = [S_cL S_cR] Q_c).  Per block
+    <= 1e-11 relative (cfg1's shape, whose blocks sit at the FP64 floor, to 1e-13 of
+    |W_a| |C_ab| |W_b| as in reading R23)."""
+    monkeypatch.setenv("MLK_ASSEMBLY", mode)
+    X, dirs = _setup(n, d, leaf, kind, points)
+    g, o = _tree_both(mlk, ctx, X, leaf, kind, dirs)
+    gb = mlk.build_basis(ctx, g, w)
+    ob = OB.build_basis(X, o, w)
+    kern = dict(family=fam, rho=rho, sigma2=1.1, nugget=1e-4 if fam == OC.GAUSSIAN else 0.0)
+    pairs = OA.admitted_pairs(X, o, ob, mode_pairs, tau)
+    ref = OAs.assemble(X, o, ob, kern, pairs)
+    cw = mlk.assemble_cw(ctx, g, gb, kern, dict(mode=mode_pairs, tau=tau))
+    assert cw.plan()["nested"] == (mode == "nested")
+    got = cw.export()
+    assert np.array_equal(got["val_off"], ref.val_off)
+    if d == 2:
+        for k, (a, b) in enumerate(pairs):
+            lo, hi = ref.val_off[k], ref.val_off[k + 1]
+            ia = o.perm[o.begin[a]:o.end[a]]
+            ib = o.perm[o.begin[b]:o.end[b]]
+            Cab = OC.cov(X[ia], X[ib], ia, ib, kern["family"], kern["rho"], kern["sigma2"], kern["nugget"])
+            scale = np.linalg.norm(ob.W[a]) * np.linalg.norm(Cab) * np.linalg.norm(ob.W[b])
+            assert np.linalg.norm(got["values"][lo:hi] - ref.values[lo:hi]) <= 1e-13 * scale
+    else:
+        errs = _block_errs(got["values"], ref)
+        assert errs.max() <= TOL_BLOCK, (errs.max(), int(errs.argmax()))
+
+
 def test_assembly_cfg4_shape_parity(mlk, ctx):
     X, dirs = _setup(8192, 50, 512, 1, "mixture")
     g, o = _tree_both(mlk, ctx, X, 512, 1, dirs)
