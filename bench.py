@@ -546,11 +546,23 @@ def main():
 
     if rank == 0:
         peak = fp64_peak()
-        k5 = stats.get("assemble_tile_contract", {"ms": float("nan"), "launches": 1})
+        # K5a = the fused tile kernel, both its assembly uses: the nested plan's leaf pass
+        # ("assemble_tile_nested") and the direct units ("assemble_tile_contract")
+        own = own_flops / flops if flops > 0 else 1.0
+        kd = stats.get("assemble_tile_contract", {"ms": 0.0, "launches": 0})
+        kn = stats.get("assemble_tile_nested", {"ms": 0.0, "launches": 0})
+        k5 = {"ms": kd["ms"] + kn["ms"], "launches": kd["launches"] + kn["launches"]}
         k5_ms_per_step = k5["ms"] / args.steps
         # this rank's share of the K5a flops (its LPT units; the whole job when ws == 1)
-        k5_flops = (sf["gram"] + sf["contract1"]) * (own_flops / flops if flops > 0 else 1.0)
+        k5_flops = (sf["gram"] + sf["contract1"]) * own
         achieved = k5_flops / (k5_ms_per_step * 1e-3) / 1e12
+        nf = plan["nested_tile_flops"] * own
+        k5_split = {"nested_leaf_pass": {"ms_per_step": kn["ms"] / args.steps, "flops": nf,
+                                         "frac": (nf / (kn["ms"] / args.steps * 1e-3) / 1e12 / fp64_peak())
+                                         if kn["ms"] > 0 else None},
+                    "direct_units": {"ms_per_step": kd["ms"] / args.steps, "flops": k5_flops - nf,
+                                     "frac": ((k5_flops - nf) / (kd["ms"] / args.steps * 1e-3) / 1e12 / fp64_peak())
+                                     if kd["ms"] > 0 else None}}
         traffic, traffic_src = None, "no ncu capture for this config"
         if os.path.exists(TRAFFIC_FILE % args.config):
             tj = json.load(open(TRAFFIC_FILE % args.config))
@@ -561,7 +573,8 @@ def main():
             else:
                 traffic_src = "stale: %s was captured on other K5a sources" % os.path.basename(TRAFFIC_FILE % args.config)
         asm_ms = sum(stats.get(k, {"ms": 0.0})["ms"] for k in
-                     ("search", "assemble_tile_contract", "assemble_wa_gemm")) / args.steps
+                     ("search", "assemble_tile_contract", "assemble_tile_nested", "assemble_transfer",
+                      "assemble_transfer_gemm", "assemble_wa_gemm")) / args.steps
         cpu = None
         if not args.no_cpu_baseline and ws == 1:
             if wl.CONFIGS[args.config].get("index_set", 0):
@@ -582,18 +595,19 @@ def main():
                      "tflops_assembly": flops / (asm_ms * 1e-3) / 1e12 if asm_ms > 0 else None,
                      "pct_of_peak_step": 100.0 * flops / (ms_per_step * 1e-3) / 1e12 / peak,
                      "peak_tflops": peak, "peak_source": "measured, profiles/fp64_peak_r01.json (DMMA loop)"},
-            "roofline": {"kernel": "assemble_tile_contract (K5a)", "bound": "tensor",
+            "roofline": {"kernel": "k_tile_contract (K5a: assemble_tile_nested + assemble_tile_contract)", "bound": "tensor",
                          "peak_source": "of measured: FP64 DMMA loop on this pool's B200 (tools/fp64_peak.cu, "
                                         "profiles/fp64_peak_r01.json; MEASURED_PEAKS.json holds bf16/HBM only)",
                          "pipe": "FP64 DMMA.8x8x4 (shares the FP64 pipe with DFMA, DESIGN.md section 6)", "achieved": achieved,
                          "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                          "traffic_source": traffic_src,
-                         "launches_per_step": k5["launches"] / args.steps,
+                         "launches_per_step": k5["launches"] / args.steps, "split": k5_split,
                          "algorithmic_flops_per_step": k5_flops, "ms_per_step": k5_ms_per_step},
             "kernels_ms_per_step": {k: v["ms"] / args.steps for k, v in sorted(stats.items())},
             "api_wall_ms_per_step": api_timed,
             "entries_per_step": entries, "blocks_nnz": nnz,
             "assembly_plan": {"nested": plan["nested"], "transfer_flops": plan["transfer_flops"],
+                              "nested_tile_flops": plan["nested_tile_flops"],
                               "k5a_flops": sf["gram"] + sf["contract1"], "k5b_flops": sf["contract2"]},
             "clocks": clocks, "gpu_launches": launches,
             "e2e": {"value": e2e_val, "unit": "covariance pairs/s", "h2d_bytes_per_step": int(h2d),

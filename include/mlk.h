@@ -222,10 +222,13 @@ typedef enum { MLK_GATHER_NONE = 0, MLK_GATHER_DEVICE = 1, MLK_GATHER_HOST = 2 }
  *  block rows/cols = cells in C_W order; each admitted unordered pair is stored once as
  *  (row, col) with row <= col in C_W order, row-major p_row x p_col, blocks sorted by
  *  (row, col).  Every block is computed exactly (no approximation inside a block).
- * Work decomposition: for each block one cell b is contracted
- * first; V_b = C(X_R, X_b) W_b^T is formed once for the union R of the row points of all
- * blocks sharing b (for ancestor pairs R = X_b itself), in work units of <= 4096 rows; a
- * block is W_a V_b[X_a], summed over the 4096-row chunks ("pieces") of X_a in chunk order.
+ * Work decomposition ("Nested assembly"): for each block one
+ * cell b is contracted first; V_b = C(X_R, X_b) W_b^T is formed once for the union R of the
+ * row points of all blocks sharing b (for ancestor pairs R = X_b itself), in work units of
+ * <= 4096 rows, either directly on the fused tile kernel or -- the nested plan, for every
+ * internal b at once -- from the leaves' scaling sums C(X_R, X_l) Phi_l^T and the merge factors
+ * of the basis; a block is W_a V_b[X_a], summed over the 4096-row chunks ("pieces") of X_a in
+ * chunk order (mlk_cw_plan reports the plan; MLK_ASSEMBLY=direct|nested overrides it).
  * With nranks > 1 the units are LPT-partitioned over ranks, each rank writes the pieces of
  * its units into its shard, and `gather` (mlk_gather) decides how the shards are combined.
  * Results are bit-identical for every nranks.
@@ -272,8 +275,10 @@ mlk_status mlk_cw_flops(mlk_cw cw, double* gram, double* contract1, double* cont
 /* The assembly plan: *nested = 1 if the internal cells' V_b came from the nested evaluation
  * (leaves' scaling sums + merge-factor transfers; MLK_ASSEMBLY=direct|nested
  * overrides the cost model), transfer_flops = the FP64 flops of those transfers (all ranks; not
- * part of mlk_cw_flops' three stages).  Either may be NULL. */
-mlk_status mlk_cw_plan(mlk_cw cw, int32_t* nested, double* transfer_flops);
+ * part of mlk_cw_flops' three stages), nested_tile_flops = the part of mlk_cw_flops' gram +
+ * contract1 done by the nested leaf pass (kernel timing name "assemble_tile_nested"; the rest is
+ * the direct units, "assemble_tile_contract").  Any output may be NULL. */
+mlk_status mlk_cw_plan(mlk_cw cw, int32_t* nested, double* transfer_flops, double* nested_tile_flops);
 /* Owner rank of every block (n_blocks): the rank of its first piece; mlk_cw_matvec BSR with
  * nranks > 1 applies the blocks a rank owns. */
 mlk_status mlk_cw_owner(mlk_cw cw, int32_t* owner);

@@ -1,5 +1,8 @@
 // Handle types shared by the translation units of libmlk, and the ABI try/catch wrapper.
 #pragma once
+#include <array>
+#include <map>
+#include <mutex>
 #include <new>
 
 #include "common.cuh"
@@ -119,6 +122,7 @@ struct mlk_cw_s {
   bool complete = false;           // values hold every block (nranks == 1 or unpacked)
   double entries = 0, flops = 0, own_entries = 0, own_flops = 0;
   double f_gram = 0, f_c1 = 0, f_c2 = 0, f_tr = 0;  // f_tr: nested-assembly transfers
+  double f_nested_k5a = 0;         // Gram + first contraction of the nested leaf pass (in f_gram, f_c1)
   bool nested = false;             // internal cells' V_b by the nested evaluation
   mlk::DevBuf<double> values;      // nnz on the device (nranks == 1: at assembly; else at unpack)
   double* hvals = nullptr;         // MLK_VALUES_HOST: nnz in mapped pinned host memory instead
@@ -132,6 +136,12 @@ struct mlk_cw_s {
 };
 
 namespace mlk {
+// nested-assembly transfers of one tree level (nested.cu): jobs {[S_cL S_cR], Q_c, S_c (or
+// nullptr), V_c}, rows x (n_nodes M) buffers with row stride ld, and per job a device flag per
+// 64-row block (V_c needed there; nullptr: everywhere); transfer_kernel_ok(M): 2M <= 144
+bool transfer_kernel_ok(int M);
+void transfer_level(Ctx& c, const std::vector<std::array<const double*, 4>>& jobs,
+                    const std::vector<const uint8_t*>& vflags, int M, int64_t rows, int64_t ld);
 // all-gather of the piece shards into the values (nranks > 1, library communicator; comm.cu)
 void gather_values(Ctx& c, mlk_cw_s* cw, const double* full);
 void gather_plan(int64_t nb, const int64_t* piece_ptr, const int64_t* piece_off, const int32_t* piece_owner,

@@ -18,8 +18,12 @@ namespace mlk {
 // n up to 32768 -- a block's pieces are full p_a x p_b partials, so at cfg5 (n = 2^20, M = 1326)
 // 4096-row pieces would hold 464 GB against 184 GB of final values (16384: 221 GB).  A function
 // of n only, so the pieces (and the results) are the same for every rank count.
-// cost-model weight per transfer flop of the nested assembly (K5a entries cost 2 dp + 16 rq + 60)
-constexpr double kTransferW = 2.6;
+// cost model of the nested assembly against the direct units (K5a entries cost 2 dp + 16 rq + 60
+// "units"): the nested leaf pass runs K5a ~15 % below the direct units' efficiency (shorter
+// b streams, r02i), a transfer flop costs kTransferW units (the transfer kernel ran at 11-21
+// TFLOP/s against K5a's 26-28, r02i)
+constexpr double kNestedK5aW = 1.15;
+constexpr double kTransferW = 3.5;
 int64_t row_chunk(int64_t n) {
   int64_t ch = 4096;
   while (ch < 32768 && (n >> 18) >= 2 * (ch / 4096)) ch *= 2;
@@ -264,6 +268,20 @@ __global__ void k_reduce_pieces(const int32_t* __restrict__ blocks, const int64_
   }
 }
 
+// the leaves' Phi blocks (M x s_l each, at their phi offsets) as one M x n row-major matrix:
+// column j = Phi_leaf(j)[:, j - begin(leaf)]
+__global__ void k_phi_all(const double* __restrict__ Phi, const int64_t* __restrict__ off,
+                          const int64_t* __restrict__ beg, const int32_t* __restrict__ sz, int M, int64_t n,
+                          double* __restrict__ out) {
+  const int l = blockIdx.y;
+  const int64_t s = sz[l];
+  const double* src = Phi + off[l];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < s * M; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = e / s, x = e - m * s;
+    out[m * n + beg[l] + x] = src[e];
+  }
+}
+
 }  // namespace
 
 void reduce_pieces(Ctx& c, mlk_cw_s* cw, const double* gathered) {
@@ -431,15 +449,49 @@ mlk_status mlk_assemble_cw_ex(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const
       int64_t nint = 0;
       for (int64_t q = 0; q < nn; q++) nint += tree->state[q] == 0;
       const int rqm = tile_rq_class(std::min(B->M, 8 * kTileMaxRQ));
-      const double nest = (double)tree->n * (double)tree->n * (2.0 * dp + 16.0 * rqm + 60.0) +
-                          kTransferW * (double)tree->n * (double)nint * 8.0 * B->M * B->M;
+      // transfers: the S half (4 M^2 per row and internal cell) for every row, the V half only
+      // for the rows of c's blocks (the same row sets the direct units would have evaluated)
+      double vrows = 0.0;
+      for (auto& kv : rs) {
+        auto rg = kv.second;
+        rg.push_back({tree->begin[kv.first], tree->end[kv.first]});
+        std::sort(rg.begin(), rg.end());
+        int64_t tot = 0, cur_lo = -1, cur_hi = -1;
+        for (auto& x : rg) {
+          if (x.first <= cur_hi) {
+            cur_hi = std::max(cur_hi, x.second);
+          } else {
+            tot += cur_hi - cur_lo;
+            cur_lo = x.first;
+            cur_hi = x.second;
+          }
+        }
+        vrows += (double)(tot + cur_hi - cur_lo);
+      }
+      const double nest = kNestedK5aW * (double)tree->n * (double)tree->n * (2.0 * dp + 16.0 * rqm + 60.0) +
+                          kTransferW * 4.0 * B->M * B->M * ((double)tree->n * (double)nint + vrows);
       nested = nest < 0.9 * direct;
     }
   }
   cw->nested = nested;
   std::vector<int> nested_unit;  // chunk -> unit
+  std::map<int, std::vector<std::pair<int64_t, int64_t>>> nested_rows;  // internal c -> row ranges R_c
   if (!dd) {
     if (nested) {
+      // the rows R_c whose V_c some block uses (X_c and the row cells of c's blocks), merged
+      for (int64_t k = 0; k < nb; k++)
+        if (tree->state[Bc[k]] == 0) nested_rows[Bc[k]].push_back({tree->begin[A[k]], tree->end[A[k]]});
+      for (auto& kv : nested_rows) {
+        auto& rg = kv.second;
+        rg.push_back({tree->begin[kv.first], tree->end[kv.first]});
+        std::sort(rg.begin(), rg.end());
+        std::vector<std::pair<int64_t, int64_t>> merged;
+        for (auto& x : rg) {
+          if (!merged.empty() && x.first <= merged.back().second) merged.back().second = std::max(merged.back().second, x.second);
+          else merged.push_back(x);
+        }
+        rg = merged;
+      }
       const double n = (double)tree->n;
       int64_t nint = 0;
       for (int64_t q = 0; q < nn; q++) nint += tree->state[q] == 0;
@@ -453,8 +505,13 @@ mlk_status mlk_assemble_cw_ex(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const
         u.nrows = hi - lo;
         u.flops_gram = 2.0 * d * (hi - lo) * n;
         u.flops_c1 = 2.0 * (hi - lo) * n * B->M;
-        u.flops_tr = 8.0 * (hi - lo) * (double)nint * B->M * B->M;
-        u.cost = (hi - lo) * n * (2.0 * dp + 16.0 * rqm + 60.0) + kTransferW * u.flops_tr;
+        // transfers: the S half for every row and internal cell (not the root), the V half for
+        // the rows of R_c in this chunk
+        double vr = 0.0;
+        for (auto& kv : nested_rows)
+          for (auto& rg : kv.second) vr += (double)std::max<int64_t>(0, std::min(rg.second, hi) - std::max(rg.first, lo));
+        u.flops_tr = 4.0 * B->M * B->M * ((double)(hi - lo) * (double)(nint - 1) + vr);
+        u.cost = kNestedK5aW * (hi - lo) * n * (2.0 * dp + 16.0 * rqm + 60.0) + kTransferW * u.flops_tr;
         nested_unit.push_back((int)units.size());
         units.push_back(u);
       }
@@ -544,6 +601,7 @@ mlk_status mlk_assemble_cw_ex(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const
     cw->f_gram += u.flops_gram;
     cw->f_c1 += u.flops_c1;
     cw->f_tr += u.flops_tr;
+    if (u.b < 0) cw->f_nested_k5a += u.flops_gram + u.flops_c1;
     cw->f_c2 += u.flops_c2;
     if (u.owner == c.rank) {
       cw->own_flops += f;
@@ -672,6 +730,37 @@ mlk_status mlk_assemble_cw_ex(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const
       const int M = B->M;
       const int64_t ld = nn * (int64_t)M;
       DevBuf<double> Sb, Vb;
+      // leaf runs streamed by one unit each (segmented K5a: consecutive heap indices, equal sizes
+      // that are multiples of 8, consecutive point ranges), G leaves per unit so a row chunk
+      // still spreads over >= 4 x 148 x 4 tasks; the others one unit per leaf
+      std::vector<int> leaves;
+      for (int64_t q = 0; q < nn; q++)
+        if (tree->state[q] == 1) leaves.push_back((int)q);
+      std::sort(leaves.begin(), leaves.end(), [&](int x, int y) { return tree->begin[x] < tree->begin[y]; });
+      DevBuf<double> phi_all;
+      bool seg_ok = !leaves.empty();
+      for (size_t i = 0; i < leaves.size() && seg_ok; i++) {
+        seg_ok = S(leaves[i]) == S(leaves[0]) && S(leaves[0]) % 8 == 0 &&
+                 (i == 0 || (leaves[i] == leaves[i - 1] + 1 && tree->begin[leaves[i]] == tree->end[leaves[i - 1]]));
+      }
+      if (seg_ok) {
+        phi_all.alloc((size_t)M * tree->n, st);
+        std::vector<int64_t> off, beg;
+        std::vector<int32_t> sz;
+        for (int q : leaves) {
+          off.push_back(B->phi_off[q]);
+          beg.push_back(tree->begin[q]);
+          sz.push_back((int32_t)S(q));
+        }
+        DevBuf<int64_t> off_d(off.size(), st), beg_d(beg.size(), st);
+        DevBuf<int32_t> sz_d(sz.size(), st);
+        off_d.upload(off);
+        beg_d.upload(beg);
+        sz_d.upload(sz);
+        k_phi_all<<<dim3(8, (unsigned)leaves.size()), 256, 0, st>>>(B->Phi.p, off_d.p, beg_d.p, sz_d.p, M, tree->n,
+                                                                    phi_all.p);
+        check_launch("k_phi_all");
+      }
       for (size_t ui = 0; ui < units.size(); ui++) {
         const Unit& u = units[ui];
         if (u.b >= 0 || u.owner != c.rank) continue;
@@ -681,23 +770,67 @@ mlk_status mlk_assemble_cw_ex(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const
           Vb.alloc((size_t)(rows * ld), st);
         }
         std::vector<TileUnit> tu;
-        for (int64_t q = 0; q < nn; q++) {
-          if (tree->state[q] != 1) continue;
-          const int32_t sl = (int32_t)S(q);
-          make_tile_units(tu, lo, (int32_t)rows, tree->begin[q], sl, B->Phi.p + B->phi_off[q], sl, M, Sb.p + q * M, ld,
-                          0, dp);
+        if (seg_ok) {
+          const int64_t want = (int64_t)4 * num_sms(c.device) * 4;
+          int64_t G = 1;
+          while (2 * G <= (int64_t)leaves.size() && ceil_div(rows, 32) * ((int64_t)leaves.size() / (2 * G)) >= want)
+            G *= 2;
+          const int32_t sl = (int32_t)S(leaves[0]);
+          for (size_t i = 0; i < leaves.size(); i += (size_t)G) {
+            const int nl = (int)std::min<int64_t>(G, (int64_t)leaves.size() - (int64_t)i);
+            const int64_t b0 = tree->begin[leaves[i]];
+            const size_t first = tu.size();
+            make_tile_units(tu, lo, (int32_t)rows, b0, sl * nl, phi_all.p + b0, tree->n, M, Sb.p + leaves[i] * M, ld,
+                            0, dp);
+            for (size_t j = first; j < tu.size(); j++) {
+              tu[j].seg = sl;
+              tu[j].seg_off = M;
+              tu[j].w_cols = tree->n - b0;
+            }
+          }
+        } else {
+          for (int q : leaves) {
+            const int32_t sl = (int32_t)S(q);
+            make_tile_units(tu, lo, (int32_t)rows, tree->begin[q], sl, B->Phi.p + B->phi_off[q], sl, M, Sb.p + q * M,
+                            ld, 0, dp);
+          }
         }
-        run_tile_contract(c, tree, kp, tu, "assemble_tile_contract");
+        run_tile_contract(c, tree, kp, tu, "assemble_tile_nested");
         trace.mark("nested_k5a");
+        // per internal cell and 64-row block of the chunk: does some row of it need V_c?
+        const int64_t nblk = ceil_div(rows, 64);
+        std::vector<uint8_t> vflag;
+        std::vector<int64_t> vflag_off(nn, -1);
+        for (int64_t q = 0; q < nn; q++) {
+          if (tree->state[q] != 0) continue;
+          vflag_off[q] = (int64_t)vflag.size();
+          vflag.resize(vflag.size() + nblk, 0);
+          auto it = nested_rows.find((int)q);
+          if (it == nested_rows.end()) continue;
+          for (auto& rg : it->second) {
+            const int64_t a0 = std::max(rg.first, lo), a1 = std::min(rg.second, lo + rows);
+            for (int64_t bk = (a0 - lo) / 64; a0 < a1 && bk <= (a1 - 1 - lo) / 64; bk++) vflag[vflag_off[q] + bk] = 1;
+          }
+        }
+        DevBuf<uint8_t> vflag_d(std::max<size_t>(vflag.size(), 1), st);
+        vflag_d.upload(vflag);
         for (int dep = tree->t - 1; dep >= 0; dep--) {
           std::vector<GemmDesc> gd;
+          std::vector<std::array<const double*, 4>> tj;
+          std::vector<const uint8_t*> tf;
           for (int64_t q = (1 << dep) - 1; q < (2 << dep) - 1 && q < nn; q++) {
             if (tree->state[q] != 0) continue;
             const double* Sch = Sb.p + (2 * q + 1) * M;  // [S_cL S_cR]: rows x 2M, adjacent slots
             const double* Q = B->Qm.p + B->q_off[q];      // 2M x 2M row-major
-            if (q > 0) gd.push_back(GemmDesc{Sch, ld, Q, 2 * M, Sb.p + q * M, ld, (int32_t)rows, M, 2 * M, 0});
-            gd.push_back(GemmDesc{Sch, ld, Q + M, 2 * M, Vb.p + q * M, ld, (int32_t)rows, M, 2 * M, 0});
+            if (transfer_kernel_ok(M)) {
+              tj.push_back({Sch, Q, q > 0 ? Sb.p + q * M : nullptr, Vb.p + q * M});
+              tf.push_back(vflag_d.p + vflag_off[q]);
+            } else {
+              if (q > 0) gd.push_back(GemmDesc{Sch, ld, Q, 2 * M, Sb.p + q * M, ld, (int32_t)rows, M, 2 * M, 0});
+              gd.push_back(GemmDesc{Sch, ld, Q + M, 2 * M, Vb.p + q * M, ld, (int32_t)rows, M, 2 * M, 0});
+            }
           }
+          transfer_level(c, tj, tf, M, rows, ld);
           if (!gd.empty()) gemm_batched(c, gd, "assemble_transfer_gemm");
         }
         trace.mark("nested_transfer");
@@ -839,11 +972,12 @@ mlk_status mlk_cw_flops(mlk_cw cw, double* gram, double* contract1, double* cont
   MLK_API_END
 }
 
-mlk_status mlk_cw_plan(mlk_cw cw, int32_t* nested, double* transfer_flops) {
+mlk_status mlk_cw_plan(mlk_cw cw, int32_t* nested, double* transfer_flops, double* nested_tile_flops) {
   MLK_API_BEGIN
   MLK_REQUIRE(cw, "cw is NULL");
   if (nested) *nested = cw->nested ? 1 : 0;
   if (transfer_flops) *transfer_flops = cw->f_tr;
+  if (nested_tile_flops) *nested_tile_flops = cw->f_nested_k5a;
   MLK_API_END
 }
 

@@ -117,6 +117,8 @@ void make_tile_units(std::vector<TileUnit>& out, int64_t a_begin, int32_t s_a, i
     u.w_col0 = 0;
     u.w_cols = s_b;
     u.cp_off = 0;
+    u.seg = 0;
+    u.seg_off = 0;
     // FP64-slot estimate per 32-row task: Gram dp + evaluation ~20 + contraction per entry
     u.cost = 32.0 * s_b * (dp + 20 + 8.0 * rq + nr);
     out.push_back(u);
@@ -262,7 +264,7 @@ __global__ void k_tile_aug(const double* __restrict__ Xt, int dpt, int d, int64_
 // reduced over each warp's 8 rows by shuffles and written to colpart (one row per warp and
 // vector); k_colpart_sum adds them in (tile, warp) order.  Half the covariance evaluations,
 // deterministic.
-template <int RQ, int FAM, int NV, bool SYM = false>
+template <int RQ, int FAM, int NV, bool SYM = false, bool SEG = false>
 __global__ void __launch_bounds__(128, TileCfg<RQ>::MIN_CTAS)
     k_tile_contract(const TileUnit* __restrict__ units, const int32_t* __restrict__ task_range,
                     const int32_t* __restrict__ task_first, int n_units, int* __restrict__ counter,
@@ -376,6 +378,48 @@ __global__ void __launch_bounds__(128, TileCfg<RQ>::MIN_CTAS)
 
     const int ar = warp * 8 + (lane >> 2);
     const int64_t ga = a0 + ar;
+    int seg_k = 0, seg_next = SEG ? u.seg : 0;  // SEG: current segment, first point of the next
+    // store sigma2 x the accumulators of the current output (segment kseg of a segmented unit,
+    // else the unit's U) and clear them; the lane-partial DFMA columns are summed over the quad
+    auto flush = [&](int kseg) {
+      double* Uo = u.U + (int64_t)kseg * u.seg_off;
+      const int r = u.row0 + ar;
+      if constexpr (NV == 0) {
+        if (NRMAX > 0 && nr > 0) {
+#pragma unroll
+          for (int l = 0; l < NRMAX; l++) {
+            double v = accr[l];
+            v += __shfl_xor_sync(0xffffffffu, v, 1);
+            v += __shfl_xor_sync(0xffffffffu, v, 2);
+            if ((lane & 3) == 0 && r < u.s_a && l < nr) {
+              v *= kp.sigma2;
+              const int col = u.c0 + 8 * RQ + l;
+              if (u.trans) Uo[(int64_t)col * u.ldu + r] = v;
+              else Uo[(int64_t)r * u.ldu + col] = v;
+            }
+            accr[l] = 0.0;
+          }
+        }
+        if (r < u.s_a) {
+#pragma unroll
+          for (int q = 0; q < RQ; q++) {
+#pragma unroll
+            for (int e = 0; e < 2; e++) {
+              const int l = 8 * q + 2 * (lane & 3) + e;
+              if (l < u.qc) {
+                const double v = kp.sigma2 * (NACC == 2 ? acc[0][q][e] + acc[NACC - 1][q][e] : acc[0][q][e]);
+                if (u.trans) Uo[(int64_t)(u.c0 + l) * u.ldu + r] = v;
+                else Uo[(int64_t)r * u.ldu + u.c0 + l] = v;
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < NACC; h++)
+#pragma unroll
+          for (int i = 0; i < RQ; i++) acc[h][i][0] = acc[h][i][1] = 0.0;
+      }
+    };
     const double na = nmode ? As[ar * sdp + dk] : 0.0;  // |u_a|^2 of the lane's row (norm mode)
     // the lane's row as a local b index (dga) and the CTA's rows' range [dga_lo, dga_hi], clamped
     // to int: b points are local indices 0 .. s_b - 1, so a far-away row never matches
@@ -534,6 +578,12 @@ __global__ void __launch_bounds__(128, TileCfg<RQ>::MIN_CTAS)
         // fragments for G n-tiles are held in registers
 #pragma unroll
         for (int t = 0; t < T; t++) {
+          if constexpr (SEG) {  // warp-uniform: a segment ends before this sub-tile
+            if (yb + 8 * t == seg_next && seg_next < u.s_b) {
+              flush(seg_k++);
+              seg_next += u.seg;
+            }
+          }
 #pragma unroll
           for (int q0 = 0; q0 < RQ; q0 += G) {
             double2 w[G];
@@ -596,34 +646,7 @@ __global__ void __launch_bounds__(128, TileCfg<RQ>::MIN_CTAS)
         }
       }
     } else {
-      if (NRMAX > 0 && nr > 0) {
-#pragma unroll
-        for (int l = 0; l < NRMAX; l++) {
-          double v = accr[l];
-          v += __shfl_xor_sync(0xffffffffu, v, 1);
-          v += __shfl_xor_sync(0xffffffffu, v, 2);
-          if ((lane & 3) == 0 && r < u.s_a && l < nr) {
-            v *= kp.sigma2;
-            const int col = u.c0 + 8 * RQ + l;
-            if (u.trans) u.U[(int64_t)col * u.ldu + r] = v;
-            else u.U[(int64_t)r * u.ldu + col] = v;
-          }
-        }
-      }
-      if (r < u.s_a) {
-#pragma unroll
-      for (int q = 0; q < RQ; q++) {
-#pragma unroll
-        for (int e = 0; e < 2; e++) {
-          const int l = 8 * q + 2 * (lane & 3) + e;
-          if (l < u.qc) {
-            const double v = kp.sigma2 * (NACC == 2 ? acc[0][q][e] + acc[NACC - 1][q][e] : acc[0][q][e]);
-            if (u.trans) u.U[(int64_t)(u.c0 + l) * u.ldu + r] = v;
-            else u.U[(int64_t)r * u.ldu + u.c0 + l] = v;
-          }
-        }
-      }
-      }
+      flush(seg_k);
     }
   }
 }
@@ -636,6 +659,7 @@ struct AugArgs {
   const int32_t* task_range;  // task -> range (relative to the class), per class
   const int32_t* task_first;  // range -> first task (relative to the class)
   double* colpart = nullptr;  // symmetric C a column partials (nullptr: ordinary product)
+  bool seg = false;           // segmented units (the nested assembly's leaf runs; rq <= 9)
 };
 
 // task -> range map of one class: ranges r own tasks first[r] .. first[r] + n_tasks[r] - 1
@@ -686,11 +710,11 @@ int class_bn(int rq) {
   }
 }
 
-template <int RQ, int FAM, int NV = 0, bool SYM = false>
+template <int RQ, int FAM, int NV = 0, bool SYM = false, bool SEG = false>
 void launch_class(Ctx& c, const AugArgs& ag, const KernelParams& kp, const TileUnit* units, int n, int* counter) {
   // units = this class's ranges; n = its tasks (ag.task_range / ag.task_first are class-relative)
   constexpr int BN = TileCfg<RQ>::BN;
-  auto fn = k_tile_contract<RQ, FAM, NV, SYM>;
+  auto fn = k_tile_contract<RQ, FAM, NV, SYM, SEG>;
   // ring depth: the deepest ring (<= NST, >= 2) that keeps MIN_CTAS resident CTAs per SM (the
   // stage size grows with d: a fixed depth cut cfg3 / cfg4 to 1-2 CTAs per SM).  Attribute and
   // occupancy queries are driver round trips: once per instantiation, device and row stride
@@ -750,14 +774,14 @@ void launch_fam(Ctx& c, const AugArgs& ag, const KernelParams& kp, int rq, const
       if (ag.colpart) launch_class<1, FAM, 4, true>(c, ag, kp, units, n, counter);
       else launch_class<1, FAM, 4>(c, ag, kp, units, n, counter);
       break;
-    case 1: launch_class<1, FAM>(c, ag, kp, units, n, counter); break;
-    case 2: launch_class<2, FAM>(c, ag, kp, units, n, counter); break;
-    case 3: launch_class<3, FAM>(c, ag, kp, units, n, counter); break;
-    case 4: launch_class<4, FAM>(c, ag, kp, units, n, counter); break;
-    case 6: launch_class<6, FAM>(c, ag, kp, units, n, counter); break;
-    case 7: launch_class<7, FAM>(c, ag, kp, units, n, counter); break;
-    case 8: launch_class<8, FAM>(c, ag, kp, units, n, counter); break;
-    case 9: launch_class<9, FAM>(c, ag, kp, units, n, counter); break;
+#define MLK_SEG_CASE(K)                                                            \
+  case K:                                                                          \
+    if (ag.seg) launch_class<K, FAM, 0, false, true>(c, ag, kp, units, n, counter); \
+    else launch_class<K, FAM>(c, ag, kp, units, n, counter);                        \
+    break;
+    MLK_SEG_CASE(1) MLK_SEG_CASE(2) MLK_SEG_CASE(3) MLK_SEG_CASE(4) MLK_SEG_CASE(6) MLK_SEG_CASE(7)
+    MLK_SEG_CASE(8) MLK_SEG_CASE(9)
+#undef MLK_SEG_CASE
     case 12: launch_class<12, FAM>(c, ag, kp, units, n, counter); break;
     case 16: launch_class<16, FAM>(c, ag, kp, units, n, counter); break;
     case 20: launch_class<20, FAM>(c, ag, kp, units, n, counter); break;
@@ -807,6 +831,10 @@ void run_tile_contract(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, s
   // conflicts of the fragment loads when dpa/4 is even
   AugArgs ag;
   ag.colpart = colpart;
+  ag.seg = units.front().seg > 0;
+  for (const auto& u : units)
+    MLK_REQUIRE((u.seg > 0) == ag.seg && (!ag.seg || (u.rq >= 1 && u.rq <= 9)),
+                "run_tile_contract: segmented and plain units cannot share a call");
   // Gram columns: augmented [u, |u|^2, 1] rows when d + 2 pads to the same multiple of 4 as d,
   // else (d = 3, 4 mod 4, e.g. cfg3's d = 20) the norm mode: one DMMA k-step fewer per sub-tile
 #ifndef MLK_NO_NORM_MODE  // A/B switch (tools/build_variant.py)

@@ -31,6 +31,11 @@ struct TileUnit {
   int64_t w_col0;            // W_b column of point b_begin (0, except the symmetric C a tasks)
   int64_t w_cols;            // columns of W_b addressable by the tensor map (s_b by default)
   int64_t cp_off;            // symmetric C a: offset of this task's column partials (NV x s_b)
+  int32_t seg;               // > 0: the b range is a run of segments of seg points (the nested
+                             // assembly's leaves), each with its own output: U + k seg_off for
+                             // segment k (the accumulators are written and cleared at every
+                             // segment boundary; seg is a multiple of 8)
+  int64_t seg_off;
 };
 
 struct KernelParams {

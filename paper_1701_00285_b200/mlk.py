@@ -113,7 +113,7 @@ _sig = {
     "mlk_shard_plan": (C.c_int, [P, P, C.c_int64, C.c_int32, P, P]),
     "mlk_launch_count": (C.c_int64, []),
     "mlk_cw_flops": (C.c_int, [P, P, P, P]),
-    "mlk_cw_plan": (C.c_int, [P, P, P]),
+    "mlk_cw_plan": (C.c_int, [P, P, P, P]),
     "mlk_cw_export_async": (C.c_int, [P, P, P]),
     "mlk_ctx_wait_copies": (C.c_int, [P]),
     "mlk_pcg_solve": (C.c_int, [P, P, P, C.POINTER(KernelSpec), P, C.c_int32, P, P, C.c_double, C.c_int32,
@@ -408,10 +408,10 @@ class CW:
         return dict(gram=g.value, contract1=a.value, contract2=b.value)
 
     def plan(self):
-        """dict(nested, transfer_flops) of mlk_cw_plan."""
-        nst, tf = C.c_int32(), C.c_double()
-        _check(_lib.mlk_cw_plan(self.h, C.byref(nst), C.byref(tf)))
-        return dict(nested=bool(nst.value), transfer_flops=tf.value)
+        """dict(nested, transfer_flops, nested_tile_flops) of mlk_cw_plan."""
+        nst, tf, nf = C.c_int32(), C.c_double(), C.c_double()
+        _check(_lib.mlk_cw_plan(self.h, C.byref(nst), C.byref(tf), C.byref(nf)))
+        return dict(nested=bool(nst.value), transfer_flops=tf.value, nested_tile_flops=nf.value)
 
     def owner(self):
         o = np.empty(self.n_blocks, np.int32)

@@ -97,6 +97,14 @@ def main():
         blocks[pairs[k]] = s
         res["targets"].append({"pair": list(pairs[k]), "pieces": len(sums[k])})
     pos = {q: i for i, q in enumerate(cells)}
+    # the completed level-1 blocks B_11, B_12 (the oracle's entries_cfg5 blocks), for a host-side
+    # comparison with the oracle entries when those are computed after this run (28 MB)
+    keep = {k: v for k, v in blocks.items() if k in ((1, 1), (1, 2), (2, 1))}
+    np.savez_compressed(os.path.join(os.path.dirname(a.out), "cfg5_level1_blocks.npz"),
+                        pairs=np.array(list(keep.keys()), np.int32),
+                        shapes=np.array([[int(B.row_off[pos[p] + 1] - B.row_off[pos[p]]),
+                                          int(B.row_off[pos[q] + 1] - B.row_off[pos[q]])] for p, q in keep], np.int64),
+                        **{"b_%d_%d" % k: v for k, v in keep.items()})
     if gold is not None:
         chk = []
         for (p, q) in [tuple(int(v) for v in b) for b in gold["blocks"]]:
