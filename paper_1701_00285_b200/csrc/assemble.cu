@@ -20,10 +20,12 @@ namespace mlk {
 // of n only, so the pieces (and the results) are the same for every rank count.
 // cost model of the nested assembly against the direct units (K5a entries cost 2 dp + 16 rq + 60
 // "units"): the nested leaf pass runs K5a ~15 % below the direct units' efficiency (shorter
-// b streams, r02i), a transfer flop costs kTransferW units (the transfer kernel ran at 11-21
-// TFLOP/s against K5a's 26-28, r02i)
+// b streams, r02i), a transfer flop costs transfer_weight(M) units (the transfer kernel ran at
+// 7-11 TFLOP/s against K5a's 26-28, r02j)
 constexpr double kNestedK5aW = 1.15;
-constexpr double kTransferW = 3.5;
+// 2M <= 112 (Q_c in <= 113 KB of shared memory, two transfer CTAs per SM): 3.5 units per flop
+// (cfg4, M = 51); larger M one CTA per SM: 6 (cfg2, M = 66: 6.7 TFLOP/s, r02j)
+inline double transfer_weight(int M) { return 2 * M <= 112 ? 3.5 : 6.0; }
 int64_t row_chunk(int64_t n) {
   int64_t ch = 4096;
   while (ch < 32768 && (n >> 18) >= 2 * (ch / 4096)) ch *= 2;
@@ -421,7 +423,7 @@ mlk_status mlk_assemble_cw_ex(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const
       nested = true;
     } else if (mode != "direct") {
       // per-entry K5a cost ~ (2 dp + 16 rq + 60) as in the unit costs below; transfers 8 M^2
-      // flops per (row, internal cell) on the batched GEMM, weighted kTransferW per flop (it ran
+      // flops per (row, internal cell) on the batched GEMM, weighted transfer_weight(M) per flop (it ran
       // at ~40 % of the FP64 peak against K5a's ~70 %: r02f)
       std::map<int, double> rows_b;
       std::map<int, std::vector<std::pair<int64_t, int64_t>>> rs;
@@ -469,7 +471,7 @@ mlk_status mlk_assemble_cw_ex(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const
         vrows += (double)(tot + cur_hi - cur_lo);
       }
       const double nest = kNestedK5aW * (double)tree->n * (double)tree->n * (2.0 * dp + 16.0 * rqm + 60.0) +
-                          kTransferW * 4.0 * B->M * B->M * ((double)tree->n * (double)nint + vrows);
+                          transfer_weight(B->M) * 4.0 * B->M * B->M * ((double)tree->n * (double)nint + vrows);
       nested = nest < 0.9 * direct;
     }
   }
@@ -511,7 +513,7 @@ mlk_status mlk_assemble_cw_ex(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const
         for (auto& kv : nested_rows)
           for (auto& rg : kv.second) vr += (double)std::max<int64_t>(0, std::min(rg.second, hi) - std::max(rg.first, lo));
         u.flops_tr = 4.0 * B->M * B->M * ((double)(hi - lo) * (double)(nint - 1) + vr);
-        u.cost = kNestedK5aW * (hi - lo) * n * (2.0 * dp + 16.0 * rqm + 60.0) + kTransferW * u.flops_tr;
+        u.cost = kNestedK5aW * (hi - lo) * n * (2.0 * dp + 16.0 * rqm + 60.0) + transfer_weight(B->M) * u.flops_tr;
         nested_unit.push_back((int)units.size());
         units.push_back(u);
       }

@@ -19,8 +19,8 @@ namespace mlk {
 namespace {
 
 constexpr int kTrRows = 64;       // rows per pass (8 warps x 8)
-// passes per CTA: Q_c is loaded once per CTA, so a CTA takes as many 64-row passes as keeps
-// >= 2 CTAs per SM busy (deep levels: many cells; the root level: 1 cell, 4 passes)
+// passes per CTA: 4 x 64 rows (Q_c loaded once per 256 rows; adaptive pass counts that keep
+// only ~2 CTAs per SM busy measured slower: 134 -> 167 ms at cfg4, r02j)
 constexpr int kTrMaxM2 = 144;     // 2M limit of the shared-memory kernel (M <= 72)
 
 struct TransferJob {
@@ -35,7 +35,8 @@ __host__ __device__ constexpr int tr_stride(int m2p) { return (m2p + 11) / 16 * 
 
 template <int NT>  // NT = 2M padded / 8 column tiles
 #ifndef MLK_TR_MINB
-#define MLK_TR_MINB 1  // CTAs per SM the register budget targets (2: 128 registers, spills at 2M = 136)
+#define MLK_TR_MINB 2  // CTAs per SM the register budget targets (128 registers; 1: 212 registers,
+                       // one CTA per SM: cfg4 transfers 167 vs 145 ms, r02j)
 #endif
 __global__ void __launch_bounds__(256, MLK_TR_MINB) k_transfer(const TransferJob* __restrict__ jobs, int M, int64_t rows,
                                                      int64_t ld, int passes) {
@@ -109,9 +110,11 @@ void launch_transfer(Ctx& c, const TransferJob* jobs, int njobs, int M, int64_t 
       set[c.device] = true;
     }
   }
-  const int64_t blocks_needed = ceil_div((int64_t)2 * num_sms(c.device), (int64_t)njobs);
   const int64_t row_blocks = ceil_div(rows, (int64_t)kTrRows);
-  const int passes = (int)std::max<int64_t>(1, std::min<int64_t>(row_blocks, std::max<int64_t>(4, row_blocks / blocks_needed)));
+#ifndef MLK_TR_PASSES
+#define MLK_TR_PASSES 4
+#endif
+  const int passes = (int)std::min<int64_t>(row_blocks, MLK_TR_PASSES);
   dim3 grid((unsigned)ceil_div(row_blocks, (int64_t)passes), (unsigned)njobs);
   k_transfer<NT><<<grid, 256, smem, c.stream>>>(jobs, M, rows, ld, passes);
   check_launch("k_transfer");

@@ -705,3 +705,24 @@ def test_full_size_goldens_match_the_sample(name):
     assert root[0] in need
     mv = np.load(os.path.join(GOLD, "matvec_%s.npz" % name))
     assert mv["y_exact"].shape == (c["n"] - M,)
+
+
+def test_cfg5_entries_golden_structure():
+    """tests/golden/entries_cfg5.npz (tools/make_golden_cfg5.py, oracle only): 4 x 4 seeded
+    entries psi_k^T C psi_l of the level-1 blocks B_11 and B_12 at full cfg5 size, with row and
+    column indices inside the cells' wavelet counts (M = 1326 for internal cells) and finite,
+    non-trivial values (checked against the GPU by tools/cfg5_all_ranks.py,
+    profiles/cfg5_level1_entries_r02.json)."""
+    g = np.load(os.path.join(GOLD, "entries_cfg5.npz"))
+    assert sorted(tuple(int(v) for v in b) for b in g["blocks"]) == [(1, 1), (1, 2)]
+    for p, q in ((1, 1), (1, 2)):
+        e = g["entries_%d_%d" % (p, q)]
+        assert e.shape == (4, 4) and np.all(np.isfinite(e)) and np.max(np.abs(e)) > 0
+        assert np.all(g["rows_%d_%d" % (p, q)] < 1326) and np.all(g["cols_%d_%d" % (p, q)] < 1326)
+    # the diagonal block's entries with equal row and column index are psi_k^T C psi_k > 0
+    r, c = g["rows_1_1"], g["cols_1_1"]
+    e = g["entries_1_1"]
+    for i in range(4):
+        for j in range(4):
+            if r[i] == c[j]:
+                assert e[i, j] > 0
