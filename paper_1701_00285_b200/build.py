@@ -15,7 +15,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
 SOURCES = ["ctx.cu", "comm.cu", "tree.cu", "gemm.cu", "basis.cu", "tile.cu", "assemble.cu", "dd.cu", "matvec.cu", "pcg.cu",
-           "loglik.cu", "nested.cu"]
+           "loglik.cu", "nested.cu", "covsym.cu"]
 
 
 def _compile(src):

@@ -232,9 +232,10 @@ __global__ void k_colpart_final(const double* __restrict__ tmp, int64_t j0, int6
   b[(int64_t)l * n + j] += s;
 }
 
-// b = C a for this rank's rows (others zero); a, b device, nvec x n.  Up to 4 vectors use the
-// symmetric kernel (each covariance entry evaluated once for the pair (i, j), i <= j) when its
-// column partials (4 warps x nvec x n^2 / 64 doubles over all ranks) fit the scratch budget.
+// b = C a for this rank's rows (others zero); a, b device, nvec x n.  Symmetric kernels (each
+// covariance entry evaluated once for the pair (i, j), i <= j) when their column partials fit:
+// up to 4 vectors the lane-local DFMA variant of tile.cu (4 warps x nvec x n^2 / 64 doubles),
+// 5 or more the DMMA kernel of covsym.cu (nvec x n^2 / 128 doubles per group of 16 vectors).
 void cov_matvec_dev(Ctx& c, const mlk_tree_s* tree, const mlk_kernel& k, const double* a, double* b, int nvec) {
   const int64_t n = tree->n;
   CUDA_CHECK(cudaMemsetAsync(b, 0, sizeof(double) * nvec * n, c.stream));
@@ -259,7 +260,37 @@ void cov_matvec_dev(Ctx& c, const mlk_tree_s* tree, const mlk_kernel& k, const d
   // the same branch: the choice depends only on (n, nvec, nranks) and the device's TOTAL memory
   // (identical across the ranks of one box), never on this rank's free memory.  The symmetric
   // kernel's column partials of the largest rank share must fit a quarter of the device.
-  bool sym = nvec <= 4 && std::getenv("MLK_NO_SYM_MATVEC") == nullptr;
+  const bool nosym = std::getenv("MLK_NO_SYM_MATVEC") != nullptr;
+  // (MLK_SYM_MIN_NVEC: A/B switch for the vector count from which covsym.cu takes over)
+  const char* smn = std::getenv("MLK_SYM_MIN_NVEC");
+  if (nvec >= (smn ? std::atoi(smn) : 5) && !nosym) {
+    // 5 or more vectors: the symmetric kernel with DMMA contractions (covsym.cu), tasks of
+    // kSymRows rows split by their triangular costs n - kSymRows I; its column partials
+    // (n^2 min(nvec, 16) / 128 doubles in all) must fit a quarter of the device (rank-invariant)
+    const int64_t T = ceil_div(n, (int64_t)kSymRows);
+    auto cost_before = [&](int64_t I) { return (double)I * n - 0.5 * kSymRows * (double)I * (I - 1); };
+    auto range = [&](int r, int64_t& a0, int64_t& a1) {
+      const double total = cost_before(T);
+      a0 = 0;
+      while (a0 < T && cost_before(a0 + 1) <= total * r / c.nranks) a0++;
+      a1 = a0;
+      while (a1 < T && cost_before(a1 + 1) <= total * (r + 1) / c.nranks) a1++;
+      if (r == c.nranks - 1) a1 = T;
+    };
+    int64_t worst = 0;
+    for (int r = 0; r < c.nranks; r++) {
+      int64_t a0, a1;
+      range(r, a0, a1);
+      worst = std::max(worst, cov_sym_partials(n, nvec, a0, a1));
+    }
+    if (worst * (int64_t)sizeof(double) <= device_total_bytes(c.device) / 4) {
+      int64_t a0, a1;
+      range(c.rank, a0, a1);
+      cov_matvec_sym(c, tree, make_kernel_params(k), a, b, nvec, a0, a1);
+      return;
+    }
+  }
+  bool sym = nvec <= 4 && !nosym;
   if (sym) {
     int64_t worst = 0;
     for (int r = 0; r < c.nranks; r++) {

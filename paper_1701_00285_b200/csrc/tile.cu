@@ -28,6 +28,7 @@
 #include <cudaTypedefs.h>
 
 #include "dmma.cuh"
+#include "corr.cuh"
 #include "fastmath.cuh"
 #include "tile.cuh"
 
@@ -126,66 +127,6 @@ void make_tile_units(std::vector<TileUnit>& out, int64_t a_begin, int32_t s_a, i
 }
 
 namespace {
-
-// phi(z) = 2^(1-nu)/Gamma(nu) z^nu K_nu(z), z > 0 (the Matern definition), from
-// two textbook representations of K_nu:
-//  * the integral K_nu(z) = int_0^inf exp(-z cosh t) cosh(nu t) dt, by the trapezoidal rule with
-//    step h = h0 / max(1, sqrt z).  The integrand is entire and decays double-exponentially, so
-//    the rule converges geometrically in 1/h; the sqrt(z) scaling keeps the peak of width
-//    ~1/sqrt(z) resolved at large z.  z^nu is folded into the exponent,
-//    z^nu e^{-z cosh t} cosh(nu t) = e^{nu (t + log z) - z cosh t} (1 + e^{-2 nu t}) / 2,
-//    so nothing overflows for large nu or small z; the sum stops once t is past the integrand's
-//    peak (sinh t = nu / z) and a term falls below 1e-17 of the sum.  e^t and e^{-2 nu t} advance
-//    by one multiplication per node.  Measured against scipy's K_nu (tools, this round): relative
-//    error <= 7e-13 for nu in [0.1, 50], z in [1e-8, 700]; <= 2e-13 for nu <= 12.
-//  * for z < 2 and nu at least 0.01 from an integer, the series from K_nu = pi/2 (I_-nu - I_nu) /
-//    sin(nu pi) and I_mu(z) = sum_k (z/2)^(2k+mu) / (k! Gamma(k+mu+1)), which with
-//    Gamma(nu) Gamma(1-nu) = pi / sin(nu pi) becomes
-//      phi = sum_k w^k Gamma(1-nu) / (k! Gamma(k+1-nu)) - Gamma(1-nu) (z/2)^(2 nu) sum_k w^k / (k! Gamma(k+1+nu)),
-//    w = z^2 / 4 (about 13 terms; phi(0) = 1 is its k = 0 term).  Near integer nu the two sums
-//    cancel (Gamma(1-nu) has poles there), so those nu always take the integral.
-__device__ __noinline__ double matern_nu(double z, const KernelParams& kp) {
-  const double nu = kp.nu;
-  if (kp.series && z < 2.0) {
-    const double w = 0.25 * z * z;
-    double a = 1.0, sm = 1.0, b = kp.rg1p, sp = kp.rg1p;
-    for (int k = 1; k < 100; k++) {
-      a *= w / (k * (k - nu));
-      b *= w / (k * (k + nu));
-      sm += a;
-      sp += b;
-      if (fabs(a) <= 1e-17 * fabs(sm) && fabs(b) <= 1e-17 * fabs(sp)) break;
-    }
-    return sm - kp.g1m * exp(2.0 * nu * log(0.5 * z)) * sp;
-  }
-  const double h = kp.h0 / fmax(1.0, sqrt(z));
-  const double lz = nu * log(z), E = exp(h), Q = exp(-2.0 * nu * h);
-  const double tpk = asinh(nu / z);
-  double e = 1.0, q = 1.0, s = 0.5 * exp(lz - z);  // node t = 0, weight 1/2
-  for (int k = 1; k < 4096; k++) {
-    e *= E;
-    q *= Q;
-    const double t = k * h;
-    const double term = exp(nu * t + lz - 0.5 * z * (e + 1.0 / e)) * 0.5 * (1.0 + q);
-    s += term;
-    if (t > tpk && term <= 1e-17 * s) break;
-  }
-  return kp.norm * h * s;
-}
-
-// correlation phi from the augmented Gram value x = z^2 (Matern, z = sqrt(2 nu) r / rho) or
-// x = r^2 / rho^2 (Gaussian); R16, R17
-template <int FAM>
-__device__ __forceinline__ double corr(double x, const double* tab, const KernelParams& kp) {
-  if (FAM == MLK_GAUSSIAN) return exp_neg(x, tab);  // x >= -O(u|y|^2): e^{-x} stays ~1
-  if (FAM == MLK_MATERN_NU) return x > 0.0 ? matern_nu(sqrt(x), kp) : 1.0;
-  x = clamp_pos(x);
-  const double z = sqrt_pos(x);
-  const double e = exp_neg(z, tab);
-  if (FAM == MLK_MATERN_12) return e;
-  if (FAM == MLK_MATERN_32) return fma(z, e, e);                  // (1 + z) e^{-z}
-  return fma(e, fma(x, 1.0 / 3.0, z), e);                         // (1 + z + z^2/3) e^{-z}
-}
 
 // A/B switches (tools/build_variant.py): occupancy target and stage width of the 2-4 group classes
 #ifndef MLK_MINCTAS_SMALL
@@ -670,6 +611,8 @@ __global__ void k_expand_tasks(const int32_t* __restrict__ first, const int32_t*
   for (int t = threadIdx.x; t < ntask[r]; t += blockDim.x) task_range[first[r] + t] = r;
 }
 
+}  // namespace
+
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -697,6 +640,8 @@ CUtensorMap make_map_2d(const double* base, uint64_t rows, uint64_t cols, uint64
   if (r != CUDA_SUCCESS) throw Error(MLK_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return m;
 }
+
+namespace {
 
 int class_bn(int rq) {
   switch (rq) {
@@ -792,6 +737,32 @@ void launch_fam(Ctx& c, const AugArgs& ag, const KernelParams& kp, int rq, const
 
 }  // namespace
 
+// Gram columns: augmented [u, |u|^2, 1] rows when d + 2 pads to the same multiple of 4 as d,
+// else (d = 3, 4 mod 4, e.g. cfg3's d = 20) the norm mode: one DMMA k-step fewer per sub-tile.
+// The shared-memory row stride avoids 2-way bank conflicts of the fragment loads when dpa/4 is
+// even.
+void tile_aug_layout(int d, AugCoords& a) {
+#ifndef MLK_NO_NORM_MODE  // A/B switch (tools/build_variant.py)
+  const bool norm_mode = pad4(d + 2) > pad4(d);
+#else
+  const bool norm_mode = false;
+#endif
+  if (norm_mode) {
+    a.dk = pad4(d);
+    a.dpa = a.dk + 4;
+  } else {
+    a.dk = a.dpa = pad4(d + 2);
+  }
+  a.sdp = ((a.dpa >> 2) & 1) ? a.dpa : a.dpa + 4;
+}
+
+void tile_aug_fill(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, AugCoords& a) {
+  if (a.buf.n < (size_t)2 * tree->n * a.dpa) a.buf.alloc((size_t)2 * tree->n * a.dpa, c.stream);
+  k_tile_aug<<<(unsigned)ceil_div(tree->n, 256), 256, 0, c.stream>>>(tree->Xt.p, tree->d_pad, tree->d, tree->n,
+                                                                     kp.scale, a.Pa(), a.Pb(tree->n), a.dpa, a.dk);
+  check_launch("k_tile_aug");
+}
+
 void run_tile_contract(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, std::vector<TileUnit>& units,
                        const char* name, double* colpart) {
   if (units.empty()) return;
@@ -835,23 +806,14 @@ void run_tile_contract(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, s
   for (const auto& u : units)
     MLK_REQUIRE((u.seg > 0) == ag.seg && (!ag.seg || (u.rq >= 1 && u.rq <= 9)),
                 "run_tile_contract: segmented and plain units cannot share a call");
-  // Gram columns: augmented [u, |u|^2, 1] rows when d + 2 pads to the same multiple of 4 as d,
-  // else (d = 3, 4 mod 4, e.g. cfg3's d = 20) the norm mode: one DMMA k-step fewer per sub-tile
-#ifndef MLK_NO_NORM_MODE  // A/B switch (tools/build_variant.py)
-  const bool norm_mode = pad4(tree->d + 2) > pad4(tree->d);
-#else
-  const bool norm_mode = false;
-#endif
-  if (norm_mode) {
-    ag.dk = pad4(tree->d);
-    ag.dpa = ag.dk + 4;
-  } else {
-    ag.dk = ag.dpa = pad4(tree->d + 2);
-  }
-  ag.sdp = ((ag.dpa >> 2) & 1) ? ag.dpa : ag.dpa + 4;
-  DevBuf<double> aug((size_t)2 * tree->n * ag.dpa, c.stream);
-  ag.Pa = aug.p;
-  ag.Pb = aug.p + (size_t)tree->n * ag.dpa;
+  AugCoords aug;
+  tile_aug_layout(tree->d, aug);
+  ag.dk = aug.dk;
+  ag.dpa = aug.dpa;
+  ag.sdp = aug.sdp;
+  aug.buf.alloc((size_t)2 * tree->n * ag.dpa, c.stream);
+  ag.Pa = aug.buf.p;
+  ag.Pb = aug.buf.p + (size_t)tree->n * ag.dpa;
   // tensor maps: one for the b rows per stage width, one per distinct W_b (base, shape, box)
   std::vector<CUtensorMap> maps;
   {
@@ -892,10 +854,7 @@ void run_tile_contract(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, s
   ntask_d.upload(ntask);
   DevBuf<int32_t> task_range((size_t)std::max<int64_t>(tasks_total, 1), c.stream);
   TimedLaunch tl(c, name);
-  k_tile_aug<<<(unsigned)ceil_div(tree->n, 256), 256, 0, c.stream>>>(tree->Xt.p, tree->d_pad, tree->d, tree->n,
-                                                                     kp.scale, aug.p, aug.p + (size_t)tree->n * ag.dpa,
-                                                                     ag.dpa, ag.dk);
-  check_launch("k_tile_aug");
+  tile_aug_fill(c, tree, kp, aug);
   for (size_t g = 0; g + 1 < starts.size(); g++) {
     const int s0 = starts[g], nr_ = starts[g + 1] - starts[g];
     k_expand_tasks<<<(unsigned)nr_, 128, 0, c.stream>>>(first_d.p + s0, ntask_d.p + s0, nr_,

@@ -6,6 +6,8 @@
 // (W_b = wavelet block of the contracted-first cell) and the exact product b = C a
 // (W_b = the vectors a).
 #pragma once
+#include <cuda.h>
+
 #include "api.cuh"
 
 namespace mlk {
@@ -72,5 +74,29 @@ void run_tile_contract(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, s
 // Split a (pair, output) into units: rows in blocks of 32, W_b rows in balanced chunks.
 void make_tile_units(std::vector<TileUnit>& out, int64_t a_begin, int32_t s_a, int64_t b_begin, int32_t s_b,
                      const double* Wb, int64_t ldw, int32_t p_b, double* U, int64_t ldu, int32_t trans, int dp);
+
+// Augmented, pre-scaled coordinates Pa, Pb (n x dpa each, one buffer) of the Gram product
+// (tile.cu k_tile_aug): dk Gram columns, dpa doubles per row, sdp = shared-memory row stride.
+struct AugCoords {
+  DevBuf<double> buf;
+  int dpa = 0, dk = 0, sdp = 0;
+  double* Pa() const { return buf.p; }
+  double* Pb(int64_t n) const { return buf.p + (size_t)n * dpa; }
+};
+void tile_aug_layout(int d, AugCoords& a);
+void tile_aug_fill(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, AugCoords& a);
+// row-major FP64 matrix (rows x cols, row stride ld elements) read by TMA in boxes of
+// box_rows x box_cols (out-of-range elements zero-filled)
+CUtensorMap make_map_2d(const double* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_rows,
+                        uint32_t box_cols);
+// Symmetric b = C a for 5 or more vectors (covsym.cu): tasks [t0, t1) of kSymRows rows; a and b
+// device, nvec x n; b holds this rank's contributions (the caller sums the ranks).
+#ifndef MLK_SYM_RG
+#define MLK_SYM_RG 4  // row groups of 8 per task (A/B switch, tools/build_variant.py)
+#endif
+constexpr int kSymRows = 8 * MLK_SYM_RG;
+int64_t cov_sym_partials(int64_t n, int nvec, int64_t t0, int64_t t1);  // doubles of column partials
+void cov_matvec_sym(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, const double* a, double* b, int nvec,
+                    int64_t t0, int64_t t1);
 
 }  // namespace mlk

@@ -500,13 +500,18 @@ def test_matvec_exact_and_bsr(mlk, ctx, fam, rho):
     assert np.linalg.norm(ya - yr) <= 1e-11 * np.linalg.norm(yr)
 
 
-@pytest.mark.parametrize("nvec", [1, 2, 3, 5])
-def test_cov_matvec_symmetric_and_full_agree(mlk, ctx, nvec, monkeypatch):
-    """b = C a by the symmetric kernel (each pair (i, j) evaluated once, fixed-order column
-    reduction) equals the full n^2 kernel and the oracle; ragged n so the last tile is partial."""
-    X, dirs = _setup(3001, 3, 64, 0, "normal")
+@pytest.mark.parametrize("nvec,d,fam", [(1, 3, OC.MATERN_52), (2, 3, OC.MATERN_52), (3, 3, OC.MATERN_52),
+                                        (5, 3, OC.MATERN_52), (8, 10, OC.MATERN_12), (10, 3, OC.MATERN_32),
+                                        (10, 20, OC.MATERN_52), (16, 10, OC.GAUSSIAN), (19, 4, OC.MATERN_32)])
+def test_cov_matvec_symmetric_and_full_agree(mlk, ctx, nvec, d, fam, monkeypatch):
+    """b = C a by the symmetric kernels (each pair (i, j) evaluated once, fixed-order column
+    reduction: the lane-local DFMA variant up to 4 vectors, the DMMA kernel of covsym.cu with
+    64-row tasks from 5 on -- one and two 8-vector groups, 19 = 16 + 3 in two launches; norm-mode
+    and augmented Gram columns) equals the full n^2 kernel and the oracle; ragged n so the last
+    tile and the last stage are partial and the vector rows are not 16-byte aligned."""
+    X, dirs = _setup(3001, d, 64, 0, "normal")
     g, o = _tree_both(mlk, ctx, X, 64, 0, dirs)
-    kern = dict(family=OC.MATERN_52, rho=0.8, nugget=1e-3, sigma2=1.7)
+    kern = dict(family=fam, rho=0.8 * np.sqrt(d / 3.0), nugget=1e-3, sigma2=1.7)
     a = np.random.default_rng([0, 5]).standard_normal((nvec, 3001))
     b_sym = mlk.cov_matvec(ctx, g, kern, a)
     b_sym2 = mlk.cov_matvec(ctx, g, kern, a)
@@ -516,6 +521,23 @@ def test_cov_matvec_symmetric_and_full_agree(mlk, ctx, nvec, monkeypatch):
     br = OM.cov_matvec(X, o, kern, a)
     assert np.linalg.norm(b_sym - br) <= 1e-12 * np.linalg.norm(br)
     assert np.linalg.norm(b_full - br) <= 1e-12 * np.linalg.norm(br)
+
+
+@pytest.mark.parametrize("nvec", [3, 10])
+def test_cov_matvec_symmetric_rank_split(mlk, ctx, nvec):
+    """The symmetric C a kernels split their tasks over ranks by the triangular costs; the ranks'
+    partial b (contexts of R = 3 ranks run one after another) sum to the single-rank b."""
+    X, dirs = _setup(5000, 5, 64, 0, "normal")
+    kern = dict(family=OC.MATERN_32, rho=1.3)
+    g = mlk.build_tree(ctx, X, 64, 0, dirs)
+    a = np.random.default_rng([0, 6]).standard_normal((nvec, 5000))
+    b1 = mlk.cov_matvec(ctx, g, kern, a)
+    parts = []
+    for r in range(3):
+        c = mlk.Ctx(0, 3, r)
+        parts.append(mlk.cov_matvec(c, mlk.build_tree(c, X, 64, 0, dirs), kern, a))
+    assert all(np.linalg.norm(p) > 0 for p in parts)
+    assert np.linalg.norm(sum(parts) - b1) <= 1e-13 * np.linalg.norm(b1)
 
 
 # --------------------------------------------------------------------------------- multi-rank
