@@ -476,7 +476,21 @@ mlk_status mlk_assemble_cw_ex(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const
     }
   }
   cw->nested = nested;
-  std::vector<int> nested_unit;  // chunk -> unit
+  // the nested units cover CHN = m CH rows (m a power of two, CHN <= 16384): fewer, larger
+  // K5a / transfer / K5b launches with fuller waves (r02v: the top transfer levels of a 4096-row
+  // chunk ran < 1 wave of CTAs).  Pieces stay per CH rows, and every value is computed per row
+  // or per piece, so the results do not depend on m; m depends only on (n, nodes, M) and the
+  // device's total memory (the S and V buffers, 2 CHN n_nodes M doubles, <= 1/8 of it), so it
+  // is the same on every rank.
+  int64_t m_nest = 1;
+  if (nested) {
+    const double per_row = 2.0 * (double)tree->n_nodes * B->M * sizeof(double);
+    while (CH * m_nest * 2 <= std::min<int64_t>(16384, tree->n) &&
+           per_row * (double)(CH * m_nest * 2) <= (double)device_total_bytes(c.device) / 8)
+      m_nest *= 2;
+  }
+  const int64_t CHN = CH * m_nest;
+  std::vector<int> nested_unit;  // nested chunk -> unit
   std::map<int, std::vector<std::pair<int64_t, int64_t>>> nested_rows;  // internal c -> row ranges R_c
   if (!dd) {
     if (nested) {
@@ -498,11 +512,11 @@ mlk_status mlk_assemble_cw_ex(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const
       int64_t nint = 0;
       for (int64_t q = 0; q < nn; q++) nint += tree->state[q] == 0;
       const int rqm = tile_rq_class(std::min(B->M, 8 * kTileMaxRQ));
-      for (int64_t c0 = 0; c0 * CH < tree->n; c0++) {
+      for (int64_t c0 = 0; c0 * CHN < tree->n; c0++) {
         Unit u;
         u.b = -1;
         u.chunk = c0;
-        const int64_t lo = c0 * CH, hi = std::min<int64_t>(tree->n, (c0 + 1) * CH);
+        const int64_t lo = c0 * CHN, hi = std::min<int64_t>(tree->n, (c0 + 1) * CHN);
         u.rows.push_back({lo, hi});
         u.nrows = hi - lo;
         u.flops_gram = 2.0 * d * (hi - lo) * n;
@@ -562,7 +576,7 @@ mlk_status mlk_assemble_cw_ex(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const
     for (int64_t k = 0; k < nb; k++) {
       int a = A[k], b = Bc[k];
       for (int64_t c0 = tree->begin[a] / CH; c0 * CH < tree->end[a]; c0++) {
-        int ui = direct_b(b) ? unit_of.at({b, c0}) : nested_unit[c0];
+        int ui = direct_b(b) ? unit_of.at({b, c0}) : nested_unit[c0 / m_nest];
         int64_t lo = std::max(tree->begin[a], c0 * CH), hi = std::min(tree->end[a], (c0 + 1) * CH);
         double f = 2.0 * B->p[a] * (double)(hi - lo) * B->p[b];
         units[ui].flops_c2 += f;
@@ -841,7 +855,8 @@ mlk_status mlk_assemble_cw_ex(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const
           if (pieces[i].unit != (int)ui) continue;
           const int64_t k = pieces[i].blk;
           const int a = A[k], b = Bc[k];
-          const int64_t plo = std::max(tree->begin[a], lo), phi = std::min(tree->end[a], lo + rows);
+          const int64_t ch = pieces[i].chunk;  // the piece's CH-row chunk inside this unit
+          const int64_t plo = std::max(tree->begin[a], ch * CH), phi = std::min(tree->end[a], (ch + 1) * CH);
           GemmDesc g{B->W.p + B->w_off[a] + (plo - tree->begin[a]), S(a), Vb.p + (plo - lo) * ld + (int64_t)b * M, ld,
                      piece_dst(i), (int64_t)B->p[pairs[k].second], B->p[a], M, (int32_t)(phi - plo), swap[k] ? 1 : 0};
           gd.push_back(g);

@@ -114,7 +114,11 @@ void launch_transfer(Ctx& c, const TransferJob* jobs, int njobs, int M, int64_t 
 #ifndef MLK_TR_PASSES
 #define MLK_TR_PASSES 4
 #endif
-  const int passes = (int)std::min<int64_t>(row_blocks, MLK_TR_PASSES);
+  // fewer passes per CTA where a level has few cells (the top levels), so that the level still
+  // spreads over ~2 CTAs per SM
+  const int64_t want = 2LL * 2 * num_sms(c.device);
+  const int passes = (int)std::max<int64_t>(1, std::min<int64_t>({row_blocks, (int64_t)MLK_TR_PASSES,
+                                                                   row_blocks * njobs / want}));
   dim3 grid((unsigned)ceil_div(row_blocks, (int64_t)passes), (unsigned)njobs);
   k_transfer<NT><<<grid, 256, smem, c.stream>>>(jobs, M, rows, ld, passes);
   check_launch("k_transfer");
