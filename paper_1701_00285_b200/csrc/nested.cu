@@ -11,6 +11,9 @@
 // straight from global memory into registers at the start of each pass (each element once,
 // 32-byte row segments, one round trip per pass).  8 M^2 flops per (row, cell).
 #include <algorithm>
+#include <cstdlib>
+#include <map>
+#include <mutex>
 
 #include "api.cuh"
 #include "dmma.cuh"
@@ -22,6 +25,9 @@ constexpr int kTrRows = 64;       // rows per pass (8 warps x 8)
 // passes per CTA: 4 x 64 rows (Q_c loaded once per 256 rows; adaptive pass counts that keep
 // only ~2 CTAs per SM busy measured slower: 134 -> 167 ms at cfg4, r02j)
 constexpr int kTrMaxM2 = 144;     // 2M limit of the shared-memory kernel (M <= 72)
+// (a tiled variant with Q_c and double-buffered 64-row A tiles in shared memory, 8 warps as
+// 2 row halves x 4 column quarters, one CTA per SM, measured 1.75x slower on cfg4: 199 against
+// 114 ms, r02 tr2 -- the A tile went through shared memory once per column warp)
 
 struct TransferJob {
   const double* Sch;     // [S_cL S_cR], rows x 2M, row stride ld
@@ -33,7 +39,7 @@ struct TransferJob {
 
 __host__ __device__ constexpr int tr_stride(int m2p) { return (m2p + 11) / 16 * 16 + 4; }  // >= m2p, 4 mod 16
 
-template <int NT>  // NT = 2M padded / 8 column tiles
+template <int NT, bool PF>  // NT = 2M padded / 8 column tiles; PF: prefetch the next pass's A (NT <= 8)
 #ifndef MLK_TR_MINB
 #define MLK_TR_MINB 2  // CTAs per SM the register budget targets (128 registers; 1: 212 registers,
                        // one CTA per SM: cfg4 transfers 167 vs 145 ms, r02j)
@@ -43,6 +49,7 @@ __global__ void __launch_bounds__(256, MLK_TR_MINB) k_transfer(const TransferJob
   extern __shared__ __align__(16) double sm[];
   constexpr int M2P = NT * 8;            // 2M padded to a multiple of 8 (k and n)
   constexpr int SQ = tr_stride(M2P);
+  constexpr int KS = M2P / 4;
   const TransferJob jb = jobs[blockIdx.y];
   const int M2 = 2 * M;
   double* Qs = sm;                       // M2P x SQ, zero padded
@@ -51,30 +58,40 @@ __global__ void __launch_bounds__(256, MLK_TR_MINB) k_transfer(const TransferJob
     const int r = e / M2P, cc = e - r * M2P;
     Qs[r * SQ + cc] = (r < M2 && cc < M2) ? jb.Q[(int64_t)r * M2 + cc] : 0.0;
   }
-  __syncthreads();
   const int64_t r_begin = (int64_t)blockIdx.x * kTrRows * passes;
   const double* bp = Qs + (lane & 3) * SQ + (lane >> 2);
+  // the lane's A elements of one pass: one memory round trip per pass, not per k-step
+  auto load = [&](int pass, double (&dst)[KS]) {
+    const int64_t r = r_begin + (int64_t)pass * kTrRows + warp * 8 + (lane >> 2);
+    const bool rok = r < rows;
+    const double* ap = jb.Sch + (rok ? r : 0) * ld + (lane & 3);
+#pragma unroll
+    for (int ks = 0; ks < KS; ks++) {
+      const int k = 4 * ks + (lane & 3);
+      dst[ks] = (rok && k < M2) ? __ldg(ap + 4 * ks) : 0.0;
+    }
+  };
+  double areg[KS], anext[PF ? KS : 1];
+  if (PF && r_begin + warp * 8 < rows) load(0, areg);  // in flight while Q_c is staged
+  __syncthreads();
   for (int pass = 0; pass < passes; pass++) {
     const int64_t r = r_begin + (int64_t)pass * kTrRows + warp * 8 + (lane >> 2);  // the lane's A row
     if (r_begin + (int64_t)pass * kTrRows + warp * 8 >= rows) break;              // warp-uniform
     const bool rok = r < rows;
+    if constexpr (PF) {
+      if (pass + 1 < passes && r_begin + (int64_t)(pass + 1) * kTrRows + warp * 8 < rows) load(pass + 1, anext);
+    } else {
+      load(pass, areg);
+    }
     // V_c only where a block with contracted-first cell c has rows (the S half is needed for
     // every row: the parents' sums); warp-uniform: a pass is one 64-row block
     const int64_t blk = (r_begin >> 6) + pass;
     const int nt_use = (jb.vflag == nullptr || jb.vflag[blk]) ? NT : (M + 7) / 8;
-    const double* ap = jb.Sch + (rok ? r : 0) * ld + (lane & 3);
-    // all of the lane's A elements up front: one memory round trip per pass, not per k-step
-    double areg[M2P / 4];
-#pragma unroll
-    for (int ks = 0; ks < M2P / 4; ks++) {
-      const int k = 4 * ks + (lane & 3);
-      areg[ks] = (rok && k < M2) ? __ldg(ap + 4 * ks) : 0.0;
-    }
     double acc[NT][2];
 #pragma unroll
     for (int t = 0; t < NT; t++) acc[t][0] = acc[t][1] = 0.0;
 #pragma unroll
-    for (int ks = 0; ks < M2P / 4; ks++) {
+    for (int ks = 0; ks < KS; ks++) {
       const double* bk = bp + 4 * ks * SQ;
 #pragma unroll
       for (int t = 0; t < NT; t++)
@@ -94,6 +111,10 @@ __global__ void __launch_bounds__(256, MLK_TR_MINB) k_transfer(const TransferJob
         }
       }
     }
+    if constexpr (PF) {
+#pragma unroll
+      for (int ks = 0; ks < KS; ks++) areg[ks] = anext[ks];
+    }
   }
 }
 
@@ -101,12 +122,21 @@ template <int NT>
 void launch_transfer(Ctx& c, const TransferJob* jobs, int njobs, int M, int64_t rows, int64_t ld) {
   constexpr int M2P = NT * 8;
   const size_t smem = sizeof(double) * (size_t)M2P * tr_stride(M2P);
+  // prefetch of the next pass's A fragments where the registers allow it without spilling
+  // (2M <= 64: cfg3's transfers 15.9 -> 14.5 ms, r02 pf; at cfg4's NT = 13 the extra 26
+  // registers spilled at the 128-register budget and the transfers took 214 against 114 ms,
+  // and one CTA per SM without spills 154 ms).  MLK_TR_NOPF: A/B switch.
+  static const bool pf_env = std::getenv("MLK_TR_NOPF") == nullptr;
+  auto fn = k_transfer<NT, false>;
+  if constexpr (NT <= 8) {
+    if (pf_env) fn = k_transfer<NT, true>;
+  }
   static std::mutex mu;
   static std::map<int, bool> set;
   {
     std::lock_guard<std::mutex> lock(mu);
     if (!set[c.device]) {
-      CUDA_CHECK(cudaFuncSetAttribute(k_transfer<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       set[c.device] = true;
     }
   }
@@ -120,7 +150,7 @@ void launch_transfer(Ctx& c, const TransferJob* jobs, int njobs, int M, int64_t 
   const int passes = (int)std::max<int64_t>(1, std::min<int64_t>({row_blocks, (int64_t)MLK_TR_PASSES,
                                                                    row_blocks * njobs / want}));
   dim3 grid((unsigned)ceil_div(row_blocks, (int64_t)passes), (unsigned)njobs);
-  k_transfer<NT><<<grid, 256, smem, c.stream>>>(jobs, M, rows, ld, passes);
+  fn<<<grid, 256, smem, c.stream>>>(jobs, M, rows, ld, passes);
   check_launch("k_transfer");
 }
 
