@@ -78,6 +78,11 @@ struct mlk_tree_s {
   mlk::DevBuf<double> norm2;      // |x|^2 in tree order
   mlk::DevBuf<double> thr_d;      // n_nodes
   mlk::DevBuf<double> dir_d;      // n_nodes x d
+  // the fused tile kernels' augmented, pre-scaled coordinates Pa, Pb (tile.cu tile_aug_get),
+  // cached for the last coordinate scale: formed once per assembly / product, not per launch
+  mutable mlk::DevBuf<double> aug;
+  mutable double aug_scale = 0.0;
+  mutable int aug_dpa = 0;
 };
 
 // Basis blocks per heap node; cells (nodes with >= 1 wavelet) listed in C_W order.

@@ -413,16 +413,16 @@ void cov_matvec_sym(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, cons
     DevBuf<int> counter(1, c.stream);
     counter.zero();
     TimedLaunch tl(c, "cov_matvec_sym");
-    if (v0 == 0) tile_aug_fill(c, tree, kp, aug);
+    const double* Pa = tile_aug_get(c, tree, kp, aug);
     k_pad_vectors<<<dim3((unsigned)ceil_div(ld, (int64_t)256), (unsigned)(8 * G)), 256, 0, c.stream>>>(
         a + (int64_t)v0 * n, n, nv, apad.p, ld, 8 * G);
     check_launch("k_pad_vectors");
-    std::vector<CUtensorMap> maps = {make_map_2d(aug.Pb(n), n, aug.dpa, aug.dpa, kBN, aug.sdp),
+    std::vector<CUtensorMap> maps = {make_map_2d(Pa + (size_t)n * aug.dpa, n, aug.dpa, aug.dpa, kBN, aug.sdp),
                                      make_map_2d(apad.p, 8 * G, ld, ld, 8 * G, kBN)};
     DevBuf<CUtensorMap> maps_d(2, c.stream);
     maps_d.upload(maps);
     SymArgs ag;
-    ag.Pa = aug.Pa();
+    ag.Pa = Pa;
     ag.dpa = aug.dpa;
     ag.dk = aug.dk;
     ag.sdp = aug.sdp;

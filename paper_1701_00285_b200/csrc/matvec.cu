@@ -197,13 +197,13 @@ void apply_w_dev(Ctx& c, const mlk_tree_s* tree, const mlk_basis_s* B, const dou
   check_launch("k_apply_w");
 }
 
-// Symmetric C a column partials: tile I (of this rank's t0..t1-1) holds 4 (warp) x nvec rows
-// of n - 32 I columns starting at column 32 I, at offset 4 nvec sum_{I' < I} (n - 32 I').
-// Two fixed-order levels: tmp[l][c][j] = sum over the tiles of chunk c (kColChunk tiles) and
-// the 4 warps, then b[l][j] += sum over chunks c in order.  Deterministic.
+// Symmetric C a column partials: tile I (of this rank's t0..t1-1) holds nvec rows of n - 32 I
+// columns starting at column 32 I (its 4 warps already summed in order by the tile kernel), at
+// offset nvec sum_{I' < I} (n - 32 I').  Two fixed-order levels: tmp[l][c][j] = sum over the
+// tiles of chunk c (kColChunk tiles), then b[l][j] += sum over chunks c in order.  Deterministic.
 constexpr int kColChunk = 64;
 __device__ __forceinline__ int64_t colpart_off(int64_t I, int64_t t0, int64_t n, int nvec) {
-  return 4 * (int64_t)nvec * ((I - t0) * n - 16 * (I * (I - 1) - t0 * (t0 - 1)));
+  return (int64_t)nvec * ((I - t0) * n - 16 * (I * (I - 1) - t0 * (t0 - 1)));
 }
 
 __global__ void k_colpart_chunks(const double* __restrict__ colpart, int64_t t0, int64_t t1, int64_t n, int nvec,
@@ -215,9 +215,8 @@ __global__ void k_colpart_chunks(const double* __restrict__ colpart, int64_t t0,
   const int64_t i1 = std::min<int64_t>({t1, i0 + kColChunk, j / 32 + 1});
   double s = 0.0;
   for (int64_t I = i0; I < i1; I++) {
-    const int64_t w = n - 32 * I, base = colpart_off(I, t0, n, nvec) + (j - 32 * I);
-#pragma unroll
-    for (int wp = 0; wp < 4; wp++) s += colpart[base + ((int64_t)wp * nvec + l) * w];
+    const int64_t w = n - 32 * I;
+    s += colpart[colpart_off(I, t0, n, nvec) + (int64_t)l * w + (j - 32 * I)];
   }
   tmp[((int64_t)l * nchunks + c) * n + j] = s;
 }
@@ -234,7 +233,7 @@ __global__ void k_colpart_final(const double* __restrict__ tmp, int64_t j0, int6
 
 // b = C a for this rank's rows (others zero); a, b device, nvec x n.  Symmetric kernels (each
 // covariance entry evaluated once for the pair (i, j), i <= j) when their column partials fit:
-// up to 4 vectors the lane-local DFMA variant of tile.cu (4 warps x nvec x n^2 / 64 doubles),
+// up to 4 vectors the lane-local DFMA variant of tile.cu (nvec x n^2 / 64 doubles),
 // 5 or more the DMMA kernel of covsym.cu (nvec x n^2 / 128 doubles per group of 16 vectors).
 void cov_matvec_dev(Ctx& c, const mlk_tree_s* tree, const mlk_kernel& k, const double* a, double* b, int nvec) {
   const int64_t n = tree->n;
@@ -253,7 +252,7 @@ void cov_matvec_dev(Ctx& c, const mlk_tree_s* tree, const mlk_kernel& k, const d
   };
   auto sym_partials = [&](int64_t a0, int64_t a1) {
     int64_t s = 0;
-    for (int64_t I = a0; I < a1; I++) s += 4 * (int64_t)nvec * (n - 32 * I);
+    for (int64_t I = a0; I < a1; I++) s += (int64_t)nvec * (n - 32 * I);
     return s;
   };
   // The symmetric and the row-panel kernels split the rows differently, so every rank must take
@@ -266,7 +265,7 @@ void cov_matvec_dev(Ctx& c, const mlk_tree_s* tree, const mlk_kernel& k, const d
   if (nvec >= (smn ? std::atoi(smn) : 5) && !nosym) {
     // 5 or more vectors: the symmetric kernel with DMMA contractions (covsym.cu), tasks of
     // kSymRows rows split by their triangular costs n - kSymRows I; its column partials
-    // (n^2 min(nvec, 16) / 128 doubles in all) must fit a quarter of the device (rank-invariant)
+    // (n^2 min(nvec, 16) / 64 doubles in all) must fit a quarter of the device (rank-invariant)
     const int64_t T = ceil_div(n, (int64_t)kSymRows);
     auto cost_before = [&](int64_t I) { return (double)I * n - 0.5 * kSymRows * (double)I * (I - 1); };
     auto range = [&](int r, int64_t& a0, int64_t& a1) {
@@ -320,7 +319,7 @@ void cov_matvec_dev(Ctx& c, const mlk_tree_s* tree, const mlk_kernel& k, const d
       u.w_col0 = r;
       u.w_cols = n;
       u.cp_off = off;
-      off += 4 * (int64_t)nvec * (n - r);
+      off += (int64_t)nvec * (n - r);
     }
     DevBuf<double> colpart(std::max<int64_t>(cp, 1), c.stream);
     run_tile_contract(c, tree, make_kernel_params(k), units, "cov_matvec_tile", colpart.p);

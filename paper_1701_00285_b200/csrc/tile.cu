@@ -153,9 +153,12 @@ struct TileCfg {
 
 // stage size rounded to 128 bytes: 2-D TMA writes need 128-byte aligned shared destinations
 // (the W part starts BN sdp doubles in, a multiple of 128 bytes since sdp is a multiple of 4)
-__host__ __device__ constexpr int stage_doubles(int rq, int bn, int sdp) {
-  return (bn * sdp + (8 * rq + tile_max_nr(rq)) * bn + 15) / 16 * 16;
+__host__ __device__ constexpr int stage_doubles(int rq, int bn, int sdp, int red = 0) {
+  return (bn * sdp + (8 * rq + tile_max_nr(rq)) * bn + red + 15) / 16 * 16;
 }
+// SYM: per stage, the four warps' column partials (4 x NV x BN doubles) for the last warp's
+// fixed-order sum
+__host__ __device__ constexpr int sym_red_doubles(bool sym, int nv, int bn) { return sym ? 4 * nv * bn : 0; }
 
 // Augmented, pre-scaled coordinates (x in tree order, s = kp.scale, u = s x), dpa doubles per row.
 // Augmented mode (dk == dpa = pad4(d + 2)):
@@ -221,7 +224,9 @@ __global__ void __launch_bounds__(128, TileCfg<RQ>::MIN_CTAS)
   __shared__ int s_unit;
   __shared__ double s_tab[kExpTabN];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int sd = stage_doubles(RQ, BN, sdp);
+  constexpr int RED = sym_red_doubles(SYM, NV, BN);
+  const int sd = stage_doubles(RQ, BN, sdp, RED);
+  const int red_off = stage_doubles(RQ, BN, sdp);  // the stage's reduction area (SYM)
   double* As = sm;                  // 32 x sdp
   double* St = sm + 32 * sdp;       // nring stages
   for (int i = tid; i < kExpTabN; i += blockDim.x) s_tab[i] = kExp2Tab[i];
@@ -492,7 +497,7 @@ __global__ void __launch_bounds__(128, TileCfg<RQ>::MIN_CTAS)
           for (int q = 0; q < Q; q++) {
             const int idx = r * Q + q;
             const int y = yb + 8 * (idx >> 1) + 2 * (lane & 3) + (idx & 1);
-            if (idx < NVAL && y < u.s_b && u.qc > 0) colpart[u.cp_off + (int64_t)warp * u.s_b + y] = v[q];
+            if (idx < NVAL) const_cast<double*>(Xs)[red_off + warp * BN + (y - yb)] = v[q];
           }
         } else if constexpr (SYM) {
           // column part: sum over the warp's 8 rows (lanes with equal lane & 3), lanes 0..3
@@ -508,8 +513,7 @@ __global__ void __launch_bounds__(128, TileCfg<RQ>::MIN_CTAS)
                 v += __shfl_xor_sync(0xffffffffu, v, 8);
                 v += __shfl_xor_sync(0xffffffffu, v, 16);
                 const int y = yb + 8 * t + 2 * lane + e;
-                if (lane < 4 && y < u.s_b && l < u.qc)
-                  colpart[u.cp_off + ((int64_t)warp * u.qc + l) * u.s_b + y] = v;
+                if (lane < 4) const_cast<double*>(Xs)[red_off + (warp * NV + l) * BN + (y - yb)] = v;
               }
             }
           }
@@ -558,11 +562,25 @@ __global__ void __launch_bounds__(128, TileCfg<RQ>::MIN_CTAS)
         }
       }
       // release the slot: the last of the four warps refills it with stage s + nring
+      if constexpr (SYM) __threadfence_block();  // the column partials, before the count
       __syncwarp();
       int last = 0;
       if (lane == 0) last = atomicAdd(&cnt[slot], 1) == 3;
       last = __shfl_sync(0xffffffffu, last, 0);
       if (last) {
+        if constexpr (SYM) {
+          // the stage's column partials of the CTA's 32 rows: warps 0..3 summed in order
+          __threadfence_block();
+          const double* rd = Xs + red_off;
+          for (int e = lane; e < NV * BN; e += 32) {
+            const int l = e / BN, y = e - l * BN;
+            if (yb + y < u.s_b && l < u.qc)
+              colpart[u.cp_off + (int64_t)l * u.s_b + yb + y] =
+                  ((rd[(0 * NV + l) * BN + y] + rd[(1 * NV + l) * BN + y]) + rd[(2 * NV + l) * BN + y]) +
+                  rd[(3 * NV + l) * BN + y];
+          }
+          __syncwarp();
+        }
         if (lane == 0) cnt[slot] = 0;
         if (s + nring < nst) issue(s + nring, slot);  // stage s + nring reuses this slot
       }
@@ -675,7 +693,8 @@ void launch_class(Ctx& c, const AugArgs& ag, const KernelParams& kp, const TileU
   Cfg& cf = cache[{c.device, ag.sdp}];
   if (cf.nring == 0) {
     for (int ns = TileCfg<RQ>::NST; ns >= 2; ns--) {
-      const size_t sm_ns = sizeof(double) * (size_t)(32 * ag.sdp + ns * stage_doubles(RQ, BN, ag.sdp));
+      const size_t sm_ns =
+          sizeof(double) * (size_t)(32 * ag.sdp + ns * stage_doubles(RQ, BN, ag.sdp, sym_red_doubles(SYM, NV, BN)));
       if (sm_ns > 227 * 1024) continue;
       CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_ns));
       attr[c.device] = sm_ns;
@@ -756,11 +775,18 @@ void tile_aug_layout(int d, AugCoords& a) {
   a.sdp = ((a.dpa >> 2) & 1) ? a.dpa : a.dpa + 4;
 }
 
-void tile_aug_fill(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, AugCoords& a) {
-  if (a.buf.n < (size_t)2 * tree->n * a.dpa) a.buf.alloc((size_t)2 * tree->n * a.dpa, c.stream);
+const double* tile_aug_get(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, const AugCoords& a) {
+  const size_t need = (size_t)2 * tree->n * a.dpa;
+  if (tree->aug.p && tree->aug.n == need && tree->aug_scale == kp.scale && tree->aug_dpa == a.dpa)
+    return tree->aug.p;
+  if (tree->aug.n != need) tree->aug.alloc(need, c.stream);
   k_tile_aug<<<(unsigned)ceil_div(tree->n, 256), 256, 0, c.stream>>>(tree->Xt.p, tree->d_pad, tree->d, tree->n,
-                                                                     kp.scale, a.Pa(), a.Pb(tree->n), a.dpa, a.dk);
+                                                                     kp.scale, tree->aug.p,
+                                                                     tree->aug.p + (size_t)tree->n * a.dpa, a.dpa, a.dk);
   check_launch("k_tile_aug");
+  tree->aug_scale = kp.scale;
+  tree->aug_dpa = a.dpa;
+  return tree->aug.p;
 }
 
 void run_tile_contract(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, std::vector<TileUnit>& units,
@@ -811,9 +837,8 @@ void run_tile_contract(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, s
   ag.dk = aug.dk;
   ag.dpa = aug.dpa;
   ag.sdp = aug.sdp;
-  aug.buf.alloc((size_t)2 * tree->n * ag.dpa, c.stream);
-  ag.Pa = aug.buf.p;
-  ag.Pb = aug.buf.p + (size_t)tree->n * ag.dpa;
+  ag.Pa = tile_aug_get(c, tree, kp, aug);  // formed on the stream here unless cached
+  ag.Pb = ag.Pa + (size_t)tree->n * ag.dpa;
   // tensor maps: one for the b rows per stage width, one per distinct W_b (base, shape, box)
   std::vector<CUtensorMap> maps;
   {
@@ -854,7 +879,6 @@ void run_tile_contract(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, s
   ntask_d.upload(ntask);
   DevBuf<int32_t> task_range((size_t)std::max<int64_t>(tasks_total, 1), c.stream);
   TimedLaunch tl(c, name);
-  tile_aug_fill(c, tree, kp, aug);
   for (size_t g = 0; g + 1 < starts.size(); g++) {
     const int s0 = starts[g], nr_ = starts[g + 1] - starts[g];
     k_expand_tasks<<<(unsigned)nr_, 128, 0, c.stream>>>(first_d.p + s0, ntask_d.p + s0, nr_,

@@ -75,16 +75,15 @@ void run_tile_contract(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, s
 void make_tile_units(std::vector<TileUnit>& out, int64_t a_begin, int32_t s_a, int64_t b_begin, int32_t s_b,
                      const double* Wb, int64_t ldw, int32_t p_b, double* U, int64_t ldu, int32_t trans, int dp);
 
-// Augmented, pre-scaled coordinates Pa, Pb (n x dpa each, one buffer) of the Gram product
-// (tile.cu k_tile_aug): dk Gram columns, dpa doubles per row, sdp = shared-memory row stride.
+// Layout of the augmented, pre-scaled coordinates Pa, Pb (n x dpa each, one buffer) of the Gram
+// product (tile.cu k_tile_aug): dk Gram columns, dpa doubles per row, sdp = shared-memory row
+// stride.  tile_aug_get returns Pa (Pb = Pa + n dpa), formed on the context stream unless the
+// tree's cache already holds them for this scale.
 struct AugCoords {
-  DevBuf<double> buf;
   int dpa = 0, dk = 0, sdp = 0;
-  double* Pa() const { return buf.p; }
-  double* Pb(int64_t n) const { return buf.p + (size_t)n * dpa; }
 };
 void tile_aug_layout(int d, AugCoords& a);
-void tile_aug_fill(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, AugCoords& a);
+const double* tile_aug_get(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, const AugCoords& a);
 // row-major FP64 matrix (rows x cols, row stride ld elements) read by TMA in boxes of
 // box_rows x box_cols (out-of-range elements zero-filled)
 CUtensorMap make_map_2d(const double* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_rows,
