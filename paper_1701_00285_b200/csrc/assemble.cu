@@ -66,14 +66,23 @@ __global__ void k_proj_minmax(const double* __restrict__ Xt, int dp, int d, cons
   }
   for (int64_t k = lbeg[leaf] + threadIdx.x; k < lend[leaf]; k += blockDim.x) {
     const double* x = Xt + k * dp;
+    // the kMmQ projections advance together coordinate by coordinate (each x_j loaded once,
+    // kMmQ independent add chains); every projection keeps its left-to-right order (R6)
+    double acc[kMmQ];
+    const double x0 = x[0];
+#pragma unroll
+    for (int i = 0; i < kMmQ; i++) acc[i] = i < nq ? __dmul_rn(x0, sv[i * d]) : 0.0;
+    for (int j = 1; j < d; j++) {
+      const double xj = x[j];
+#pragma unroll
+      for (int i = 0; i < kMmQ; i++)
+        if (i < nq) acc[i] = __dadd_rn(acc[i], __dmul_rn(xj, sv[i * d + j]));
+    }
 #pragma unroll
     for (int i = 0; i < kMmQ; i++) {
       if (i < nq) {
-        const double* v = sv + i * d;
-        double acc = __dmul_rn(x[0], v[0]);
-        for (int j = 1; j < d; j++) acc = __dadd_rn(acc, __dmul_rn(x[j], v[j]));
-        mn[i] = fmin(mn[i], acc);
-        mx[i] = fmax(mx[i], acc);
+        mn[i] = fmin(mn[i], acc[i]);
+        mx[i] = fmax(mx[i], acc[i]);
       }
     }
   }
