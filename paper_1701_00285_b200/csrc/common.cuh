@@ -90,8 +90,14 @@ struct TimedLaunch {
   ~TimedLaunch() {
     if (!c.timing || a == nullptr) return;
     cudaEvent_t b = nullptr;
-    if (cudaEventCreate(&b) != cudaSuccess || cudaEventRecord(b, c.stream) != cudaSuccess) {
-      if (b) cudaEventDestroy(b);
+    if (!c.event_pool.empty()) {  // pooled (set_timing pre-creates them): no driver call here
+      b = c.event_pool.back();
+      c.event_pool.pop_back();
+    } else if (cudaEventCreate(&b) != cudaSuccess) {
+      b = nullptr;
+    }
+    if (b == nullptr || cudaEventRecord(b, c.stream) != cudaSuccess) {
+      if (b) c.event_pool.push_back(b);
       c.event_pool.push_back(a);
       return;
     }

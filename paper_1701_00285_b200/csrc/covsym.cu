@@ -312,7 +312,7 @@ __global__ void k_sym_chunks(const double* __restrict__ colpart, int64_t t0, int
 // b[l][j] = sigma2 ((row partials of j's task, warps 0..3) + sum over chunks c of tmp)
 __global__ void k_sym_final(const double* __restrict__ tmp, const double* __restrict__ rowpart, int64_t t0,
                             int64_t t1, int64_t n, int nvec, int nchunks, double sigma2, double* __restrict__ b,
-                            int64_t ldb) {
+                            int64_t ldb, int accumulate) {
   const int64_t j = kSymRows * t0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int l = blockIdx.y;
   if (j >= n) return;
@@ -324,7 +324,8 @@ __global__ void k_sym_final(const double* __restrict__ tmp, const double* __rest
   }
   double t = 0.0;
   for (int c = 0; c < nchunks; c++) t += tmp[((int64_t)l * nchunks + c) * n + j];
-  b[(int64_t)l * ldb + j] = sigma2 * (s + t);
+  double* bp = b + (int64_t)l * ldb + j;
+  *bp = accumulate ? *bp + sigma2 * (s + t) : sigma2 * (s + t);
 }
 
 template <int FAM, int G>
@@ -397,6 +398,12 @@ int64_t cov_sym_partials(int64_t n, int nvec, int64_t t0, int64_t t1) {
   return t1 > t0 ? sym_off(t1, t0, n, std::min(nvec, 16)) : 0;
 }
 
+// Tasks in batches whose column partials fit an eighth of the device (a function of n, nvec and
+// the device's total memory only, so every rank cuts the same batches; cfg3's 10 vectors: one
+// batch of 21 GB, cfg4's: four).  Batches of 2 GB measured 34 % slower on cfg3 (59.8 against
+// 44.7 ms: eleven launches with their tails).  All buffers are allocated before the timed region
+// (an allocation inside it once stalled the stream by 50-150 ms, r02 bn).  Batch k adds its
+// part of b in batch order: deterministic.
 void cov_matvec_sym(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, const double* a, double* b, int nvec,
                     int64_t t0, int64_t t1) {
   const int64_t n = tree->n;
@@ -404,13 +411,30 @@ void cov_matvec_sym(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, cons
   AugCoords aug;
   tile_aug_layout(tree->d, aug);
   const int64_t ld = (n + 7) / 8 * 8;
+  const int64_t batch_doubles = std::max<int64_t>(device_total_bytes(c.device) / 8 / 8, 4 * n);
   for (int v0 = 0; v0 < nvec; v0 += 16) {
     const int nv = std::min(16, nvec - v0);
     const int G = nv <= 8 ? 1 : 2;
+    // batches [bt[k], bt[k + 1])
+    std::vector<int64_t> bt = {t0};
+    int64_t cp_max = 0, rows_max = 0;
+    for (int64_t I = t0, acc = 0; I < t1; I++) {
+      const int64_t w = (int64_t)nv * (n - kSymRows * I);
+      if (acc > 0 && acc + w > batch_doubles) {
+        bt.push_back(I);
+        acc = 0;
+      }
+      acc += w;
+      cp_max = std::max(cp_max, acc);
+    }
+    bt.push_back(t1);
+    for (size_t k = 0; k + 1 < bt.size(); k++) rows_max = std::max(rows_max, bt[k + 1] - bt[k]);
     DevBuf<double> apad((size_t)8 * G * ld, c.stream);
-    DevBuf<double> colpart((size_t)std::max<int64_t>(cov_sym_partials(n, nv, t0, t1), 1), c.stream);
-    DevBuf<double> rowpart((size_t)(t1 - t0) * 4 * nv * kSymRows, c.stream);
-    DevBuf<int> counter(1, c.stream);
+    DevBuf<double> colpart((size_t)std::max<int64_t>(cp_max, 1), c.stream);
+    DevBuf<double> rowpart((size_t)rows_max * 4 * nv * kSymRows, c.stream);
+    const int nchunks_max = (int)ceil_div(rows_max, (int64_t)kSymChunk);
+    DevBuf<double> tmp((size_t)nv * nchunks_max * n, c.stream);
+    DevBuf<int> counter(bt.size(), c.stream);
     counter.zero();
     TimedLaunch tl(c, "cov_matvec_sym");
     const double* Pa = tile_aug_get(c, tree, kp, aug);
@@ -421,35 +445,37 @@ void cov_matvec_sym(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, cons
                                      make_map_2d(apad.p, 8 * G, ld, ld, 8 * G, kBN)};
     DevBuf<CUtensorMap> maps_d(2, c.stream);
     maps_d.upload(maps);
-    SymArgs ag;
-    ag.Pa = Pa;
-    ag.dpa = aug.dpa;
-    ag.dk = aug.dk;
-    ag.sdp = aug.sdp;
-    ag.a = apad.p;
-    ag.lda = ld;
-    ag.nvec = nv;
-    ag.n = n;
-    ag.t0 = t0;
-    ag.t1 = t1;
-    ag.xmap = maps_d.p;
-    ag.amap = maps_d.p + 1;
-    ag.colpart = colpart.p;
-    ag.rowpart = rowpart.p;
-    ag.counter = counter.p;
-    ag.nring = 0;
-    if (G == 1) launch_sym_fam<1>(c, ag, kp, t1 - t0);
-    else launch_sym_fam<2>(c, ag, kp, t1 - t0);
-    const int nchunks = (int)ceil_div(t1 - t0, (int64_t)kSymChunk);
-    DevBuf<double> tmp((size_t)nv * nchunks * n, c.stream);
-    const int64_t jn = n - kSymRows * t0;
-    dim3 g1((unsigned)ceil_div(jn, (int64_t)256), (unsigned)nchunks, (unsigned)nv);
-    k_sym_chunks<<<g1, 256, 0, c.stream>>>(colpart.p, t0, t1, n, nv, nchunks, tmp.p);
-    check_launch("k_sym_chunks");
-    dim3 g2((unsigned)ceil_div(jn, (int64_t)256), (unsigned)nv);
-    k_sym_final<<<g2, 256, 0, c.stream>>>(tmp.p, rowpart.p, t0, t1, n, nv, nchunks, kp.sigma2,
-                                          b + (int64_t)v0 * n + 0, n);
-    check_launch("k_sym_final");
+    for (size_t k = 0; k + 1 < bt.size(); k++) {
+      const int64_t b0 = bt[k], b1 = bt[k + 1];
+      SymArgs ag;
+      ag.Pa = Pa;
+      ag.dpa = aug.dpa;
+      ag.dk = aug.dk;
+      ag.sdp = aug.sdp;
+      ag.a = apad.p;
+      ag.lda = ld;
+      ag.nvec = nv;
+      ag.n = n;
+      ag.t0 = b0;
+      ag.t1 = b1;
+      ag.xmap = maps_d.p;
+      ag.amap = maps_d.p + 1;
+      ag.colpart = colpart.p;
+      ag.rowpart = rowpart.p;
+      ag.counter = counter.p + k;
+      ag.nring = 0;
+      if (G == 1) launch_sym_fam<1>(c, ag, kp, b1 - b0);
+      else launch_sym_fam<2>(c, ag, kp, b1 - b0);
+      const int nchunks = (int)ceil_div(b1 - b0, (int64_t)kSymChunk);
+      const int64_t jn = n - kSymRows * b0;
+      dim3 g1((unsigned)ceil_div(jn, (int64_t)256), (unsigned)nchunks, (unsigned)nv);
+      k_sym_chunks<<<g1, 256, 0, c.stream>>>(colpart.p, b0, b1, n, nv, nchunks, tmp.p);
+      check_launch("k_sym_chunks");
+      dim3 g2((unsigned)ceil_div(jn, (int64_t)256), (unsigned)nv);
+      k_sym_final<<<g2, 256, 0, c.stream>>>(tmp.p, rowpart.p, b0, b1, n, nv, nchunks, kp.sigma2,
+                                            b + (int64_t)v0 * n, n, k > 0 ? 1 : 0);
+      check_launch("k_sym_final");
+    }
   }
 }
 

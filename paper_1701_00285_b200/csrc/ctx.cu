@@ -280,6 +280,13 @@ mlk_status mlk_ctx_set_timing(mlk_ctx ctx, int enable) {
   MLK_REQUIRE(ctx, "ctx is NULL");
   ctx->c.flush_timing();
   ctx->c.timing = enable != 0;
+  // pre-create the events of a few steps' timed launches, so that recording them inside a
+  // timed region never waits on cudaEventCreate
+  while (enable && ctx->c.event_pool.size() < 8192) {
+    cudaEvent_t e;
+    CUDA_CHECK(cudaEventCreate(&e));
+    ctx->c.event_pool.push_back(e);
+  }
   MLK_API_END
 }
 

@@ -18,46 +18,109 @@ struct CellJob {
   const double* W;    // p x s
 };
 
-// a[v][begin + x] += sum_r W[r][x] v[v][row_off + r] for the cells of one level
+// a[v][begin + x] += sum_r W[r][x] v[v][row_off + r] for the cells of one level; the vectors in
+// groups of kAwVG, so each W element is read once per group (not once per vector)
+constexpr int kAwVG = 8;
+template <int VG>
 __global__ void k_apply_wt(const CellJob* __restrict__ jobs, const double* __restrict__ v, int64_t dim,
                            double* __restrict__ a, int64_t n, int nvec) {
   const CellJob jb = jobs[blockIdx.x];
   for (int x = blockIdx.y * blockDim.x + threadIdx.x; x < jb.s; x += gridDim.y * blockDim.x) {
-    for (int iv = 0; iv < nvec; iv++) {
-      const double* vv = v + (int64_t)iv * dim + jb.row_off;
-      // four partial sums: four independent W loads in flight per thread (the pass is bound by
-      // memory-level parallelism, one accumulator left it latency-bound at ~0.5 TB/s)
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    for (int iv0 = 0; iv0 < nvec; iv0 += VG) {
+      const int nv = min(VG, nvec - iv0);
+      const double* vv = v + (int64_t)iv0 * dim + jb.row_off;
+      // four partial sums per vector: four independent W loads in flight per thread (the pass is
+      // bound by memory-level parallelism, one accumulator left it latency-bound at ~0.5 TB/s)
+      double s0[VG], s1[VG], s2[VG], s3[VG];
+#pragma unroll
+      for (int q = 0; q < VG; q++) s0[q] = s1[q] = s2[q] = s3[q] = 0.0;
       const double* w = jb.W + x;
       int r = 0;
       for (; r + 3 < jb.p; r += 4) {
-        s0 = fma(w[(int64_t)r * jb.s], vv[r], s0);
-        s1 = fma(w[(int64_t)(r + 1) * jb.s], vv[r + 1], s1);
-        s2 = fma(w[(int64_t)(r + 2) * jb.s], vv[r + 2], s2);
-        s3 = fma(w[(int64_t)(r + 3) * jb.s], vv[r + 3], s3);
+        const double w0 = w[(int64_t)r * jb.s], w1 = w[(int64_t)(r + 1) * jb.s], w2 = w[(int64_t)(r + 2) * jb.s],
+                     w3 = w[(int64_t)(r + 3) * jb.s];
+#pragma unroll
+        for (int q = 0; q < VG; q++) {
+          if (q < nv) {
+            const double* vq = vv + (int64_t)q * dim;
+            s0[q] = fma(w0, vq[r], s0[q]);
+            s1[q] = fma(w1, vq[r + 1], s1[q]);
+            s2[q] = fma(w2, vq[r + 2], s2[q]);
+            s3[q] = fma(w3, vq[r + 3], s3[q]);
+          }
+        }
       }
-      for (; r < jb.p; r++) s0 = fma(w[(int64_t)r * jb.s], vv[r], s0);
-      a[(int64_t)iv * n + jb.pt_begin + x] += (s0 + s1) + (s2 + s3);
+      for (; r < jb.p; r++) {
+        const double w0 = w[(int64_t)r * jb.s];
+#pragma unroll
+        for (int q = 0; q < VG; q++)
+          if (q < nv) s0[q] = fma(w0, vv[(int64_t)q * dim + r], s0[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < VG; q++)
+        if (q < nv) a[(int64_t)(iv0 + q) * n + jb.pt_begin + x] += (s0[q] + s1[q]) + (s2[q] + s3[q]);
     }
   }
 }
 
-// y[v][row_off + r] = sum_x W[r][x] b[v][begin + x]; one warp per row
-__global__ void k_apply_w(const CellJob* __restrict__ jobs, const double* __restrict__ b, int64_t n,
-                          double* __restrict__ y, int64_t dim, int nvec) {
-  const CellJob jb = jobs[blockIdx.x];
-  const int lane = threadIdx.x & 31;
-  const int wid = blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int nw = gridDim.y * (blockDim.x >> 5);
-  for (int r = wid; r < jb.p; r += nw) {
+// y[v][row_off + r] = sum_x W[r][x] b[v][begin + x].  A CTA per (cell, chunk of kAwChunk
+// points), a warp per row, lanes strided over the chunk's points, vectors in groups of VG (each W
+// element read once per group); a cell of one chunk writes y, longer cells write per-chunk
+// partials that k_apply_w_reduce adds in chunk order (deterministic).  The root row's p rows
+// of n points were one warp each (latency-bound at cfg3: 3.4 ms for 10 vectors).
+constexpr int kAwChunk = 4096;
+struct WJob {
+  int32_t cell;     // index into the level-order job list
+  int32_t x0, x1;   // point range of the chunk
+  int64_t part;     // partial offset (doubles, nvec x p), or -1: write y
+};
+template <int VG>
+__global__ void k_apply_w(const CellJob* __restrict__ jobs, const WJob* __restrict__ wj, const double* __restrict__ b,
+                          int64_t n, double* __restrict__ y, int64_t dim, int nvec, double* __restrict__ part) {
+  const WJob w_ = wj[blockIdx.x];
+  const CellJob jb = jobs[w_.cell];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int r = warp; r < jb.p; r += nw) {
     const double* w = jb.W + (int64_t)r * jb.s;
-    for (int iv = 0; iv < nvec; iv++) {
-      const double* bb = b + (int64_t)iv * n + jb.pt_begin;
-      double s = 0.0;
-      for (int x = lane; x < jb.s; x += 32) s = fma(w[x], bb[x], s);
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) y[(int64_t)iv * dim + jb.row_off + r] = s;
+    for (int iv0 = 0; iv0 < nvec; iv0 += VG) {
+      const int nv = min(VG, nvec - iv0);
+      const double* bb = b + (int64_t)iv0 * n + jb.pt_begin;
+      double s[VG];
+#pragma unroll
+      for (int q = 0; q < VG; q++) s[q] = 0.0;
+      for (int x = w_.x0 + lane; x < w_.x1; x += 32) {
+        const double wx = w[x];
+#pragma unroll
+        for (int q = 0; q < VG; q++)
+          if (q < nv) s[q] = fma(wx, bb[(int64_t)q * n + x], s[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < VG; q++) {
+        if (q < nv) {  // warp-uniform
+          for (int o = 16; o > 0; o >>= 1) s[q] += __shfl_xor_sync(0xffffffffu, s[q], o);
+          if (lane == 0) {
+            if (w_.part < 0) y[(int64_t)(iv0 + q) * dim + jb.row_off + r] = s[q];
+            else part[w_.part + (int64_t)(iv0 + q) * jb.p + r] = s[q];
+          }
+        }
+      }
     }
+  }
+}
+
+struct WRed {
+  int32_t cell, nch;
+  int64_t part;  // first chunk's partials; chunk c at part + c nvec p
+};
+__global__ void k_apply_w_reduce(const CellJob* __restrict__ jobs, const WRed* __restrict__ rj,
+                                 const double* __restrict__ part, double* __restrict__ y, int64_t dim, int nvec) {
+  const WRed q = rj[blockIdx.x];
+  const CellJob jb = jobs[q.cell];
+  for (int e = threadIdx.x; e < nvec * jb.p; e += blockDim.x) {
+    const int iv = e / jb.p, r = e - iv * jb.p;
+    double s = 0.0;
+    for (int c = 0; c < q.nch; c++) s += part[q.part + (int64_t)c * nvec * jb.p + e];
+    y[(int64_t)iv * dim + jb.row_off + r] = s;
   }
 }
 
@@ -175,26 +238,47 @@ void apply_wt_dev(Ctx& c, const mlk_tree_s* tree, const mlk_basis_s* B, const do
     int smax = 0;
     for (auto& j : lv[dep]) smax = std::max(smax, j.s);
     dim3 grid((unsigned)lv[dep].size(), (unsigned)std::max<int64_t>(1, std::min<int64_t>(64, ceil_div(smax, 256))));
-    k_apply_wt<<<grid, 256, 0, c.stream>>>(dj.p, v, B->dim, a, tree->n, nvec);
+    if (nvec == 1) k_apply_wt<1><<<grid, 256, 0, c.stream>>>(dj.p, v, B->dim, a, tree->n, nvec);
+    else k_apply_wt<kAwVG><<<grid, 256, 0, c.stream>>>(dj.p, v, B->dim, a, tree->n, nvec);
     check_launch("k_apply_wt");
   }
 }
 
 void apply_w_dev(Ctx& c, const mlk_tree_s* tree, const mlk_basis_s* B, const double* b, double* y, int nvec) {
   std::vector<CellJob> all;
-  int pmax = 0;
   for (auto& l : level_jobs(tree, B))
-    for (auto& j : l) {
-      all.push_back(j);
-      pmax = std::max(pmax, j.p);
-    }
+    for (auto& j : l) all.push_back(j);
   if (all.empty()) return;
+  std::vector<WJob> wj;
+  std::vector<WRed> red;
+  int64_t parts = 0;
+  for (int32_t i = 0; i < (int32_t)all.size(); i++) {
+    const int32_t s = all[i].s, nch = (int32_t)ceil_div((int64_t)s, (int64_t)kAwChunk);
+    if (nch == 1) {
+      wj.push_back({i, 0, s, -1});
+      continue;
+    }
+    red.push_back({i, nch, parts});
+    for (int32_t ch = 0; ch < nch; ch++) {
+      wj.push_back({i, ch * kAwChunk, std::min(s, (ch + 1) * kAwChunk), parts});
+      parts += (int64_t)nvec * all[i].p;
+    }
+  }
   DevBuf<CellJob> dj(all.size(), c.stream);
   dj.upload(all);
+  DevBuf<WJob> dw(wj.size(), c.stream);
+  dw.upload(wj);
+  DevBuf<double> part((size_t)std::max<int64_t>(parts, 1), c.stream);
   TimedLaunch tl(c, "apply_w");
-  dim3 grid((unsigned)all.size(), (unsigned)std::max<int64_t>(1, std::min<int64_t>(32, ceil_div(pmax, 8))));
-  k_apply_w<<<grid, 256, 0, c.stream>>>(dj.p, b, tree->n, y, B->dim, nvec);
+  if (nvec == 1) k_apply_w<1><<<(unsigned)wj.size(), 256, 0, c.stream>>>(dj.p, dw.p, b, tree->n, y, B->dim, nvec, part.p);
+  else k_apply_w<kAwVG><<<(unsigned)wj.size(), 256, 0, c.stream>>>(dj.p, dw.p, b, tree->n, y, B->dim, nvec, part.p);
   check_launch("k_apply_w");
+  if (!red.empty()) {
+    DevBuf<WRed> dr(red.size(), c.stream);
+    dr.upload(red);
+    k_apply_w_reduce<<<(unsigned)red.size(), 256, 0, c.stream>>>(dj.p, dr.p, part.p, y, B->dim, nvec);
+    check_launch("k_apply_w_reduce");
+  }
 }
 
 // Symmetric C a column partials: tile I (of this rank's t0..t1-1) holds nvec rows of n - 32 I
@@ -264,8 +348,8 @@ void cov_matvec_dev(Ctx& c, const mlk_tree_s* tree, const mlk_kernel& k, const d
   const char* smn = std::getenv("MLK_SYM_MIN_NVEC");
   if (nvec >= (smn ? std::atoi(smn) : 5) && !nosym) {
     // 5 or more vectors: the symmetric kernel with DMMA contractions (covsym.cu), tasks of
-    // kSymRows rows split by their triangular costs n - kSymRows I; its column partials
-    // (n^2 min(nvec, 16) / 64 doubles in all) must fit a quarter of the device (rank-invariant)
+    // kSymRows rows split by their triangular costs n - kSymRows I (rank-invariant); it bounds
+    // its column partials by processing the tasks in batches
     const int64_t T = ceil_div(n, (int64_t)kSymRows);
     auto cost_before = [&](int64_t I) { return (double)I * n - 0.5 * kSymRows * (double)I * (I - 1); };
     auto range = [&](int r, int64_t& a0, int64_t& a1) {
@@ -276,18 +360,10 @@ void cov_matvec_dev(Ctx& c, const mlk_tree_s* tree, const mlk_kernel& k, const d
       while (a1 < T && cost_before(a1 + 1) <= total * (r + 1) / c.nranks) a1++;
       if (r == c.nranks - 1) a1 = T;
     };
-    int64_t worst = 0;
-    for (int r = 0; r < c.nranks; r++) {
-      int64_t a0, a1;
-      range(r, a0, a1);
-      worst = std::max(worst, cov_sym_partials(n, nvec, a0, a1));
-    }
-    if (worst * (int64_t)sizeof(double) <= device_total_bytes(c.device) / 4) {
-      int64_t a0, a1;
-      range(c.rank, a0, a1);
-      cov_matvec_sym(c, tree, make_kernel_params(k), a, b, nvec, a0, a1);
-      return;
-    }
+    int64_t a0, a1;
+    range(c.rank, a0, a1);
+    cov_matvec_sym(c, tree, make_kernel_params(k), a, b, nvec, a0, a1);
+    return;
   }
   bool sym = nvec <= 4 && !nosym;
   if (sym) {

@@ -132,6 +132,9 @@ namespace {
 #ifndef MLK_MINCTAS_SMALL
 #define MLK_MINCTAS_SMALL 5  // 5 CTAs: cfg3 K5a 250.6 -> 246.3 ms (r02d)
 #endif
+#ifndef MLK_BN_ONE
+#define MLK_BN_ONE 56
+#endif
 #ifndef MLK_BN_SMALL
 #define MLK_BN_SMALL 40
 #endif
@@ -140,7 +143,7 @@ struct TileCfg {
   // b points per stage.  BN = 8 (mod 16) makes a W row 8 BN doubles = 64 (mod 128) bytes, so
   // the 16-byte B-fragment loads of a quarter-warp (2 rows x 4 chunks) hit distinct banks
   // without any swizzle -- which a 1-D bulk copy could not apply
-  static constexpr int BN = RQ >= 6 ? 24 : (RQ == 1 ? 56 : MLK_BN_SMALL);  // 40 for RQ 6-9 measured 13 % slower on cfg4
+  static constexpr int BN = RQ >= 6 ? 24 : (RQ == 1 ? MLK_BN_ONE : MLK_BN_SMALL);  // 40 for RQ 6-9 measured 13 % slower on cfg4
   // maximum stages in the smem ring (the launch uses the deepest ring that keeps the target
   // occupancy, >= 2): the one-group class (C a, tiny cells) has short stages, so it wants a
   // deeper ring to cover the TMA latency
@@ -153,8 +156,11 @@ struct TileCfg {
 
 // stage size rounded to 128 bytes: 2-D TMA writes need 128-byte aligned shared destinations
 // (the W part starts BN sdp doubles in, a multiple of 128 bytes since sdp is a multiple of 4)
-__host__ __device__ constexpr int stage_doubles(int rq, int bn, int sdp, int red = 0) {
-  return (bn * sdp + (8 * rq + tile_max_nr(rq)) * bn + red + 15) / 16 * 16;
+// W_b rows a stage holds: 8 rq + the DFMA remainder rows, or NV for the C a variants (their
+// tensor map box covers only the vector rows)
+__host__ __device__ constexpr int stage_wrows(int rq, int nv) { return nv > 0 ? nv : 8 * rq + tile_max_nr(rq); }
+__host__ __device__ constexpr int stage_doubles(int rq, int bn, int sdp, int red = 0, int nv = 0) {
+  return (bn * sdp + stage_wrows(rq, nv) * bn + red + 15) / 16 * 16;
 }
 // SYM: per stage, the four warps' column partials (4 x NV x BN doubles) for the last warp's
 // fixed-order sum
@@ -225,8 +231,8 @@ __global__ void __launch_bounds__(128, TileCfg<RQ>::MIN_CTAS)
   __shared__ double s_tab[kExpTabN];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int RED = sym_red_doubles(SYM, NV, BN);
-  const int sd = stage_doubles(RQ, BN, sdp, RED);
-  const int red_off = stage_doubles(RQ, BN, sdp);  // the stage's reduction area (SYM)
+  const int sd = stage_doubles(RQ, BN, sdp, RED, NV);
+  const int red_off = stage_doubles(RQ, BN, sdp, 0, NV);  // the stage's reduction area (SYM)
   double* As = sm;                  // 32 x sdp
   double* St = sm + 32 * sdp;       // nring stages
   for (int i = tid; i < kExpTabN; i += blockDim.x) s_tab[i] = kExp2Tab[i];
@@ -694,7 +700,7 @@ void launch_class(Ctx& c, const AugArgs& ag, const KernelParams& kp, const TileU
   if (cf.nring == 0) {
     for (int ns = TileCfg<RQ>::NST; ns >= 2; ns--) {
       const size_t sm_ns =
-          sizeof(double) * (size_t)(32 * ag.sdp + ns * stage_doubles(RQ, BN, ag.sdp, sym_red_doubles(SYM, NV, BN)));
+          sizeof(double) * (size_t)(32 * ag.sdp + ns * stage_doubles(RQ, BN, ag.sdp, sym_red_doubles(SYM, NV, BN), NV));
       if (sm_ns > 227 * 1024) continue;
       CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_ns));
       attr[c.device] = sm_ns;
