@@ -839,6 +839,18 @@ mlk_status mlk_assemble_cw_ex(mlk_ctx ctx, mlk_tree tree, mlk_basis basis, const
         }
         DevBuf<uint8_t> vflag_d(std::max<size_t>(vflag.size(), 1), st);
         vflag_d.upload(vflag);
+        if (trace.on && ui == 0) {  // V_c blocks per level (MLK_TRACE)
+          for (int dep = 0; dep < tree->t; dep++) {
+            int64_t on = 0, tot = 0;
+            for (int64_t q = (1 << dep) - 1; q < (2 << dep) - 1 && q < nn; q++) {
+              if (vflag_off[q] < 0) continue;
+              for (int64_t bk = 0; bk < nblk; bk++) on += vflag[vflag_off[q] + bk];
+              tot += nblk;
+            }
+            std::fprintf(stderr, "[mlk] nested chunk 0 level %d: V_c needed in %lld of %lld 64-row blocks\n", dep,
+                         (long long)on, (long long)tot);
+          }
+        }
         for (int dep = tree->t - 1; dep >= 0; dep--) {
           std::vector<GemmDesc> gd;
           std::vector<std::array<const double*, 4>> tj;

@@ -69,6 +69,11 @@ struct Ctx {
   cudaEvent_t copy_ready = nullptr;
   void* comm = nullptr;                // ncclComm_t of mlk_ctx_create with a unique id (comm.cu)
   int64_t scratch_budget_bytes();
+  // grow-only scratch buffers kept across calls (ctx.cu): the symmetric C a kernels' partials
+  // (up to a few x 10 GB) are re-used instead of re-allocated per product -- a stream-ordered
+  // allocation of that size, when the pool must map memory, stalled the step by up to 80 ms (r02)
+  std::map<std::string, std::pair<void*, size_t>> scratch_cache;
+  double* scratch(const char* key, size_t doubles);
 
   cudaEvent_t get_event();
   void flush_timing();  // synchronize and fold pending events into stats

@@ -430,10 +430,10 @@ void cov_matvec_sym(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, cons
     bt.push_back(t1);
     for (size_t k = 0; k + 1 < bt.size(); k++) rows_max = std::max(rows_max, bt[k + 1] - bt[k]);
     DevBuf<double> apad((size_t)8 * G * ld, c.stream);
-    DevBuf<double> colpart((size_t)std::max<int64_t>(cp_max, 1), c.stream);
+    double* colpart = c.scratch("sym_colpart", (size_t)cp_max);
     DevBuf<double> rowpart((size_t)rows_max * 4 * nv * kSymRows, c.stream);
     const int nchunks_max = (int)ceil_div(rows_max, (int64_t)kSymChunk);
-    DevBuf<double> tmp((size_t)nv * nchunks_max * n, c.stream);
+    double* tmp = c.scratch("sym_tmp", (size_t)nv * nchunks_max * n);
     DevBuf<int> counter(bt.size(), c.stream);
     counter.zero();
     TimedLaunch tl(c, "cov_matvec_sym");
@@ -460,7 +460,7 @@ void cov_matvec_sym(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, cons
       ag.t1 = b1;
       ag.xmap = maps_d.p;
       ag.amap = maps_d.p + 1;
-      ag.colpart = colpart.p;
+      ag.colpart = colpart;
       ag.rowpart = rowpart.p;
       ag.counter = counter.p + k;
       ag.nring = 0;
@@ -469,10 +469,10 @@ void cov_matvec_sym(Ctx& c, const mlk_tree_s* tree, const KernelParams& kp, cons
       const int nchunks = (int)ceil_div(b1 - b0, (int64_t)kSymChunk);
       const int64_t jn = n - kSymRows * b0;
       dim3 g1((unsigned)ceil_div(jn, (int64_t)256), (unsigned)nchunks, (unsigned)nv);
-      k_sym_chunks<<<g1, 256, 0, c.stream>>>(colpart.p, b0, b1, n, nv, nchunks, tmp.p);
+      k_sym_chunks<<<g1, 256, 0, c.stream>>>(colpart, b0, b1, n, nv, nchunks, tmp);
       check_launch("k_sym_chunks");
       dim3 g2((unsigned)ceil_div(jn, (int64_t)256), (unsigned)nv);
-      k_sym_final<<<g2, 256, 0, c.stream>>>(tmp.p, rowpart.p, b0, b1, n, nv, nchunks, kp.sigma2,
+      k_sym_final<<<g2, 256, 0, c.stream>>>(tmp, rowpart.p, b0, b1, n, nv, nchunks, kp.sigma2,
                                             b + (int64_t)v0 * n, n, k > 0 ? 1 : 0);
       check_launch("k_sym_final");
     }

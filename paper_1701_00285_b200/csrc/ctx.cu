@@ -128,6 +128,26 @@ int64_t Ctx::scratch_budget_bytes() {
   return std::max<int64_t>(avail / 3, (int64_t)256 << 20);
 }
 
+double* Ctx::scratch(const char* key, size_t doubles) {
+  auto& e = scratch_cache[key];
+  const size_t bytes = std::max<size_t>(doubles, 1) * sizeof(double);
+  if (e.first && e.second >= bytes) return static_cast<double*>(e.first);
+  if (e.first) {
+    CUDA_CHECK(cudaFreeAsync(e.first, stream));
+    g_live_bytes.fetch_sub((int64_t)e.second, std::memory_order_relaxed);
+    e = {nullptr, 0};
+  }
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, bytes, stream) != cudaSuccess) {
+    cudaGetLastError();
+    CUDA_CHECK(cudaDeviceSynchronize());
+    CUDA_CHECK(cudaMallocAsync(&p, bytes, stream));
+  }
+  g_live_bytes.fetch_add((int64_t)bytes, std::memory_order_relaxed);
+  e = {p, bytes};
+  return static_cast<double*>(p);
+}
+
 cudaEvent_t Ctx::get_event() {
   if (!event_pool.empty()) {
     cudaEvent_t e = event_pool.back();
@@ -246,6 +266,9 @@ void mlk_ctx_destroy(mlk_ctx ctx) {
     cudaEventDestroy(p.b);
   }
   for (auto e : ctx->c.event_pool) cudaEventDestroy(e);
+  for (auto& s : ctx->c.scratch_cache)
+    if (s.second.first) cudaFreeAsync(s.second.first, ctx->c.stream);
+  cudaStreamSynchronize(ctx->c.stream);
   if (ctx->c.aux_stream) {
     cudaStreamSynchronize(ctx->c.aux_stream);
     cudaStreamDestroy(ctx->c.aux_stream);

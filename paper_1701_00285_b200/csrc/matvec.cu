@@ -397,16 +397,16 @@ void cov_matvec_dev(Ctx& c, const mlk_tree_s* tree, const mlk_kernel& k, const d
       u.cp_off = off;
       off += (int64_t)nvec * (n - r);
     }
-    DevBuf<double> colpart(std::max<int64_t>(cp, 1), c.stream);
-    run_tile_contract(c, tree, make_kernel_params(k), units, "cov_matvec_tile", colpart.p);
-    TimedLaunch tl(c, "cov_matvec_colsum");
+    double* colpart = c.scratch("sym4_colpart", (size_t)cp);
     const int nchunks = (int)ceil_div(t1 - t0, kColChunk);
-    DevBuf<double> tmp((size_t)nvec * nchunks * n, c.stream);
+    double* tmp = c.scratch("sym4_tmp", (size_t)nvec * nchunks * n);
+    run_tile_contract(c, tree, make_kernel_params(k), units, "cov_matvec_tile", colpart);
+    TimedLaunch tl(c, "cov_matvec_colsum");
     dim3 g1((unsigned)ceil_div(n - 32 * t0, 256), (unsigned)nchunks, (unsigned)nvec);
-    k_colpart_chunks<<<g1, 256, 0, c.stream>>>(colpart.p, t0, t1, n, nvec, nchunks, tmp.p);
+    k_colpart_chunks<<<g1, 256, 0, c.stream>>>(colpart, t0, t1, n, nvec, nchunks, tmp);
     check_launch("k_colpart_chunks");
     dim3 g2((unsigned)ceil_div(n - 32 * t0, 256), (unsigned)nvec);
-    k_colpart_final<<<g2, 256, 0, c.stream>>>(tmp.p, 32 * t0, n, nchunks, b);
+    k_colpart_final<<<g2, 256, 0, c.stream>>>(tmp, 32 * t0, n, nchunks, b);
     check_launch("k_colpart_final");
     return;
   }

@@ -11,6 +11,7 @@
 // straight from global memory into registers at the start of each pass (each element once,
 // 32-byte row segments, one round trip per pass).  8 M^2 flops per (row, cell).
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -86,17 +87,24 @@ __global__ void __launch_bounds__(256, MLK_TR_MINB) k_transfer(const TransferJob
     // V_c only where a block with contracted-first cell c has rows (the S half is needed for
     // every row: the parents' sums); warp-uniform: a pass is one 64-row block
     const int64_t blk = (r_begin >> 6) + pass;
-    const int nt_use = (jb.vflag == nullptr || jb.vflag[blk]) ? NT : (M + 7) / 8;
+    const int nt_use = (jb.vflag == nullptr || jb.vflag[blk]) ? NT : (NT + 1) / 2;  // (NT + 1) / 2 = ceil(M / 8)
     double acc[NT][2];
 #pragma unroll
     for (int t = 0; t < NT; t++) acc[t][0] = acc[t][1] = 0.0;
+    // the tile count is a compile-time constant in each branch: a DMMA predicated off by a
+    // runtime test still occupies the pipe (the S-only passes, 96 % of the (row, cell) pairs at
+    // cfg4, ran 13 DMMA tiles for 7 useful ones: 71 % DMMA-active at 38 % of the FP64 peak, r02)
+    auto mm = [&](auto ntc) {
+      constexpr int NU = decltype(ntc)::value;
 #pragma unroll
-    for (int ks = 0; ks < KS; ks++) {
-      const double* bk = bp + 4 * ks * SQ;
+      for (int ks = 0; ks < KS; ks++) {
+        const double* bk = bp + 4 * ks * SQ;
 #pragma unroll
-      for (int t = 0; t < NT; t++)
-        if (t < nt_use) dmma_8x8x4(acc[t][0], acc[t][1], areg[ks], bk[8 * t]);
-    }
+        for (int t = 0; t < NU; t++) dmma_8x8x4(acc[t][0], acc[t][1], areg[ks], bk[8 * t]);
+      }
+    };
+    if (nt_use == NT) mm(std::integral_constant<int, NT>{});
+    else mm(std::integral_constant<int, (NT + 1) / 2>{});
     if (rok) {
 #pragma unroll
       for (int t = 0; t < NT; t++) {
