@@ -1,7 +1,7 @@
 #!/bin/bash
 # Full validation session: smoke, the whole GPU suite, default bench line (cfg4, with the oracle
-# baseline), cfg3 / cfg2 lines, ncu launch list of cfg4, ncu --set full of the nested K5a and of a
-# deep-level transfer launch.
+# baseline), cfg3 / cfg2 lines, the reference arm, and per config an ncu launch list plus one
+# ncu --set full capture of the dominant K5a launch (traffic + counters, tools/summarize_profiles.py).
 set -u
 TAG=${1:-r02final}
 OUT=gpurun_out
@@ -17,14 +17,14 @@ echo "bench_rc=$?" >> $OUT/bench_cfg4_$TAG.err
 timeout 900 python bench.py --config cfg3 > $OUT/bench_cfg3_$TAG.json 2> $OUT/bench_cfg3_$TAG.err
 timeout 900 python bench.py --config cfg2 > $OUT/bench_cfg2_$TAG.json 2> $OUT/bench_cfg2_$TAG.err
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/bench_ref_$TAG.json 2> $OUT/bench_ref_$TAG.err
-SHORT="python bench.py --steps 1 --warmup 1 --e2e-steps 0 --no-cpu-baseline --pcg-tol 0 --no-matvec-report --config cfg4"
-timeout 600 $SHORT > $OUT/short_$TAG.log 2>&1 && \
-  timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-    --log-file $OUT/launches_cfg4_$TAG.csv $SHORT > $OUT/ncu_launch_cfg4_$TAG.log 2>&1
-echo "ncu_launch_rc=$?" >> $OUT/short_$TAG.log
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_tile_contract -s 1 -c 1 \
-    -o $OUT/k5a_cfg4_$TAG -f $SHORT > $OUT/ncu_k5a_cfg4_$TAG.log 2>&1
-echo "ncu_k5a_rc=$?" >> $OUT/ncu_k5a_cfg4_$TAG.log
-timeout 900 ncu --set full --clock-control none -k regex:k_transfer -s 0 -c 1 \
-    -o $OUT/ktr_cfg4_$TAG -f $SHORT > $OUT/ncu_ktr_cfg4_$TAG.log 2>&1
-echo "ncu_ktr_rc=$?" >> $OUT/ncu_ktr_cfg4_$TAG.log
+for cfg in cfg4 cfg3 cfg2; do
+  SHORT="python bench.py --steps 1 --warmup 1 --e2e-steps 0 --no-cpu-baseline --pcg-tol 0 --no-matvec-report --config $cfg"
+  SKIP=1; [ $cfg = cfg2 ] && SKIP=0
+  timeout 600 $SHORT > $OUT/short_${cfg}_$TAG.log 2>&1 && \
+    timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+      --log-file $OUT/launches_${cfg}_$TAG.csv $SHORT > $OUT/ncu_launch_${cfg}_$TAG.log 2>&1
+  echo "ncu_launch_rc=$?" >> $OUT/short_${cfg}_$TAG.log
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_tile_contract -s $SKIP -c 1 \
+      -o $OUT/k5a_${cfg}_$TAG -f $SHORT > $OUT/ncu_k5a_${cfg}_$TAG.log 2>&1
+  echo "ncu_k5a_rc=$?" >> $OUT/ncu_k5a_${cfg}_$TAG.log
+done
