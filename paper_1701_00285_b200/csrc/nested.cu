@@ -28,7 +28,10 @@ constexpr int kTrRows = 64;       // rows per pass (8 warps x 8)
 constexpr int kTrMaxM2 = 144;     // 2M limit of the shared-memory kernel (M <= 72)
 // (a tiled variant with Q_c and double-buffered 64-row A tiles in shared memory, 8 warps as
 // 2 row halves x 4 column quarters, one CTA per SM, measured 1.75x slower on cfg4: 199 against
-// 114 ms, r02 tr2 -- the A tile went through shared memory once per column warp)
+// 114 ms, r02 tr2 -- the A tile went through shared memory once per column warp); so did a
+// variant with 16 warps, one CTA per SM and each warp's next-pass A rows staged by 8-byte
+// cp.async into its own shared buffer during the current pass's DMMAs (cfg4 97.1 vs 82.8 ms,
+// cfg3 16.5 vs 13.8 ms, bit-identical; r02 trasync): the load latency is not what limits it)
 
 struct TransferJob {
   const double* Sch;     // [S_cL S_cR], rows x 2M, row stride ld

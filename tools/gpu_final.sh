@@ -27,4 +27,8 @@ for cfg in cfg4 cfg3 cfg2; do
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_tile_contract -s $SKIP -c 1 \
       -o $OUT/k5a_${cfg}_$TAG -f $SHORT > $OUT/ncu_k5a_${cfg}_$TAG.log 2>&1
   echo "ncu_k5a_rc=$?" >> $OUT/ncu_k5a_${cfg}_$TAG.log
+  # gpurun copies back <= 64 MiB: keep the raw page as CSV, drop the report
+  ncu -i $OUT/k5a_${cfg}_$TAG.ncu-rep --page raw --csv > $OUT/k5a_${cfg}_$TAG.raw.csv 2>> $OUT/ncu_k5a_${cfg}_$TAG.log
+  rm -f $OUT/k5a_${cfg}_$TAG.ncu-rep
 done
+du -sh $OUT

@@ -66,7 +66,10 @@ def _sha():
 
 
 def k5a(rep, tag, note, cfg="cfg2"):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):  # the raw page exported on the GPU box (tools/gpu_final.sh)
+        raw = open(rep).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     h, u, v = rows[0], rows[1], rows[2]
     m = {a: (b, c) for a, b, c in zip(h, u, v)}
@@ -101,4 +104,7 @@ if __name__ == "__main__":
                       % (a.config, a.config))
     sfx = a.tag if a.config == "cfg2" else "%s_%s" % (a.config, a.tag)
     launches(os.path.join(ROOT, "gpurun_out", "launches_%s.csv" % sfx), a.tag, note, a.config)
-    k5a(os.path.join(ROOT, "gpurun_out", "k5a_%s.ncu-rep" % sfx), a.tag, note, a.config)
+    rep = os.path.join(ROOT, "gpurun_out", "k5a_%s.ncu-rep" % sfx)
+    if not os.path.exists(rep):
+        rep = os.path.join(ROOT, "gpurun_out", "k5a_%s.raw.csv" % sfx)
+    k5a(rep, a.tag, note, a.config)
