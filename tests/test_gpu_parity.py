@@ -70,6 +70,33 @@ def _block_errs(got, ref):
     return np.array(errs)
 
 
+_REF = {}
+
+
+def _oracle_bsr(X, o, ob, kern, pairs, key=None, fast=False):
+    """The oracle's BSR of the admitted pairs.  fast=True evaluates each block with the oracle's
+    plain-C direct-difference tile (oracle/fastcov.py block_streamed: the same definition
+    B_ab = W_a C(X_a, X_b) W_b^T, pinned in tests/test_oracle.py) instead of the NumPy tile --
+    the n >= 4096 shapes otherwise spend minutes of host time per case.  `key` caches the result
+    for the other parametrisations of the same inputs (two entries kept)."""
+    if key is not None and key in _REF:
+        return _REF[key]
+    if fast:
+        from oracle import fastcov as F
+        cells, row_off, brow_ptr, bcol, val_off = OAs.bsr_structure(ob, pairs)
+        values = np.zeros(int(val_off[-1]))
+        for k, (a, b) in enumerate(pairs):
+            values[val_off[k]:val_off[k + 1]] = F.block_streamed(X, o, ob, kern, a, b).ravel()
+        ref = OAs.BSR(cells, row_off, brow_ptr, bcol, val_off, values)
+    else:
+        ref = OAs.assemble(X, o, ob, kern, pairs)
+    if key is not None:
+        while len(_REF) >= 2:
+            _REF.pop(next(iter(_REF)))
+        _REF[key] = ref
+    return ref
+
+
 # --------------------------------------------------------------------------------- tree
 @pytest.mark.parametrize("n,d,leaf,kind,points", [
     (1024, 2, 32, 0, "uniform"),       # cfg1 shape (kD)
@@ -189,7 +216,7 @@ def test_assembly_fp64_parity(mlk, ctx, fam, rho, n, d, w, leaf, kind, mode, tau
     ob = OB.build_basis(X, o, w)
     kern = dict(family=fam, rho=rho, sigma2=1.3, nugget=1e-3 if fam == OC.GAUSSIAN else 0.0)
     pairs = OA.admitted_pairs(X, o, ob, mode, tau)
-    ref = OAs.assemble(X, o, ob, kern, pairs)
+    ref = _oracle_bsr(X, o, ob, kern, pairs, fast=n >= 4096)
     cw = mlk.assemble_cw(ctx, g, gb, kern, dict(mode=mode, tau=tau))
     got = cw.export()
     assert np.array_equal(got["val_off"], ref.val_off)
@@ -219,7 +246,9 @@ def test_nested_and_direct_assembly(mlk, ctx, monkeypatch, mode, n, d, w, leaf, 
     ob = OB.build_basis(X, o, w)
     kern = dict(family=fam, rho=rho, sigma2=1.1, nugget=1e-4 if fam == OC.GAUSSIAN else 0.0)
     pairs = OA.admitted_pairs(X, o, ob, mode_pairs, tau)
-    ref = OAs.assemble(X, o, ob, kern, pairs)
+    # one oracle reference for both plans (and for test_assembly_cfg4_shape_parity)
+    ref = _oracle_bsr(X, o, ob, kern, pairs, key=(n, d, w, leaf, kind, fam, rho, mode_pairs, tau, points),
+                      fast=n >= 8192)
     cw = mlk.assemble_cw(ctx, g, gb, kern, dict(mode=mode_pairs, tau=tau))
     assert cw.plan()["nested"] == (mode == "nested")
     got = cw.export()
@@ -242,9 +271,12 @@ def test_assembly_cfg4_shape_parity(mlk, ctx):
     g, o = _tree_both(mlk, ctx, X, 512, 1, dirs)
     gb = mlk.build_basis(ctx, g, 1)
     ob = OB.build_basis(X, o, 1)
-    kern = dict(family=OC.MATERN_12, rho=3.0)
+    kern = dict(family=OC.MATERN_12, rho=3.0, sigma2=1.1, nugget=0.0)
     pairs = OA.admitted_pairs(X, o, ob, 1, 1e-7)
-    ref = OAs.assemble(X, o, ob, kern, pairs)
+    # the plan the cost model picks, against the reference of test_nested_and_direct_assembly's
+    # cfg4-shape case (same inputs and kernel)
+    ref = _oracle_bsr(X, o, ob, kern, pairs, key=(8192, 50, 1, 512, 1, OC.MATERN_12, 3.0, 1, 1e-7, "mixture"),
+                      fast=True)
     got = mlk.assemble_cw(ctx, g, gb, kern, dict(mode=1, tau=1e-7)).export()
     assert np.array_equal(got["val_off"], ref.val_off)
     assert _block_errs(got["values"], ref).max() <= TOL_BLOCK
@@ -303,7 +335,6 @@ def _full(name):
             pairs = [tuple(int(v) for v in p) for p in np.load(gp)["pairs"]]
         else:
             pairs = OA.admitted_pairs(X, o, ob, c["pairs"], c["tau"])
-        _FULL.clear()   # one config at a time (host memory)
         _FULL[name] = (inp, c, X, o, ob, pairs)
     return _FULL[name]
 
@@ -430,7 +461,7 @@ def test_cfg5_shape_mini(mlk, ctx):
         assert np.linalg.norm(Wg - ob.W[q]) <= TOL_BLOCK * np.linalg.norm(ob.W[q])
     kern = wl.kernel_dict(c)
     pairs = OA.admitted_pairs(X, o, ob, c["pairs"], c["tau"])
-    ref = OAs.assemble(X, o, ob, kern, pairs)
+    ref = _oracle_bsr(X, o, ob, kern, pairs, fast=True)
     got = mlk.assemble_cw(ctx, g, gb, kern, dict(mode=c["pairs"], tau=c["tau"])).export()
     assert np.array_equal(got["val_off"], ref.val_off) and np.array_equal(got["bcol"], ref.bcol)
     assert _block_errs(got["values"], ref).max() <= TOL_BLOCK
@@ -778,6 +809,7 @@ def test_rank_share_blocks_from_pieces(mlk, ctx):
     """One rank's share of an R-rank assembly, checked without the all-gather (what
     tools/cfg5_share.py does at full cfg5 size): every block whose pieces this rank owns equals
     the sum of its pieces in the rank's shard, and matches the oracle within 1e-11."""
+    from oracle import fastcov as F
     X, dirs = _setup(16384, 10, 256, 1)
     kern = dict(family=OC.MATERN_32, rho=1.0)
     sp = dict(mode=1, tau=1e-6)
@@ -802,7 +834,7 @@ def test_rank_share_blocks_from_pieces(mlk, ctx):
         for i in range(pp[k], pp[k + 1]):
             got = got + shard[po[i]:po[i] + ln]
         a, b = pairs[k]
-        ref = OAs.block(X, o, ob, kern, a, b).ravel()
+        ref = F.block_streamed(X, o, ob, kern, a, b).ravel()   # the oracle's plain-C tile
         assert np.linalg.norm(got - ref) <= TOL_BLOCK * np.linalg.norm(ref), (a, b)
         checked += 1
     assert checked >= 0.1 * len(pairs) / R
