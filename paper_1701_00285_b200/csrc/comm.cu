@@ -167,9 +167,13 @@ void gather_values(Ctx& c, mlk_cw_s* cw, const double* full) {
   const int64_t nb = cw->n_blocks;
   std::vector<int64_t> blen(nb);
   for (int64_t k = 0; k < nb; k++) blen[k] = cw->val_off[k + 1] - cw->val_off[k];
-  // staging (receive buffer): an eighth of the scratch budget, at least 512 KB
+  // staging (receive buffer): 1/32 of the device's total memory (5.6 GB on a B200), at least
+  // 512 KB.  The group plan must be the SAME on every rank (each group is one ncclAllGather of a
+  // common count), so the budget may depend only on quantities all ranks share -- not on
+  // scratch_budget_bytes(), which follows the rank's own free memory and live handles (its shard
+  // length differs from rank to rank).
   // (MLK_GATHER_BUDGET: doubles, diagnostics / tests -- many small groups)
-  int64_t budget = std::max<int64_t>(c.scratch_budget_bytes() / 8 / (int64_t)sizeof(double), (int64_t)1 << 16);
+  int64_t budget = std::max<int64_t>(device_total_bytes(c.device) / 32 / (int64_t)sizeof(double), (int64_t)1 << 16);
   if (const char* e = std::getenv("MLK_GATHER_BUDGET")) budget = std::max<int64_t>(1, std::atoll(e));
   std::vector<int64_t> gptr, glo, gcnt;
   gather_plan(nb, cw->piece_ptr.data(), cw->piece_off.data(), cw->piece_owner.data(), blen.data(), c.nranks, budget,

@@ -630,6 +630,41 @@ def test_multirank_emulated_bit_identical(mlk, ctx, R, monkeypatch):
         assert np.array_equal(cw.export()["values"], ref)
 
 
+@pytest.mark.parametrize("R", [2, 5])
+def test_multirank_nested_plan(mlk, ctx, R, monkeypatch):
+    """The nested plan (what bench.py's cfg4 / cfg3 runs take) sharded over R ranks: contexts of
+    R ranks on one GPU, one after another; the gathered values equal the single-rank nested
+    values bit for bit (pieces are per 4096-row chunk and reduced in chunk order whatever the
+    owner), every rank has work, and the shares' flops add up to the job's."""
+    import torch
+    monkeypatch.setenv("MLK_ASSEMBLY", "nested")
+    X, dirs = _setup(16384, 20, 256, 1, "normal")
+    kern = dict(family=OC.MATERN_52, rho=2.0)
+    sp = dict(mode=1, tau=1e-7)
+    g = mlk.build_tree(ctx, X, 256, 1, dirs)
+    gb = mlk.build_basis(ctx, g, 1)
+    cw1 = mlk.assemble_cw(ctx, g, gb, kern, sp)
+    assert cw1.plan()["nested"]
+    ref = cw1.export()["values"]
+    ctxs = [mlk.Ctx(0, R, r) for r in range(R)]
+    trees = [mlk.build_tree(c, X, 256, 1, dirs) for c in ctxs]
+    bases = [mlk.build_basis(c, t, 1) for c, t in zip(ctxs, trees)]
+    cws = [mlk.assemble_cw(c, t, b, kern, sp) for c, t, b in zip(ctxs, trees, bases)]
+    assert all(cw.plan()["nested"] for cw in cws)
+    assert all(cw.own_flops > 0 for cw in cws)
+    assert abs(sum(cw.own_flops for cw in cws) - cws[0].flops) < 1e-6 * cws[0].flops
+    mx = max(cw.shard_len()[1] for cw in cws)
+    shards = []
+    for c, cw in zip(ctxs, cws):
+        buf = torch.empty(max(mx, 1), dtype=torch.float64, device="cuda")
+        mlk.pack_cw(c, cw, buf)
+        shards.append(buf)
+    gathered = torch.cat(shards)
+    for c, cw in zip(ctxs, cws):
+        mlk.unpack_cw(c, cw, gathered)
+        assert np.array_equal(cw.export()["values"], ref)
+
+
 def test_library_nccl_communicator_world1(mlk, ctx):
     """A context with its own NCCL communicator (mlk_ctx_create with a unique id; one rank on
     this one-GPU box): the library runs ncclAllReduce on C_W v itself, and assembly (gather mode),
