@@ -281,26 +281,32 @@ void apply_w_dev(Ctx& c, const mlk_tree_s* tree, const mlk_basis_s* B, const dou
   }
 }
 
-// Symmetric C a column partials: tile I (of this rank's t0..t1-1) holds nvec rows of n - 32 I
-// columns starting at column 32 I (its 4 warps already summed in order by the tile kernel), at
-// offset nvec sum_{I' < I} (n - 32 I').  Two fixed-order levels: tmp[l][c][j] = sum over the
-// tiles of chunk c (kColChunk tiles), then b[l][j] += sum over chunks c in order.  Deterministic.
+// Symmetric C a column partials.  This rank's tiles are I_m = r + R m, m = 0 .. T_r - 1 (cyclic
+// over the nranks = R ranks: every rank gets the same mix of long and short triangular tasks, so
+// its waves fill like the single-rank run's; contiguous tile ranges of equal cost left rank 0
+// with ~T/16 full-length tasks -- less than one wave -- and 30 against 21 ms at cfg4 / 8 ranks).
+// Tile I_m holds nvec rows of n - 32 I_m columns starting at column 32 I_m (its 4 warps already
+// summed in order by the tile kernel), at offset nvec sum_{m' < m} (n - 32 I_m').  Two
+// fixed-order levels: tmp[l][c][j] = sum over the tiles of chunk c (kColChunk tiles), then
+// b[l][j] += sum over chunks c in order.  Deterministic; R = 1 is the plain tile order.
 constexpr int kColChunk = 64;
-__device__ __forceinline__ int64_t colpart_off(int64_t I, int64_t t0, int64_t n, int nvec) {
-  return (int64_t)nvec * ((I - t0) * n - 16 * (I * (I - 1) - t0 * (t0 - 1)));
+__device__ __forceinline__ int64_t colpart_off(int64_t m, int64_t r, int64_t R, int64_t n, int nvec) {
+  return (int64_t)nvec * (m * n - 32 * (r * m + R * (m * (m - 1) / 2)));
 }
 
-__global__ void k_colpart_chunks(const double* __restrict__ colpart, int64_t t0, int64_t t1, int64_t n, int nvec,
-                                 int nchunks, double* __restrict__ tmp) {
-  const int64_t j = 32 * t0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+__global__ void k_colpart_chunks(const double* __restrict__ colpart, int64_t r, int64_t R, int64_t Tr, int64_t n,
+                                 int nvec, int nchunks, double* __restrict__ tmp) {
+  const int64_t j = 32 * r + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int c = blockIdx.y, l = blockIdx.z;
   if (j >= n) return;
-  const int64_t i0 = t0 + (int64_t)c * kColChunk;
-  const int64_t i1 = std::min<int64_t>({t1, i0 + kColChunk, j / 32 + 1});
+  const int64_t m0 = (int64_t)c * kColChunk;
+  // tiles that reach column j: 32 I_m <= j
+  const int64_t m1 = std::min<int64_t>({Tr, m0 + kColChunk, (j / 32 - r) / R + 1});
   double s = 0.0;
-  for (int64_t I = i0; I < i1; I++) {
+  for (int64_t m = m0; m < m1; m++) {
+    const int64_t I = r + R * m;
     const int64_t w = n - 32 * I;
-    s += colpart[colpart_off(I, t0, n, nvec) + (int64_t)l * w + (j - 32 * I)];
+    s += colpart[colpart_off(m, r, R, n, nvec) + (int64_t)l * w + (j - 32 * I)];
   }
   tmp[((int64_t)l * nchunks + c) * n + j] = s;
 }
@@ -322,21 +328,14 @@ __global__ void k_colpart_final(const double* __restrict__ tmp, int64_t j0, int6
 void cov_matvec_dev(Ctx& c, const mlk_tree_s* tree, const mlk_kernel& k, const double* a, double* b, int nvec) {
   const int64_t n = tree->n;
   CUDA_CHECK(cudaMemsetAsync(b, 0, sizeof(double) * nvec * n, c.stream));
-  // rows of this rank: a contiguous range of 32-row tiles (for the symmetric kernel balanced by
-  // the triangular task costs n - 32 I)
+  // rows of this rank: 32-row tiles, cyclic over the ranks for the symmetric kernel (tile I belongs
+  // to rank I mod nranks), a contiguous range for the row-panel kernel
   const int64_t tiles = ceil_div(n, 32);
-  auto sym_range = [&](int r, int64_t& a0, int64_t& a1) {
-    auto cost_before = [&](int64_t I) { return (double)I * n - 16.0 * I * (I - 1); };
-    const double total = cost_before(tiles);
-    a0 = 0;
-    while (a0 < tiles && cost_before(a0 + 1) <= total * r / c.nranks) a0++;
-    a1 = a0;
-    while (a1 < tiles && cost_before(a1 + 1) <= total * (r + 1) / c.nranks) a1++;
-    if (r == c.nranks - 1) a1 = tiles;
-  };
-  auto sym_partials = [&](int64_t a0, int64_t a1) {
+  const int64_t R = c.nranks;
+  auto sym_count = [&](int64_t r) { return tiles > r ? (tiles - r + R - 1) / R : (int64_t)0; };
+  auto sym_partials = [&](int64_t r) {
     int64_t s = 0;
-    for (int64_t I = a0; I < a1; I++) s += (int64_t)nvec * (n - 32 * I);
+    for (int64_t m = 0; m < sym_count(r); m++) s += (int64_t)nvec * (n - 32 * (r + R * m));
     return s;
   };
   // The symmetric and the row-panel kernels split the rows differently, so every rank must take
@@ -368,48 +367,42 @@ void cov_matvec_dev(Ctx& c, const mlk_tree_s* tree, const mlk_kernel& k, const d
   bool sym = nvec <= 4 && !nosym;
   if (sym) {
     int64_t worst = 0;
-    for (int r = 0; r < c.nranks; r++) {
-      int64_t a0, a1;
-      sym_range(r, a0, a1);
-      worst = std::max(worst, sym_partials(a0, a1));
-    }
+    for (int r = 0; r < c.nranks; r++) worst = std::max(worst, sym_partials(r));
     sym = worst * (int64_t)sizeof(double) <= device_total_bytes(c.device) / 4;
   }
-  int64_t t0 = tiles * c.rank / c.nranks, t1 = tiles * (c.rank + 1) / c.nranks;
-  int64_t cp = 0;
-  if (sym) {
-    sym_range(c.rank, t0, t1);
-    cp = sym_partials(t0, t1);
-  }
-  if (t1 <= t0) return;
   const int nv = nvec == 1 ? 1 : nvec == 2 ? 2 : 4;
   std::vector<TileUnit> units;
   if (sym) {
+    const int64_t r = c.rank, Tr = sym_count(r);
+    if (Tr == 0) return;
+    const int64_t cp = sym_partials(r);
     int64_t off = 0;
-    for (int64_t I = t0; I < t1; I++) {
-      const int64_t r = 32 * I;
-      make_tile_units(units, r, (int32_t)std::min<int64_t>(32, n - r), r, (int32_t)(n - r), a, n, nvec, b + r, n, 1,
-                      tree->d_pad);
+    for (int64_t m = 0; m < Tr; m++) {
+      const int64_t row = 32 * (r + R * m);
+      make_tile_units(units, row, (int32_t)std::min<int64_t>(32, n - row), row, (int32_t)(n - row), a, n, nvec,
+                      b + row, n, 1, tree->d_pad);
       TileUnit& u = units.back();
       u.rq = -nv;
-      u.w_col0 = r;
+      u.w_col0 = row;
       u.w_cols = n;
       u.cp_off = off;
-      off += (int64_t)nvec * (n - r);
+      off += (int64_t)nvec * (n - row);
     }
     double* colpart = c.scratch("sym4_colpart", (size_t)cp);
-    const int nchunks = (int)ceil_div(t1 - t0, kColChunk);
+    const int nchunks = (int)ceil_div(Tr, (int64_t)kColChunk);
     double* tmp = c.scratch("sym4_tmp", (size_t)nvec * nchunks * n);
     run_tile_contract(c, tree, make_kernel_params(k), units, "cov_matvec_tile", colpart);
     TimedLaunch tl(c, "cov_matvec_colsum");
-    dim3 g1((unsigned)ceil_div(n - 32 * t0, 256), (unsigned)nchunks, (unsigned)nvec);
-    k_colpart_chunks<<<g1, 256, 0, c.stream>>>(colpart, t0, t1, n, nvec, nchunks, tmp);
+    dim3 g1((unsigned)ceil_div(n - 32 * r, 256), (unsigned)nchunks, (unsigned)nvec);
+    k_colpart_chunks<<<g1, 256, 0, c.stream>>>(colpart, r, R, Tr, n, nvec, nchunks, tmp);
     check_launch("k_colpart_chunks");
-    dim3 g2((unsigned)ceil_div(n - 32 * t0, 256), (unsigned)nvec);
-    k_colpart_final<<<g2, 256, 0, c.stream>>>(tmp, 32 * t0, n, nchunks, b);
+    dim3 g2((unsigned)ceil_div(n - 32 * r, 256), (unsigned)nvec);
+    k_colpart_final<<<g2, 256, 0, c.stream>>>(tmp, 32 * r, n, nchunks, b);
     check_launch("k_colpart_final");
     return;
   }
+  const int64_t t0 = tiles * c.rank / c.nranks, t1 = tiles * (c.rank + 1) / c.nranks;
+  if (t1 <= t0) return;
   const int64_t r0 = t0 * 32, r1 = std::min<int64_t>(n, t1 * 32);
   // rows r0..r1 as an a range; b range = all points; W_b = the vectors a (nvec x n)
   make_tile_units(units, r0, (int32_t)(r1 - r0), 0, (int32_t)n, a, n, nvec, b + r0, n, 1, tree->d_pad);
