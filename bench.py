@@ -589,7 +589,8 @@ def main():
         line = {
             "metric": METRIC,
             "value": value, "unit": "covariance pairs/s", "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "steps_ms": [round(x, 2) for x in step_ms],
+            "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_dict(args.config, ws),
             "fp64": {"assembly_flops_per_step": flops, "tflops_step": flops / (ms_per_step * 1e-3) / 1e12,
                      "tflops_assembly": flops / (asm_ms * 1e-3) / 1e12 if asm_ms > 0 else None,

@@ -141,6 +141,9 @@ struct mlk_cw_s {
 };
 
 namespace mlk {
+// free device memory at the context's first query less the live handles since (ctx.cu): no
+// driver call after the first -- cudaMemGetInfo stalls under NVML polling
+int64_t ctx_avail_bytes(Ctx& c);
 // nested-assembly transfers of one tree level (nested.cu): jobs {[S_cL S_cR], Q_c, S_c (or
 // nullptr), V_c}, rows x (n_nodes M) buffers with row stride ld, and per job a device flag per
 // 64-row block (V_c needed there; nullptr: everywhere); transfer_kernel_ok(M): 2M <= 144

@@ -815,6 +815,19 @@ mlk_status mlk_build_basis_ex(mlk_ctx ctx, mlk_tree tree, int32_t index_set, int
   MLK_API_BEGIN
   MLK_REQUIRE(ctx && tree && out, "NULL argument");
   *out = nullptr;
+  // MLK_SLOW_MS=<ms>: report host phases of this call that took longer (diagnostics)
+  struct SlowMark {
+    double thr;
+    std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
+    SlowMark() : thr(std::getenv("MLK_SLOW_MS") ? std::atof(std::getenv("MLK_SLOW_MS")) : -1.0) {}
+    void operator()(const char* what) {
+      if (thr < 0) return;
+      auto now = std::chrono::steady_clock::now();
+      const double ms = std::chrono::duration<double, std::milli>(now - last).count();
+      if (ms >= thr) std::fprintf(stderr, "[mlk slow] basis.%s %.1f ms\n", what, ms);
+      last = now;
+    }
+  } slow;
   MLK_REQUIRE(index_set >= MLK_INDEX_TD && index_set <= MLK_INDEX_TP, "unknown index set");
   MLK_REQUIRE(w >= 0 && w <= 64, "need 0 <= w <= 64");
   MLK_REQUIRE((flags & ~(MLK_BASIS_KEEP_DEFICIENT | MLK_BASIS_DROP_PHI)) == 0, "unknown basis flags");
@@ -870,16 +883,17 @@ mlk_status mlk_build_basis_ex(mlk_ctx ctx, mlk_tree tree, int32_t index_set, int
     }
   }
   B->dim = row;
+  slow("setup");
   B->W.alloc(std::max<int64_t>(woff, 1), st);
+  slow("W.alloc");
   // Phi blocks of every node cost M x n doubles per level (cfg5: 111 GB next to 106 GB of W).
   // They are kept (for mlk_basis_export) only when W + Phi fit in half of the free memory or
   // MLK_BASIS_DROP_PHI is not set; otherwise the construction keeps the leaves' Phi and two
   // alternating level buffers (node q at M begin[q]) and retains only L = Phi_root.
   bool drop_phi = (flags & MLK_BASIS_DROP_PHI) != 0;
   if (!drop_phi && (woff + phioff) * (int64_t)sizeof(double) > ((int64_t)1 << 30)) {
-    size_t freeb = 0, totalb = 0;
-    CUDA_CHECK(cudaMemGetInfo(&freeb, &totalb));
-    drop_phi = phioff * (int64_t)sizeof(double) > (int64_t)freeb / 2;
+    // (the context's estimate, not cudaMemGetInfo: a driver query per call stalls under NVML polling)
+    drop_phi = phioff * (int64_t)sizeof(double) > std::max<int64_t>(ctx_avail_bytes(c), 0) / 2;
   }
   B->phi_dropped = drop_phi;
   const int64_t mn = (int64_t)M * tree->n;
@@ -896,7 +910,9 @@ mlk_status mlk_build_basis_ex(mlk_ctx ctx, mlk_tree tree, int32_t index_set, int
     if (tree->state[q] == 1) return leafphi.p + (int64_t)M * tree->begin[q];
     return lvlphi[tree->depth[q] & 1].p + (int64_t)M * tree->begin[q];
   };
+  slow("Phi.alloc");
   DevBuf<double> Rbuf((size_t)nn * M * M, st);
+  slow("Rbuf.alloc");
   DevBuf<int> flag(1, st);
   flag.zero();
 
@@ -908,6 +924,7 @@ mlk_status mlk_build_basis_ex(mlk_ctx ctx, mlk_tree tree, int32_t index_set, int
   DevBuf<int32_t> facd(fh.size(), st);
   facd.upload(fh);
 
+  slow("facd");
   HostTrace trace("basis");
   // ---- leaves
   {
@@ -951,6 +968,7 @@ mlk_status mlk_build_basis_ex(mlk_ctx ctx, mlk_tree tree, int32_t index_set, int
     run_qr(c, qj, M, flag.p, "basis_leaf_qr");
   }
   trace.mark("leaves");
+  slow("leaves");
   {
     auto fl = flag.download(1);
     if (fl[0] && !(flags & MLK_BASIS_KEEP_DEFICIENT))
@@ -958,6 +976,7 @@ mlk_status mlk_build_basis_ex(mlk_ctx ctx, mlk_tree tree, int32_t index_set, int
   }
   B->keep_deficient = (flags & MLK_BASIS_KEEP_DEFICIENT) != 0;
   trace.mark("leaf_check");
+  slow("leaf_check");
   // ---- internal levels, bottom-up, on the auxiliary stream: the call returns while they run
   // ([R_L; R_R] has full column rank whenever R_L does, so the synchronous leaf check above is
   // the one that can fail; merge_flag re-checks numerically when the basis is first used)
@@ -1066,6 +1085,7 @@ mlk_status mlk_build_basis_ex(mlk_ctx ctx, mlk_tree tree, int32_t index_set, int
     }
   }
   trace.mark("levels");
+  slow("levels");
   if (drop_phi) {
     // L = Phi_root: the root's level buffer (or the leaf buffer when the root is a leaf)
     B->Phi = std::move(tree->state[0] == 1 ? leafphi : lvlphi[0]);

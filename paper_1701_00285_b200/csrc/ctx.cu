@@ -110,16 +110,23 @@ void upload_async(void* dst, const void* src, size_t bytes, cudaStream_t s) {
 
 std::atomic<int64_t> g_live_bytes{0};
 
-int64_t Ctx::scratch_budget_bytes() {
-  if (free_at_first_use < 0) {
+// What was free at the context's first query, less what live handles (W, BSR values, shards,
+// scratch) have taken since.  cudaMemGetInfo itself runs once per context: under NVML polling
+// (the bench's clock sampler, nvidia-smi on the box) a call stalled the host by up to 500 ms,
+// and one call per mlk_build_basis made cfg4 steps of 830 ms take up to 1330 ms (r02 spk).
+int64_t ctx_avail_bytes(Ctx& c) {
+  if (c.free_at_first_use < 0) {
     size_t freeb = 0, totalb = 0;
     CUDA_CHECK(cudaMemGetInfo(&freeb, &totalb));
-    free_at_first_use = (int64_t)freeb;
-    live_at_first_use = g_live_bytes.load();
+    c.free_at_first_use = (int64_t)freeb;
+    c.live_at_first_use = g_live_bytes.load();
   }
-  // a third of what was free at first use, less what live handles (W, BSR values, shards)
-  // have taken since; at least 256 MB so small problems never starve
-  const int64_t avail = free_at_first_use - (g_live_bytes.load() - live_at_first_use);
+  return c.free_at_first_use - (g_live_bytes.load() - c.live_at_first_use);
+}
+
+int64_t Ctx::scratch_budget_bytes() {
+  // a third of what is available, at least 256 MB so small problems never starve
+  const int64_t avail = ctx_avail_bytes(*this);
   static const int64_t forced = [] {
     const char* e = std::getenv("MLK_SCRATCH_BUDGET_MB");  // diagnostics: force small batches
     return e ? (int64_t)std::atoll(e) << 20 : (int64_t)0;
@@ -229,6 +236,17 @@ mlk_status mlk_ctx_create(int device, int nranks, int rank, const void* nccl_uni
     CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t thr = UINT64_MAX;
     CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    // Reuse of a block freed on another stream (the auxiliary stream of the basis merges, stream 0
+    // of the handle frees) must not depend on whether that free happens to have completed when the
+    // allocation is requested ("opportunistic" reuse): when it had not, the allocator took other
+    // blocks, a later large request (cfg4: the 13.7 GB S / V buffers, the 1 GB W) found no block
+    // and the pool grew -- 150-600 ms of driver time in ~1 step of 5 (cfg4 steps of 830 ms
+    // measured 970-1470 ms, r02 spk; MLK_SLOW_MS showed the stalls inside cudaMallocAsync).
+    // With internal dependencies only, every step takes the same blocks.
+    if (std::getenv("MLK_POOL_OPPORTUNISTIC") == nullptr) {
+      int off = 0;
+      CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowOpportunistic, &off));
+    }
   }
   auto* h = new mlk_ctx_s();
   h->c.device = device;
