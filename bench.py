@@ -295,13 +295,18 @@ def run_reference(args):
         sampler.sample(min(3.0, args.ref_budget), seed_tag=100 + w, min_blocks=1)
     vals = []
     desc = cores = None
+    step_s = []
     for s in range(args.steps):
+        t0 = time.perf_counter()
         v, desc, cores = sampler.sample(args.ref_budget, seed_tag=s + 1)
+        step_s.append(time.perf_counter() - t0)
         vals.append(v)
     value = float(np.mean(vals))
     line = {
         "impl": "reference", "metric": METRIC, "value": value,
         "unit": "covariance pairs/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        # one step = one bounded sample of the workload (host wall clock; no GPU work in this arm)
+        "ms_per_step": 1e3 * float(np.mean(step_s)), "scaling": "weak", "gpu_launches": 0,
         "higher_is_better": True, "dtype": "f64", "data": "synthetic", "config": config_dict(args.config, ws),
         "cpu_baseline": {"value": value, "unit": "covariance pairs/s", "cores": cores, "kind": "oracle",
                          "sample": desc},
