@@ -35,3 +35,20 @@ def test_single_rank_default_and_mismatch_rejected():
     assert rc == 0 and out[0]["n_gpus"] == 1
     rc, out, _ = _run(["--gpus", "4", "--dry-run"], env={"WORLD_SIZE": "2", "RANK": "0", "LOCAL_RANK": "0"})
     assert rc == 2 and "error" in out[0]
+
+
+def test_reference_arm_line_has_the_contract_keys():
+    """`--impl reference` times the oracle on host cores and prints the base contract's line plus
+    `impl`, `cpu_baseline` and a zero-copy `e2e` (no GPU work: gpu_launches 0)."""
+    rc, out, err = _run(["--impl", "reference", "--steps", "1", "--warmup", "0", "--config", "cfg2",
+                         "--ref-budget", "0.5"])
+    assert rc == 0, err
+    line = out[-1]
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "dtype", "data", "config", "cpu_baseline", "e2e", "vs_baseline"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["gpu_launches"] == 0 and line["n_gpus"] == 1
+    assert line["value"] > 0 and line["ms_per_step"] > 0 and line["cpu_baseline"]["kind"] == "oracle"
+    assert line["e2e"] == {"value": line["value"], "unit": line["unit"], "h2d_bytes_per_step": 0,
+                           "d2h_bytes_per_step": 0}
+    assert line["config"]["workload"] == "cfg2"
